@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark: fused MP-LARS step time + all-reduce bus bandwidth on ResNet-50
+gradients (BASELINE.json), 1..8 B200, one process per GPU.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our arm
+  python bench.py --impl reference [...]                   # the reference's
+                                                           # CPU path (oracle)
+
+One step = pack the rank's 161 fp16 gradient tensors into theta-buckets ->
+all-reduce every bucket over NCCL (N > 1) -> pass 1 (mean, overflow flags,
+unscale, fp64 segment norms) -> trust ratios -> pass 2 (momentum / master /
+working-copy update) -> read the flags (the one host sync).  Inputs are
+resident in HBM; L2 is flushed (256 MiB written) before every timed step and
+each step is timed alone with CUDA events on the launching stream; the value
+is the mean step time, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fused MP-LARS step time (ms) + allreduce bus GB/s, ResNet-50 grads, 1/2/4/8 B200"
+PIECE = "pass2"   # dominant kernel for the roofline line
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
+    ap.add_argument("--algorithm", default="ring", choices=["ring", "hierarchical", "sharded"])
+    ap.add_argument("--group-size", type=int, default=4, help="k of Topology(p, k)")
+    ap.add_argument("--eta-bytes", type=int, default=None,
+                    help="hybrid threshold; default: 0 for ring, inf otherwise")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-allreduce-sweep", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+
+def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, warmup: int,
+                  budget_s: float = 150.0) -> dict:
+    """The reference's CPU implementation of the path (the oracle port of
+    pkg/src/gradsync composed per SURVEY.md §8a-14), p workers simulated in one
+    process as the reference does, on this host's cores."""
+    import numpy as np
+    from oracle import reference_port as rp
+    from paper_1807_11205_b200 import shapes as sh
+
+    specs = sh.load_shapes(model)
+    names = [s.name for s in specs]
+    sizes = [s.numel for s in specs]
+    order = list(reversed(range(len(specs))))
+    master = sh.synth_master(specs, seed=0)
+    groups, o = [], 0
+    for s in specs:
+        w = master[o:o + s.numel].copy()
+        groups.append(rp.Group(s.name, s.kind, w, np.zeros(s.numel, np.float32),
+                               np.zeros(s.numel, np.float32), rp.narrow(w)))
+        o += s.numel
+    wires = []
+    for r in range(p):
+        flat = sh.synth_wire_grads(specs, rank=r, seed=0)
+        parts, o = [], 0
+        for s in specs:
+            parts.append(flat[o:o + s.numel])
+            o += s.numel
+        wires.append(parts)
+    hp = rp.LarsHyper(0.001, 0.0, 5e-4, 0.9)
+    threads = rp.default_threads()
+    # first (untimed) step sizes the sample
+    t0 = time.perf_counter()
+    rp.compose_step_fp16(wires, names, sizes, order, groups, hp, 0.1,
+                         rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
+    t_full = time.perf_counter() - t0
+    total = steps + max(0, warmup - 1)
+    frac = 1.0
+    if t_full * total > budget_s:
+        frac = max(0.02, budget_s / (t_full * total))
+    # sample = the first `frac` of the wire (backward order), whole tensors
+    if frac < 1.0:
+        keep, acc, target = [], 0, frac * sum(sizes)
+        for i in order:
+            if acc >= target:
+                break
+            keep.append(i)
+            acc += sizes[i]
+        frac = acc / sum(sizes)
+        sub = sorted(keep)
+        remap = {old: new for new, old in enumerate(sub)}
+        s_names = [names[i] for i in sub]
+        s_sizes = [sizes[i] for i in sub]
+        s_groups = [groups[i] for i in sub]
+        s_wires = [[w[i] for i in sub] for w in wires]
+        s_order = [remap[i] for i in order if i in remap]
+    else:
+        s_names, s_sizes, s_groups, s_wires, s_order = names, sizes, groups, wires, order
+    for _ in range(max(0, warmup - 1)):
+        rp.compose_step_fp16(s_wires, s_names, s_sizes, s_order, s_groups, hp, 0.1,
+                             rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rp.compose_step_fp16(s_wires, s_names, s_sizes, s_order, s_groups, hp, 0.1,
+                             rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
+        times.append((time.perf_counter() - t0) / frac)
+    ms = 1e3 * statistics.mean(times)
+    return {"ms": ms, "threads": threads, "frac": frac, "t_full_s": t_full,
+            "sample": (f"{model} p={p} theta={theta}: "
+                       + ("full workload" if frac == 1.0 else
+                          f"first {frac:.3f} of the parameters (wire order), time scaled by 1/frac")
+                       + f", {steps} timed steps")}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    eta = args.eta_bytes if args.eta_bytes is not None else (0 if args.algorithm == "ring" else 1 << 62)
+    r = cpu_reference(args.model, world, args.theta, eta, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.model} fused MP-LARS step, fp16 wire, CPU oracle port",
+                   "params": None, "theta": args.theta, "p": world,
+                   "parallelism": f"dp{world} simulated in one process"},
+        "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": r["threads"],
+                         "kind": "port", "sample": r["sample"]},
+        "e2e": {"value": round(r["ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank: int, world: int, local: int) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_11205_b200 as gs
+    from paper_1807_11205_b200 import _native, shapes as sh
+    from paper_1807_11205_b200.dist import Communicator
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    specs = sh.load_shapes(args.model)
+    n_params = sh.total_params(specs)
+    comm = None
+    if world > 1:
+        k = args.group_size if args.algorithm != "ring" else 1
+        comm = Communicator(gs.Topology(world, k if world % k == 0 else 1))
+    eta = args.eta_bytes if args.eta_bytes is not None else (0 if args.algorithm == "ring" else 1 << 62)
+    cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0, weight_decay=5e-4,
+                        momentum=0.9)
+    pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=args.theta, comm=comm, eta_bytes=eta,
+                               hier_variant=args.algorithm if args.algorithm != "ring" else "hierarchical",
+                               init_master=sh.synth_master(specs, seed=0),
+                               loss_scale=gs.LossScale(1024.0), device=dev)
+    grads_host = torch.from_numpy(sh.synth_wire_grads(specs, rank=rank, seed=0)).pin_memory()
+    grads = grads_host.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    s0 = torch.cuda.current_stream(dev)
+
+    def flush_l2():
+        _native.call("gs_fill_zero", flush.data_ptr(), flush.numel(), int(s0.cuda_stream))
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    # ---- warmup
+    for i in range(args.warmup):
+        pipe.step(grads, i)
+
+    # ---- timed region: K steps, each alone between an L2 flush and a sync
+    ev = {}
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(s0)
+        ev.setdefault(name, []).append(e)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    launches0 = _native.launch_count
+    step_ms, phase_ms = [], {"pack": [], "pass1": [], "trust": [], "pass2": []}
+    for i in range(args.steps):
+        flush_l2()
+        ev.clear()
+        mark("start")
+        pipe.enqueue(grads, args.warmup + i, timer=mark if world == 1 else
+                     (lambda nm: mark(nm) if nm in ("trust", "pass2", "end") else None))
+        res = pipe.finish()
+        step_ms.append(ev["start"][0].elapsed_time(ev["end"][0]))
+        if world == 1:
+            phase_ms["pack"].append(ev["pack"][0].elapsed_time(ev["pass1"][0]))
+            phase_ms["pass1"].append(ev["pass1"][0].elapsed_time(ev["trust"][0]))
+        phase_ms["trust"].append(ev["trust"][0].elapsed_time(ev["pass2"][0]))
+        phase_ms["pass2"].append(ev["pass2"][0].elapsed_time(ev["end"][0]))
+    launches = _native.launch_count - launches0 - args.steps  # minus the L2 flushes
+    barrier()
+    clk = clocks.stop()
+
+    mean_ms = statistics.mean(step_ms)
+    t = torch.tensor([mean_ms, statistics.mean(phase_ms["pass2"])], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mean_ms, pass2_ms = float(t[0]), float(t[1])
+
+    # ---- all-reduce bus bandwidth on the whole fp16 gradient (S = 2N bytes)
+    allreduce = None
+    if world > 1 and not args.no_allreduce_sweep:
+        allreduce = allreduce_busbw(pipe, world, local, dev)
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        arena = pipe.grad_arena()
+        e2e_ms = []
+        for i in range(max(2, min(args.steps, 10))):
+            flush_l2()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s0)
+            arena.copy_(grads_host, non_blocking=True)
+            pipe.enqueue(arena, 1000 + i)
+            pipe.finish()
+            b.record(s0)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+        te = torch.tensor([statistics.mean(e2e_ms[1:])], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(float(te[0]), 4), "unit": "ms",
+               "h2d_bytes_per_step": 2 * n_params, "d2h_bytes_per_step": 4 + 8}
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        r = cpu_reference(args.model, 1, args.theta, eta, steps=3, warmup=1, budget_s=30.0)
+        cpu = {"value": round(r["ms"], 2), "unit": "ms", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"]}
+
+    if rank != 0:
+        return
+    peak, peak_kind = load_peaks()
+    pass2_bytes = 20 * n_params
+    achieved = pass2_bytes / (pass2_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "pass2_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(args.model)
+    update_bytes = 26 * n_params + 4 * n_params  # pass1+pass2 (26 B) + pack (4 B)
+    line = {
+        "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "wire_dtype": "f16", "data": "synthetic",
+        "config": {"workload": f"{args.model} fused MP-LARS step (pack -> "
+                               f"{'allreduce -> ' if world > 1 else ''}pass1 -> trust -> pass2)",
+                   "model": args.model, "params": n_params, "tensors": len(specs),
+                   "theta": args.theta, "buckets": len(pipe.buckets),
+                   "algorithm": args.algorithm if world > 1 else "none",
+                   "topology": (f"Topology({world},{comm.topo.k})" if comm else "1 GPU"),
+                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every step"},
+        "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
+        "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
+        "roofline": {"bound": "hbm", "kernel": "gs_lars_pass2", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": pass2_bytes},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "allreduce": allreduce,
+        "cpu_baseline": cpu,
+        "last_step": {"applied": res.applied, "scale": res.scale, "grad_norm": res.grad_norm},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def allreduce_busbw(pipe, world, local, dev) -> dict:
+    """busBW = S/t * 2(p-1)/p for the flat ring, the literal master hierarchy
+    and the sharded hierarchy on the whole fp16 gradient buffer."""
+    import torch
+    import torch.distributed as dist
+    import paper_1807_11205_b200 as gs
+    from paper_1807_11205_b200.dist import Communicator
+
+    buf = torch.zeros(pipe.total, dtype=torch.uint16, device=dev).view(torch.float16)
+    S = 2 * sum(pipe.sizes)
+    out = {"bytes": S}
+    variants = [("ring", 1)]
+    for k in (4, 2):
+        if world % k == 0 and k < world:
+            variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k)]
+    comms = {}
+    s0 = torch.cuda.current_stream(dev)
+    for name, k in variants:
+        if k not in comms:
+            comms[k] = Communicator(gs.Topology(world, k))
+        comm = comms[k]
+        algo = name.split("_")[0]
+        n = buf.numel() - buf.numel() % (k * 8)
+        t = buf[:n]
+        for _ in range(3):
+            comm.allreduce(t, algo)
+        torch.cuda.synchronize(dev)
+        dist.barrier(device_ids=[local])
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        iters = 10
+        a.record(s0)
+        for _ in range(iters):
+            comm.allreduce(t, algo)
+        b.record(s0)
+        b.synchronize()
+        ms = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        sec = float(ms) * 1e-3
+        out[name] = {"us": round(sec * 1e6, 2),
+                     "busbw_gbs": round(S / sec * 2 * (world - 1) / world / 1e9, 1),
+                     "algbw_gbs": round(S / sec / 1e9, 1)}
+    return out
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        from paper_1807_11205_b200.dist import init_from_env
+        init_from_env("nccl")
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

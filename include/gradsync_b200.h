@@ -1,0 +1,191 @@
+/*
+ * gradsync_b200.h — C ABI of the B200 gradient-pipeline library
+ * (libgradsync_b200.so, built from paper_1807_11205_b200/csrc/).
+ *
+ * The reference (gradsync, pkg/src/gradsync) is pure Python + numpy and has no
+ * FFI layer; its drop-in boundary is the Python API re-exported by
+ * pkg/src/gradsync/__init__.py:3-70.  Every entry point below replaces the
+ * numpy arithmetic behind one of those Python functions; the Python shims in
+ * paper_1807_11205_b200/*.py keep the reference signatures, validation and
+ * error messages and call these through ctypes.
+ *
+ * Conventions
+ *   - All data pointers are CUDA device pointers (or peer-mapped device
+ *     pointers for the *_slots entry points).  Tables (gs_segment, gs_chunk,
+ *     gs_copy, slot pointer arrays, gs_step_params) also live in device memory;
+ *     the caller builds and uploads them once and reuses them.
+ *   - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous
+ *     on that stream, allocates nothing and never synchronises.
+ *   - Return value: 0 on success, negative on a bad argument (GS_EINVAL) or a
+ *     launch error (GS_ECUDA); gs_last_error() then holds a message.
+ *   - fp16 data is carried as uint16_t binary16 bit patterns, exactly like the
+ *     reference (halfprec.py:3-7).  Every narrowing is IEEE round-to-nearest-
+ *     even with overflow to +-Inf and every NaN canonicalised to 0x7E00
+ *     (halfprec.py:40-85).
+ *   - No FMA contraction anywhere an fp32 result is observable: products and
+ *     sums are rounded separately, matching numpy's separate ufunc calls.
+ */
+#ifndef GRADSYNC_B200_H
+#define GRADSYNC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+#define GS_OK 0
+#define GS_EINVAL (-1)
+#define GS_ECUDA (-2)
+
+/* gs_segment.flags — same bit meaning as the LARS v1 checkpoint flag byte
+ * (lars.py:186-188 / pkg/README.md:167-173). */
+#define GS_SEG_DECAY_EXEMPT 1u
+#define GS_SEG_LARS_ENABLED 2u
+
+/* gs_step_params.mode bits */
+#define GS_MODE_DIV1 1u        /* divide widened gradient by div1 (mean over p) */
+#define GS_MODE_DIV1_POW2 2u   /* div1 is a power of two: multiply by rcp1 (bit-identical) */
+#define GS_MODE_DIV2 4u        /* divide by div2 (loss-scale unscale) */
+#define GS_MODE_DIV2_POW2 8u   /* div2 is a power of two: multiply by rcp2 */
+#define GS_MODE_DECAY 16u      /* cfg.weight_decay != 0.0 (lars.py:169) */
+#define GS_MODE_GRADNORM 32u   /* also accumulate sum(g^2) for the grad-norm metric */
+
+/* device flag word bits written by gs_lars_pass1 / gs_nonfinite_* */
+#define GS_FLAG_SCALED_NONFINITE 1u   /* LossScale.update finite test (halfprec.py:210) */
+#define GS_FLAG_GRAD_NONFINITE 2u     /* lars_step finite gate (lars.py:161-163) */
+
+/* One parameter group (lars.py:92-125) as seen by the fused kernels. */
+typedef struct gs_segment {
+  const void* g;        /* gradient: fp16 bits (uint16) or fp32, per call flag */
+  float* w;             /* fp32 master weights */
+  float* v;             /* fp32 velocity */
+  uint16_t* w16;        /* binary16 working copy */
+  int64_t n;            /* element count */
+  int32_t chunk_begin;  /* first chunk of this segment in the chunk table */
+  int32_t chunk_count;  /* number of chunks of this segment */
+  uint32_t flags;       /* GS_SEG_* */
+  uint32_t reserved[3];
+} gs_segment; /* 64 bytes */
+
+/* A contiguous piece [start, start+len) of segment `seg`; len <= 65536. */
+typedef struct gs_chunk {
+  int64_t start;
+  int32_t seg;
+  int32_t len;
+} gs_chunk; /* 16 bytes */
+
+/* One byte range copy for the fusion packer (fusion.py:83-94). */
+typedef struct gs_copy {
+  const void* src;
+  void* dst;
+  int64_t nbytes;
+} gs_copy; /* 24 bytes */
+
+/* Per-step scalars, in device memory so a captured CUDA graph can be replayed
+ * with a new loss scale / learning rate by rewriting this struct. */
+typedef struct gs_step_params {
+  double eta;           /* LarsConfig.eta (lars.py:76) */
+  double epsilon;       /* LarsConfig.epsilon */
+  double gamma;         /* Schedule.lr(step) (lars.py:165), fp64 */
+  float weight_decay;   /* float32(cfg.weight_decay) (lars.py:166) */
+  float momentum;       /* float32(cfg.momentum) (lars.py:167) */
+  float div1, rcp1;     /* mean divisor float32(p) (collectives.py:268-269) */
+  float div2, rcp2;     /* unscale divisor float32(scale) (halfprec.py:234) */
+  uint32_t mode;        /* GS_MODE_* */
+  uint32_t reserved;
+} gs_step_params; /* 56 bytes */
+
+int gs_abi_version(void);
+const char* gs_last_error(void);
+int gs_device_sm_count(int device);
+
+/* ---- halfprec (halfprec.py) -------------------------------------------- */
+
+/* h[i] = f32_to_f16(x[i] * scale)  (halfprec.py:108-121; with scale == 1 the
+ * multiply is the identity).  If nonfinite != NULL, OR 1 into *nonfinite when
+ * any h[i] is Inf/NaN. */
+int gs_f32_to_f16(const float* x, uint16_t* h, int64_t n, float scale,
+                  uint32_t* nonfinite, void* stream);
+
+/* x[i] = f16_to_f32(h[i]), exact (halfprec.py:88-105, 124-132). */
+int gs_f16_to_f32(const uint16_t* h, float* x, int64_t n, void* stream);
+
+/* y[i] = f16_to_f32(f32_to_f16(x[i])) (halfprec.py:135-137). */
+int gs_quantize_f32(const float* x, float* y, int64_t n, void* stream);
+
+/* out[i] = float32(g[i]) / float32(scale), IEEE division (halfprec.py:230-234). */
+int gs_unscale_f32(const float* g, float* out, int64_t n, float scale, void* stream);
+
+/* OR `bit` into *flag if any element of any tensor is non-finite
+ * (LossScale.update, halfprec.py:209-210; lars_step gate, lars.py:161-163).
+ * ptrs/lens are device arrays of ntensors entries; max_len (host value) is the
+ * longest length and sizes the grid; is_f16 selects uint16 binary16 vs fp32. */
+int gs_nonfinite(const uint64_t* ptrs, const int64_t* lens, int ntensors, int64_t max_len,
+                 int is_f16, uint32_t* flag, uint32_t bit, void* stream);
+
+/* ---- fusion (fusion.py) ------------------------------------------------ */
+
+/* Batched byte copy: copies[i].src -> copies[i].dst for ncopies entries
+ * (device table).  Used for FusionBuffer._emit (fusion.py:83-94) and for the
+ * fused pipeline's bucket packer.  Entries may have any alignment. */
+int gs_batched_copy(const gs_copy* copies, int ncopies, void* stream);
+
+/* ---- in-order folds (collectives.py:261-283) -------------------------- */
+
+/* out = slots[0] + slots[1] + ... + slots[p-1] as an ascending fp32 left fold;
+ * if mean, out /= float32(p) (fold_ascending, collectives.py:261-270).
+ * slots: device array of p device (or peer) pointers; each slot is offset by
+ * `offset` elements.  out may alias slots[0]. */
+int gs_fold_f32(const uint64_t* slots, int p, int64_t offset, float* out, int64_t n,
+                int mean, void* stream);
+
+/* Pairwise-tree fold of binary16 patterns with widen-add-narrow combines:
+ * level pairs (i, i+1), odd tail carried (fold_f16_tree, collectives.py:273-283).
+ * out may alias slots[0].  If nonfinite != NULL, OR 1 into *nonfinite when any
+ * output element is Inf/NaN. */
+int gs_fold_f16_tree(const uint64_t* slots, int p, int64_t offset, uint16_t* out,
+                     int64_t n, uint32_t* nonfinite, void* stream);
+
+/* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
+
+/* Pass 1 over `nchunk` chunks starting at chunk index `chunk0`: widen (fp16
+ * grads) / mean / unscale per params->mode, OR the non-finite flags, and write
+ * per-chunk fp64 partials {sum w^2, sum eff^2, sum g^2} (lars.py:145-146,
+ * 169-172; experiment.py:408-411) to partials[3*chunk + k].  g_is_f16 selects
+ * the gradient element type for every segment. */
+int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
+                  int g_is_f16, const gs_step_params* params, double* partials,
+                  uint32_t* flags, void* stream);
+
+/* Per segment: fold the chunk partials in chunk order, take the fp64 norms,
+ * local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150, 173-176) and
+ * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (optional,
+ * nseg x 4 doubles) receives {||w||, ||eff||, local, sum g^2}; grad_norm_out
+ * (optional) receives sqrt of the sum of per-segment g^2 in segment order
+ * (experiment.py:408-411). */
+int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
+                  const gs_step_params* params, float* seg_scale, double* seg_out,
+                  double* grad_norm_out, void* stream);
+
+/* Pass 2: if (*flags & flag_mask) do nothing (lars.py:161-163 — the step is
+ * rejected with no mutation).  Otherwise per element
+ *   eff = g  or  g + wd*w                 (lars.py:169-172)
+ *   v   = momentum*v + seg_scale[s]*eff   (lars.py:178)
+ *   w   = w - v                           (lars.py:179)
+ *   w16 = f32_to_f16(w)                   (lars.py:180)
+ */
+int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
+                  int g_is_f16, const gs_step_params* params, const float* seg_scale,
+                  const uint32_t* flags, uint32_t flag_mask, void* stream);
+
+/* Write `nbytes` of 0 to dst with a kernel (L2 flush helper / flag reset). */
+int gs_fill_zero(void* dst, int64_t nbytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRADSYNC_B200_H */

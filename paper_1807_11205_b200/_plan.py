@@ -1,0 +1,176 @@
+"""Segment / chunk tables and the three-kernel LARS launch sequence.
+
+A *segment* is one parameter group (lars.py:92-125): pointers to its
+gradient, fp32 master, fp32 velocity and binary16 working copy.  A *chunk*
+is a contiguous range of one segment of at most CHUNK_ELEMS elements; one
+CTA of gs_lars_pass1 / gs_lars_pass2 handles one chunk, so the chunk table
+is the grid.  Chunks are laid out in the order the caller wants them
+traversed (the fused pipeline uses wire order so a bucket is a contiguous
+chunk range).  The fp64 partial sums of a segment are folded by
+gs_lars_trust in chunk order, so results depend only on this table.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _native
+
+#: elements per chunk: 256 threads x 8 elements x 4 unrolled rounds
+CHUNK_ELEMS = 8192
+
+
+def build_chunks(sizes, order=None, chunk_elems: int = CHUNK_ELEMS):
+    """Chunk table over segments `sizes` traversed in `order`.
+
+    Returns (chunks[CHUNK_DTYPE], chunk_begin[nseg], chunk_count[nseg]).
+    Zero-length segments own no chunk.
+    """
+    sizes = [int(n) for n in sizes]
+    order = list(range(len(sizes))) if order is None else list(order)
+    begin = np.zeros(len(sizes), dtype=np.int32)
+    count = np.zeros(len(sizes), dtype=np.int32)
+    rows = []
+    for s in order:
+        n = sizes[s]
+        begin[s] = len(rows)
+        nch = (n + chunk_elems - 1) // chunk_elems
+        for c in range(nch):
+            st = c * chunk_elems
+            rows.append((st, s, min(chunk_elems, n - st)))
+        count[s] = nch
+    chunks = np.zeros(len(rows), dtype=_native.CHUNK_DTYPE)
+    if rows:
+        arr = np.array(rows, dtype=np.int64)
+        chunks["start"] = arr[:, 0]
+        chunks["seg"] = arr[:, 1]
+        chunks["len"] = arr[:, 2]
+    return chunks, begin, count
+
+
+def _pow2_rcp(d: np.float32):
+    """(is_pow2, reciprocal) — x*rcp == x/d bitwise when d is a power of two
+    whose reciprocal is exactly representable."""
+    d = np.float32(d)
+    if not np.isfinite(d) or d <= 0:
+        return False, np.float32(0)
+    m, _ = np.frexp(d)
+    if m != 0.5:
+        return False, np.float32(0)
+    with np.errstate(over="ignore"):
+        r = np.float32(1) / d
+    ok = np.isfinite(r) and np.float32(r * d) == np.float32(1) and np.frexp(r)[0] == 0.5 \
+        and r >= np.finfo(np.float32).tiny
+    return bool(ok), r
+
+
+def step_params(*, eta: float, epsilon: float, gamma: float, weight_decay: float,
+                momentum: float, mean_divisor: float | None = None,
+                unscale_divisor: float | None = None, grad_norm: bool = False) -> np.ndarray:
+    """Host struct gs_step_params for one step."""
+    p = np.zeros(1, dtype=_native.STEP_PARAMS_DTYPE)
+    p["eta"] = float(eta)
+    p["epsilon"] = float(epsilon)
+    p["gamma"] = float(gamma)
+    p["weight_decay"] = np.float32(weight_decay)
+    p["momentum"] = np.float32(momentum)
+    mode = 0
+    if weight_decay != 0.0:
+        mode |= _native.MODE_DECAY
+    if grad_norm:
+        mode |= _native.MODE_GRADNORM
+    if mean_divisor is not None:
+        d = np.float32(mean_divisor)
+        pw, r = _pow2_rcp(d)
+        p["div1"], p["rcp1"] = d, r
+        mode |= _native.MODE_DIV1 | (_native.MODE_DIV1_POW2 if pw else 0)
+    if unscale_divisor is not None:
+        d = np.float32(unscale_divisor)
+        pw, r = _pow2_rcp(d)
+        p["div2"], p["rcp2"] = d, r
+        mode |= _native.MODE_DIV2 | (_native.MODE_DIV2_POW2 if pw else 0)
+    p["mode"] = mode
+    return p
+
+
+@dataclass
+class SegmentSpec:
+    g: int
+    w: int
+    v: int
+    w16: int
+    n: int
+    flags: int
+
+
+class LarsPlan:
+    """Device tables + scratch for running pass1 -> trust -> pass2 over a
+    fixed set of segments."""
+
+    def __init__(self, specs: list[SegmentSpec], device: torch.device, order=None,
+                 chunk_elems: int = CHUNK_ELEMS):
+        self.device = device
+        self.nseg = len(specs)
+        chunks, begin, count = build_chunks([s.n for s in specs], order, chunk_elems)
+        segs = np.zeros(self.nseg, dtype=_native.SEGMENT_DTYPE)
+        for i, s in enumerate(specs):
+            segs[i]["g"], segs[i]["w"], segs[i]["v"], segs[i]["w16"] = s.g, s.w, s.v, s.w16
+            segs[i]["n"] = s.n
+            segs[i]["flags"] = s.flags
+        segs["chunk_begin"] = begin
+        segs["chunk_count"] = count
+        self.host_segs, self.host_chunks = segs, chunks
+        self.nchunk = len(chunks)
+        self.d_segs = dev.upload(segs, device)
+        self.d_chunks = dev.upload(chunks, device)
+        self.partials = torch.zeros(max(1, 3 * self.nchunk), dtype=torch.float64, device=device)
+        self.seg_scale = torch.zeros(max(1, self.nseg), dtype=torch.float32, device=device)
+        self.seg_out = torch.zeros(max(1, 4 * self.nseg), dtype=torch.float64, device=device)
+        self.grad_norm = torch.zeros(1, dtype=torch.float64, device=device)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+        self.params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize, dtype=torch.uint8,
+                                  device=device)
+        self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
+                                          dtype=torch.uint8).pin_memory()
+
+    # -- individual launches (all async on `stream`) --------------------
+    def set_params(self, params: np.ndarray, stream=None) -> None:
+        """Stage the step scalars into the device struct.  The pinned staging
+        buffer is reused, so the caller must not call this again before the
+        previous copy executed (lars_step syncs every call; the pipeline keeps
+        its own double buffer)."""
+        self._pinned_params.numpy()[:] = params.view(np.uint8).reshape(-1)
+        s = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            self.params.copy_(self._pinned_params, non_blocking=True)
+
+    def reset_flags(self, stream_h: int) -> None:
+        _native.call("gs_fill_zero", dev.ptr(self.flags), 4, stream_h)
+
+    def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None):
+        n = self.nchunk - chunk0 if nchunk is None else nchunk
+        _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
+                     1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.partials),
+                     dev.ptr(self.flags), stream_h)
+
+    def trust(self, stream_h: int):
+        _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
+                     dev.ptr(self.params), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
+                     dev.ptr(self.grad_norm), stream_h)
+
+    def pass2(self, stream_h: int, g_is_f16: bool, flag_mask: int, chunk0: int = 0,
+              nchunk: int | None = None):
+        n = self.nchunk - chunk0 if nchunk is None else nchunk
+        _native.call("gs_lars_pass2", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
+                     1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.seg_scale),
+                     dev.ptr(self.flags), flag_mask, stream_h)
+
+    def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
+        self.reset_flags(stream_h)
+        self.pass1(stream_h, g_is_f16)
+        self.trust(stream_h)
+        self.pass2(stream_h, g_is_f16, flag_mask)

@@ -1,0 +1,130 @@
+// gs_common.cuh — shared device helpers for libgradsync_b200.
+//
+// Numerics contract:
+//  * narrowing = IEEE RNE (cvt.rn.f16.f32 -> F2FP.F16.F32), overflow -> +-Inf,
+//    and every NaN forced to 0x7E00 (reference halfprec.py:37, 76-77);
+//  * widening is exact (cvt.f32.f16);
+//  * every observable fp32 product/sum is rounded separately (__fmul_rn /
+//    __fadd_rn / __fsub_rn), never contracted to FFMA, because the reference
+//    applies numpy ufuncs one at a time (lars.py:172, 178-179);
+//  * divisions are IEEE (__fdiv_rn) unless the divisor is a power of two, in
+//    which case x * (1/d) is bit-identical (both round the same real number).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gradsync_b200.h"
+
+namespace gs {
+
+constexpr uint16_t kCanonicalNaN = 0x7E00;
+
+__device__ __forceinline__ float widen(uint16_t h) {
+  return __half2float(__ushort_as_half(h));
+}
+
+__device__ __forceinline__ uint16_t narrow(float x) {
+  const uint16_t h = __half_as_ushort(__float2half_rn(x));
+  return (x != x) ? kCanonicalNaN : h;
+}
+
+// Two lanes at once: one F2FP.F16.F32.PACK_AB plus NaN canonicalisation.
+__device__ __forceinline__ uint32_t narrow2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  uint32_t bits = *reinterpret_cast<uint32_t*>(&h);
+  if (lo != lo) bits = (bits & 0xFFFF0000u) | kCanonicalNaN;
+  if (hi != hi) bits = (bits & 0x0000FFFFu) | (uint32_t(kCanonicalNaN) << 16);
+  return bits;
+}
+
+__device__ __forceinline__ float2 widen2(uint32_t bits) {
+  __half2 h = *reinterpret_cast<__half2*>(&bits);
+  return __half22float2(h);
+}
+
+__device__ __forceinline__ bool is_finite_f32(float x) {
+  return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u;
+}
+
+__host__ __device__ __forceinline__ bool is_aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// Mean-then-unscale chain of the reference step: widened sum / float32(p)
+// (collectives.py:268-269 via experiment.py:297-299), then / float32(scale)
+// (halfprec.py:234 via experiment.py:407).  `stage1` receives the still-scaled
+// mean that LossScale.update inspects (experiment.py:403).
+struct Unscale {
+  uint32_t mode;
+  float div1, rcp1, div2, rcp2;
+
+  __device__ __forceinline__ void load(const gs_step_params* p) {
+    mode = p->mode;
+    div1 = p->div1;
+    rcp1 = p->rcp1;
+    div2 = p->div2;
+    rcp2 = p->rcp2;
+  }
+  __device__ __forceinline__ float mean(float x) const {
+    if (mode & GS_MODE_DIV1) x = (mode & GS_MODE_DIV1_POW2) ? __fmul_rn(x, rcp1) : __fdiv_rn(x, div1);
+    return x;
+  }
+  __device__ __forceinline__ float unscale(float x) const {
+    if (mode & GS_MODE_DIV2) x = (mode & GS_MODE_DIV2_POW2) ? __fmul_rn(x, rcp2) : __fdiv_rn(x, div2);
+    return x;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// Fixed-order block reduction of three doubles (deterministic: the shuffle
+// tree and the warp order never change for a given blockDim).  Result valid
+// in thread 0.
+template <int kThreads>
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ double red[3][kWarps];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = a;
+    red[1][warp] = b;
+    red[2][warp] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = red[0][0], y = red[1][0], z = red[2][0];
+#pragma unroll
+    for (int i = 1; i < kWarps; ++i) {
+      x += red[0][i];
+      y += red[1][i];
+      z += red[2][i];
+    }
+    a = x;
+    b = y;
+    c = z;
+  }
+}
+
+}  // namespace gs
+
+// ---- error plumbing for the extern "C" layer ----
+void gs_set_error(const char* fmt, ...);
+int gs_check_launch(const char* what);
+
+#define GS_REQUIRE(cond, ...)      \
+  do {                             \
+    if (!(cond)) {                 \
+      gs_set_error(__VA_ARGS__);   \
+      return GS_EINVAL;            \
+    }                              \
+  } while (0)

@@ -1,0 +1,144 @@
+"""Multi-GPU gradient all-reduce over NCCL / NVLink, one process per GPU.
+
+The reference executes p workers in one process (collectives.py:286-340) or
+over loopback TCP (tcp.py); on a B200 box each worker is a process that owns
+one GPU and the bucket all-reduce runs over NVLink 5 / NVSwitch:
+
+  "ring"          flat 1xp: ncclAllReduce(sum) on the world communicator
+                  (ring_allreduce / allreduce_f16 "ring", collectives.py:291-302,
+                  322-340; NCCL picks ring or NVLS itself);
+  "hierarchical"  the paper's three phases (hierarchical_schedule,
+                  collectives.py:183-235) on sub-communicators of
+                  Topology(p, k): ncclReduce to the group master (lowest rank,
+                  collectives.py:76-77) -> ncclAllReduce among the masters ->
+                  ncclBroadcast inside the group;
+  "sharded"       bandwidth-optimal hierarchy for NVSwitch: intra-group
+                  reduce-scatter -> all-reduce among same-offset ranks of all
+                  groups -> intra-group all-gather (moves 2(p-1)/p S per GPU,
+                  the flat ring's volume, instead of the master's 3S).
+
+Sums never use ncclAvg: the reference sums and then divides by float32(p)
+(collectives.py:268-269), which the LARS pass-1 kernel does on the fly.
+NCCL's summation order differs from the reference's pairwise tree, so these
+paths match the oracle within the reference's own fp16 tolerance (2^-9
+relative, test_collectives.py:237-250); the skip decision is order-free for
+Inf/NaN inputs.
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+from .collectives import Topology, choose_algorithm
+
+__all__ = ["Communicator", "init_from_env", "ALGORITHMS"]
+
+ALGORITHMS = ("ring", "hierarchical", "sharded")
+
+
+def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
+    """Initialise torch.distributed from torchrun's env (127.0.0.1 rendezvous).
+    Returns (rank, world_size, local_rank)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29512")
+        be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+        if be == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(be, rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(be, rank=rank, world_size=world)
+    return rank, world, local
+
+
+class Communicator:
+    """World + Topology(p, k) sub-groups for one rank.
+
+    Every rank must construct it (group creation is collective).  Groups:
+      intra[g]  = ranks of group g            (contiguous, collectives.py:70-74)
+      masters   = lowest rank of every group  (collectives.py:76-77)
+      cross[j]  = member j of every group     (the sharded middle phase)
+    """
+
+    def __init__(self, topo: Topology, rank: int | None = None):
+        self.topo = topo
+        self.rank = dist.get_rank() if rank is None else rank
+        self.world_size = topo.p
+        if dist.is_initialized() and dist.get_world_size() != topo.p:
+            raise ValueError(f"topology is for p={topo.p}, world size is {dist.get_world_size()}")
+        self.world = dist.group.WORLD
+        p, k, G = topo.p, topo.k, topo.group_count
+        self.group = topo.group_of(self.rank)
+        self.offset = self.rank - self.group * k
+        self.master = self.group * k
+        self.intra = None
+        self.masters = None
+        self.cross = None
+        if p > 1 and k > 1:
+            for g in range(G):
+                pg = dist.new_group(list(topo.members(g)))
+                if g == self.group:
+                    self.intra = pg
+        if p > 1 and G > 1:
+            pg = dist.new_group(topo.masters())
+            if self.rank == self.master:
+                self.masters = pg
+            for j in range(k):
+                pg = dist.new_group([g * k + j for g in range(G)])
+                if j == self.offset:
+                    self.cross = pg
+
+    # -- the three algorithms; all in place, sum, on the caller's current stream
+    def allreduce_ring(self, t: torch.Tensor, async_op: bool = False):
+        return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.world, async_op=async_op)
+
+    def allreduce_hierarchical(self, t: torch.Tensor):
+        """Literal three-phase: reduce to master, masters all-reduce, broadcast."""
+        topo = self.topo
+        if topo.k > 1:
+            dist.reduce(t, dst=self.master, op=dist.ReduceOp.SUM, group=self.intra)
+        if topo.group_count > 1 and self.rank == self.master:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.masters)
+        if topo.k > 1:
+            dist.broadcast(t, src=self.master, group=self.intra)
+
+    def allreduce_sharded(self, t: torch.Tensor):
+        """Reduce-scatter inside the group, all-reduce the shard across groups,
+        all-gather inside the group.  t.numel() must be a multiple of k."""
+        topo = self.topo
+        k = topo.k
+        if k == 1:
+            if topo.group_count > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.cross)
+            return
+        n = t.numel()
+        if n % k:
+            raise ValueError(f"sharded all-reduce needs a multiple of k={k} elements, got {n}")
+        shard = t.view(k, n // k)[self.offset]
+        dist.reduce_scatter_tensor(shard, t, op=dist.ReduceOp.SUM, group=self.intra)
+        if topo.group_count > 1:
+            dist.all_reduce(shard, op=dist.ReduceOp.SUM, group=self.cross)
+        dist.all_gather_into_tensor(t, shard, group=self.intra)
+
+    def allreduce(self, t: torch.Tensor, algorithm: str) -> None:
+        if self.topo.p == 1:
+            return
+        if algorithm == "ring":
+            self.allreduce_ring(t)
+        elif algorithm == "hierarchical":
+            self.allreduce_hierarchical(t)
+        elif algorithm == "sharded":
+            self.allreduce_sharded(t)
+        else:
+            raise ValueError(f"unknown algorithm {algorithm!r}")
+
+    def pick(self, nbytes: int, eta_bytes: int, hier_variant: str = "hierarchical") -> str:
+        """Hybrid rule (collectives.py:238-244) mapped onto the NCCL variants."""
+        return hier_variant if choose_algorithm(nbytes, eta_bytes) == "hierarchical" else "ring"

@@ -1,0 +1,393 @@
+"""The fused per-step gradient pipeline of one data-parallel rank.
+
+This composes the reference's step body (experiment.py:368-413) on the fp16
+wire that the north star asks for, device-resident:
+
+  1. pack       per-parameter fp16 gradients -> theta-buckets of the wire
+                buffer, in enqueue (backward) order; bucket boundaries are
+                exactly FusionBuffer's (fusion.py:58-94)       gs_batched_copy
+  2. all-reduce every bucket, sum, over NCCL (flat ring / hierarchical /
+                sharded), bucket i in flight while bucket i+1 is packed and
+                bucket i-1 runs pass 1                          dist.Communicator
+  3. pass 1     widen, /float32(p) (mean, collectives.py:268-269), finite test
+                on the scaled mean (LossScale.update, experiment.py:403),
+                /float32(step_scale) (unscale, experiment.py:407), finite
+                gate (lars.py:161-163), fp64 partial norms      gs_lars_pass1
+  4. trust      per-group trust ratio and fp32 scale            gs_lars_trust
+  5. pass 2     momentum / master / working-copy update, skipped on the
+                device when either flag is set                  gs_lars_pass2
+
+Memory layout (HBM): one uint16 wire buffer holding every bucket back to
+back (each bucket starts on a 512-byte boundary; the zero slack after a
+bucket's payload is never part of any tensor, so the per-bucket unpack_map is
+the reference's), and fp32 master / fp32 velocity / uint16 working arenas
+laid out at the SAME element offsets as the wire, so pass 1/2 stream four
+arrays with one index.  ParamGroup objects are views into the arenas.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _native
+from ._plan import LarsPlan, SegmentSpec, step_params
+from .fusion import copy_table, plan_buckets
+from .halfprec import LossScale
+from .lars import LarsConfig, ParamGroup, segment_flags
+
+__all__ = ["ParamSpec", "Bucket", "GradientPipeline", "StepResult", "BUCKET_ALIGN",
+           "plan_layout"]
+
+#: wire-buffer granularity (elements): bucket starts are 512-byte aligned and
+#: padded lengths are multiples of 256 so any k <= 8 shards 16-byte aligned
+BUCKET_ALIGN = 256
+
+
+@dataclass(frozen=True)
+class ParamSpec:
+    name: str
+    shape: tuple
+    kind: str
+
+    @property
+    def numel(self) -> int:
+        return int(np.prod(self.shape, dtype=np.int64)) if len(self.shape) else 1
+
+
+@dataclass
+class Bucket:
+    start: int                 # wire offset (elements)
+    length: int                # payload elements (the reference batch size)
+    padded: int                # allocated elements (multiple of BUCKET_ALIGN)
+    params: list               # registration indices, wire order
+    unpack_map: tuple          # ((name, offset, length), ...) as fusion.py:84-88
+    chunk0: int = 0
+    nchunk: int = 0
+    algorithm: str = "ring"
+
+    @property
+    def nbytes(self) -> int:
+        return 2 * self.length
+
+
+@dataclass
+class StepResult:
+    applied: bool
+    scale: float               # the loss scale the step was unscaled with
+    grad_norm: float           # experiment.py:408-411 (0.0 when not applied)
+    flags: int
+    algorithms: list = field(default_factory=list)
+
+
+def _roundup(n: int, a: int) -> int:
+    return (n + a - 1) // a * a
+
+
+def plan_layout(specs, order, threshold_bytes: int):
+    """Host-only wire layout: (wire offset per parameter, buckets, total).
+
+    Bucket membership and per-bucket unpack maps are exactly what
+    FusionBuffer(threshold) emits for uint16 tensors enqueued in `order`
+    (fusion.py:58-94); bucket b starts at a BUCKET_ALIGN-aligned wire offset.
+    """
+    sizes = [s.numel for s in specs]
+    groups_pos = plan_buckets([sizes[i] for i in order], 2, threshold_bytes)
+    wire_off = [0] * len(specs)
+    buckets, off = [], 0
+    for pos_list in groups_pos:
+        start, umap = off, []
+        idxs = [order[q] for q in pos_list]
+        for i in idxs:
+            wire_off[i] = off
+            umap.append((specs[i].name, off - start, sizes[i]))
+            off += sizes[i]
+        length = off - start
+        off = start + max(BUCKET_ALIGN, _roundup(length, BUCKET_ALIGN))
+        buckets.append(Bucket(start, length, off - start, idxs, tuple(umap)))
+    return wire_off, buckets, max(off, BUCKET_ALIGN)
+
+
+class GradientPipeline:
+    """Device-resident fp16-wire MP-LARS step for one rank.
+
+    Args:
+      specs: parameters in registration order (ParamSpec or (name, shape, kind)).
+      cfg: LarsConfig.
+      threshold_bytes: fusion threshold theta (fusion.py:42-44).
+      loss_scale: LossScale (host state, updated from the device flag).
+      order: enqueue order as registration indices (default: backward order,
+        i.e. reversed registration).
+      comm: dist.Communicator for p > 1 (None = single worker, no collective).
+      eta_bytes: hybrid threshold (collectives.py:238-244) on fp16 bucket bytes.
+      hier_variant: NCCL variant for hierarchical buckets ("hierarchical" =
+        literal master path, "sharded" = RS/AR/AG).
+      init_master: flat fp32 initial weights in registration order.
+      grad_norm: compute the experiment's grad-norm metric in pass 1.
+      local_workers: with comm=None, simulate p workers on this GPU the way
+        the reference's in-memory executor does (collectives.py:286-340):
+        each worker's gradients are packed into its own wire buffer and every
+        bucket is reduced by the ordered pairwise-tree fold kernel
+        (gs_fold_f16_tree), bit-identical to allreduce_f16.  enqueue() then
+        takes one gradient set per worker.
+    """
+
+    def __init__(self, specs, cfg: LarsConfig, *, threshold_bytes: int = 4 << 20,
+                 loss_scale: LossScale | None = None, order=None, comm=None,
+                 eta_bytes: int = 0, hier_variant: str = "hierarchical",
+                 init_master=None, grad_norm: bool = True, device=None,
+                 local_workers: int = 1):
+        self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
+                      for s in specs]
+        self.cfg = cfg
+        self.loss_scale = loss_scale if loss_scale is not None else LossScale()
+        self.comm = comm
+        if comm is not None and local_workers != 1:
+            raise ValueError("local_workers is only for the single-process (comm=None) mode")
+        self.p = comm.topo.p if comm is not None else int(local_workers)
+        self.local = comm is None and self.p > 1
+        self.eta_bytes = int(eta_bytes)
+        self.hier_variant = hier_variant
+        self.grad_norm_enabled = grad_norm
+        self.device = device or dev.require_cuda()
+        n = len(self.specs)
+        self.order = list(reversed(range(n))) if order is None else list(order)
+        if sorted(self.order) != list(range(n)):
+            raise ValueError("order must be a permutation of the parameter indices")
+        sizes = [s.numel for s in self.specs]
+        self.sizes = sizes
+
+        # ---- wire layout: FusionBuffer boundaries over the enqueue order
+        self.wire_off, self.buckets, self.total = plan_layout(self.specs, self.order,
+                                                              threshold_bytes)
+
+        d = self.device
+        self.wire = torch.zeros(self.total, dtype=torch.uint16, device=d)
+        self.master = torch.zeros(self.total, dtype=torch.float32, device=d)
+        self.velocity = torch.zeros(self.total, dtype=torch.float32, device=d)
+        self.working = torch.zeros(self.total, dtype=torch.uint16, device=d)
+        self.grad32 = torch.zeros(self.total, dtype=torch.float32, device=d)
+        if init_master is not None:
+            self.load_master(init_master)
+
+        self.groups = [self._group_view(i) for i in range(n)]
+
+        # ---- segment table (registration order = group order, so the
+        # grad-norm sum runs in the reference's group order) and chunk table
+        # in wire order, so every bucket owns a contiguous chunk range
+        wb, mb, vb, hb = (t.data_ptr() for t in (self.wire, self.master, self.velocity,
+                                                   self.working))
+        segs = [SegmentSpec(wb + 2 * self.wire_off[i], mb + 4 * self.wire_off[i],
+                            vb + 4 * self.wire_off[i], hb + 2 * self.wire_off[i], sizes[i],
+                            segment_flags(self.groups[i])) for i in range(n)]
+        self.plan = LarsPlan(segs, d, order=self.order)
+        begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]
+        c = 0
+        for b in self.buckets:
+            b.chunk0 = c
+            b.nchunk = int(sum(int(count[i]) for i in b.params))
+            if b.nchunk:
+                assert int(begin[b.params[0]]) == c or sizes[b.params[0]] == 0
+            c += b.nchunk
+            if comm is not None:
+                b.algorithm = comm.pick(b.nbytes, self.eta_bytes, hier_variant)
+            else:
+                b.algorithm = "ordered" if self.local else "none"
+        assert c == self.plan.nchunk
+
+        self._pack_cache: dict = {}
+        self._grad_arena = None
+        self._pack_stream = torch.cuda.Stream(device=d) if comm is not None else None
+        if self.local:
+            self.rank_wire = [torch.zeros(self.total, dtype=torch.uint16, device=d)
+                              for _ in range(self.p)]
+            self._slots = dev.upload(np.array([t.data_ptr() for t in self.rank_wire],
+                                              dtype=np.uint64), d)
+        self._result_host = torch.zeros(2, dtype=torch.float64).pin_memory()
+        self._flags_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+
+    # ------------------------------------------------------------ layout
+    def _group_view(self, i: int) -> ParamGroup:
+        s, o, n = self.specs[i], self.wire_off[i], self.sizes[i]
+        return ParamGroup(name=s.name, kind=s.kind, master_w=self.master[o:o + n],
+                          grad=self.grad32[o:o + n], velocity=self.velocity[o:o + n],
+                          working_w16=self.working[o:o + n])
+
+    def load_master(self, flat) -> None:
+        """Set master weights from a flat fp32 vector in registration order and
+        refresh the working copy (make_param_group, lars.py:128-139)."""
+        src = dev.to_cuda(np.asarray(flat, dtype=np.float32) if not dev.is_tensor(flat)
+                          else flat.to(torch.float32), self.device).reshape(-1)
+        if src.numel() != sum(self.sizes):
+            raise ValueError(f"expected {sum(self.sizes)} master values, got {src.numel()}")
+        ro = 0
+        for i, n in enumerate(self.sizes):
+            o = self.wire_off[i]
+            self.master[o:o + n].copy_(src[ro:ro + n])
+            ro += n
+        from .halfprec import f32_to_f16
+        self.working.copy_(f32_to_f16(self.master))
+
+    def registration_view(self, arena: torch.Tensor) -> torch.Tensor:
+        """Gather an arena (wire layout) into registration order (host checks)."""
+        return torch.cat([arena[self.wire_off[i]:self.wire_off[i] + n]
+                          for i, n in enumerate(self.sizes)])
+
+    def bucket_payload(self, b: int) -> torch.Tensor:
+        bk = self.buckets[b]
+        return self.wire[bk.start:bk.start + bk.length]
+
+    # ------------------------------------------------------------ packing
+    def grad_arena(self) -> torch.Tensor:
+        """A device fp16 (uint16) gradient arena in registration order that a
+        backward pass (or a host copy) can write into; step() accepts it."""
+        if self._grad_arena is None:
+            self._grad_arena = torch.zeros(sum(self.sizes), dtype=torch.uint16, device=self.device)
+        return self._grad_arena
+
+    def _grad_views(self, grads):
+        if dev.is_tensor(grads):
+            flat = grads.reshape(-1)
+            if flat.numel() != sum(self.sizes):
+                raise ValueError("flat gradient length does not match the parameters")
+            views, ro = [], 0
+            for n in self.sizes:
+                views.append(flat[ro:ro + n])
+                ro += n
+            return views
+        views = list(grads)
+        if len(views) != len(self.sizes):
+            raise ValueError(f"expected {len(self.sizes)} gradients, got {len(views)}")
+        return views
+
+    def _tables_for(self, views, dst: torch.Tensor):
+        """Per-bucket gs_copy tables packing `views` into `dst` (cached)."""
+        key = (dst.data_ptr(),) + tuple((t.data_ptr(), t.numel()) for t in views)
+        tabs = self._pack_cache.get(key)
+        if tabs is None:
+            for t, n in zip(views, self.sizes):
+                if t.numel() != n or t.dtype not in (torch.uint16, torch.float16) or not t.is_cuda:
+                    raise ValueError("gradients must be CUDA fp16/uint16 tensors of the "
+                                     "parameter sizes")
+            wb = dst.data_ptr()
+            tabs = []
+            for b in self.buckets:
+                t = copy_table((views[i].data_ptr(), wb + 2 * self.wire_off[i], 2 * self.sizes[i])
+                               for i in b.params if self.sizes[i])
+                tabs.append((dev.upload(t, self.device), len(t)))
+            if len(self._pack_cache) > 8:
+                self._pack_cache.clear()
+            self._pack_cache[key] = tabs
+        return tabs
+
+    @staticmethod
+    def _pack(tabs, b: int, stream_h: int) -> None:
+        tab, n = tabs[b]
+        if n:
+            _native.call("gs_batched_copy", dev.ptr(tab), n, stream_h)
+
+    # ------------------------------------------------------------ the step
+    def params_for(self, step: int) -> np.ndarray:
+        cfg = self.cfg
+        return step_params(eta=cfg.eta, epsilon=cfg.epsilon, gamma=cfg.schedule.lr(step),
+                           weight_decay=cfg.weight_decay, momentum=cfg.momentum,
+                           mean_divisor=self.p if self.p > 1 else None,
+                           unscale_divisor=self.loss_scale.scale,
+                           grad_norm=self.grad_norm_enabled)
+
+    def enqueue(self, grads, step: int, timer=None) -> None:
+        """Launch one step on the current stream (no host sync).  `timer`, if
+        given, is called with a phase name before each phase (event hooks)."""
+        plan = self.plan
+        s0 = torch.cuda.current_stream(self.device)
+        sh = int(s0.cuda_stream)
+        if self.local:
+            if len(grads) != self.p:
+                raise ValueError(f"expected gradients of {self.p} workers, got {len(grads)}")
+            tabs = [self._tables_for(self._grad_views(g), w) for g, w in zip(grads, self.rank_wire)]
+        else:
+            tabs = self._tables_for(self._grad_views(grads), self.wire)
+        plan.set_params(self.params_for(step), s0)
+        plan.reset_flags(sh)
+        if self.comm is None:
+            if timer:
+                timer("pack")
+            for b in range(len(self.buckets)):
+                if self.local:
+                    for t in tabs:
+                        self._pack(t, b, sh)
+                else:
+                    self._pack(tabs, b, sh)
+            if self.local:
+                if timer:
+                    timer("fold")
+                wb = self.wire.data_ptr()
+                for bk in self.buckets:
+                    if bk.length:
+                        _native.call("gs_fold_f16_tree", dev.ptr(self._slots), self.p, bk.start,
+                                     wb + 2 * bk.start, bk.length, None, sh)
+            if timer:
+                timer("pass1")
+            plan.pass1(sh, g_is_f16=True)
+        else:
+            ps = self._pack_stream
+            ps.wait_stream(s0)
+            works = []
+            for b, bk in enumerate(self.buckets):
+                with torch.cuda.stream(ps):
+                    self._pack(tabs, b, int(ps.cuda_stream))
+                    payload = self.wire[bk.start:bk.start + bk.padded]
+                    if bk.algorithm == "ring":
+                        works.append(self.comm.allreduce_ring(payload, async_op=True))
+                    else:
+                        self.comm.allreduce(payload, bk.algorithm)
+                        ev = torch.cuda.Event()
+                        ev.record(ps)
+                        works.append(ev)
+            for b, bk in enumerate(self.buckets):
+                w = works[b]
+                if isinstance(w, torch.cuda.Event):
+                    s0.wait_event(w)
+                else:
+                    w.wait()
+                plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+        if timer:
+            timer("trust")
+        plan.trust(sh)
+        if timer:
+            timer("pass2")
+        plan.pass2(sh, g_is_f16=True,
+                   flag_mask=_native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE)
+        if timer:
+            timer("end")
+
+    def finish(self) -> StepResult:
+        """Read the step's flags (the one host sync) and advance LossScale
+        exactly as experiment.py:403-413 does."""
+        self._flags_host.copy_(self.plan.flags, non_blocking=True)
+        self._result_host[0:1].copy_(self.plan.grad_norm, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        flags = int(self._flags_host.item())
+        step_scale = self.loss_scale.scale
+        applied = self.loss_scale.update_from_flag(bool(flags & _native.FLAG_SCALED_NONFINITE))
+        grad_norm = 0.0
+        if applied:
+            grad_norm = float(self._result_host[0].item()) if self.grad_norm_enabled else 0.0
+            applied = not (flags & _native.FLAG_GRAD_NONFINITE)
+        return StepResult(applied=applied, scale=step_scale, grad_norm=grad_norm, flags=flags,
+                          algorithms=sorted({b.algorithm for b in self.buckets}))
+
+    def step(self, grads, step: int) -> StepResult:
+        self.enqueue(grads, step)
+        return self.finish()
+
+    # ------------------------------------------------------------ inspection
+    def seg_scales(self) -> np.ndarray:
+        return dev.to_host(self.plan.seg_scale)[: len(self.specs)]
+
+    def seg_stats(self) -> np.ndarray:
+        """(nseg, 4): ||w||, ||eff||, local lr, sum g^2 of the last step."""
+        return dev.to_host(self.plan.seg_out).reshape(-1, 4)[: len(self.specs)]

@@ -160,6 +160,19 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
                   int g_is_f16, const gs_step_params* params, double* partials,
                   uint32_t* flags, void* stream);
 
+/* gs_lars_pass1 fused with gs_lars_trust.  counters: device uint32[nseg + 1],
+ * zero before the first chunk of a step is launched (reset together with
+ * the flags).  The last CTA to finish a segment folds that segment's
+ * partials (same fixed order as gs_lars_trust) and writes seg_scale /
+ * seg_out; the last segment to finish (of nseg_active segments that own at
+ * least one chunk) fills the empty segments and writes *grad_norm_out.  May
+ * be called over several disjoint chunk ranges per step (e.g. one per
+ * bucket as its all-reduce lands). */
+int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
+                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params,
+                        double* partials, uint32_t* flags, uint32_t* counters, float* seg_scale,
+                        double* seg_out, double* grad_norm_out, void* stream);
+
 /* Per segment: fold the chunk partials in chunk order, take the fp64 norms,
  * local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150, 173-176) and
  * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (optional,

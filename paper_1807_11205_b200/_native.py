@@ -67,6 +67,9 @@ SIGNATURES = {
                                  c_void_p]),
     "gs_lars_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
+    "gs_lars_pass1_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
     "gs_lars_trust": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
     "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,

@@ -131,7 +131,13 @@ class LarsPlan:
         self.seg_scale = torch.zeros(max(1, self.nseg), dtype=torch.float32, device=device)
         self.seg_out = torch.zeros(max(1, 4 * self.nseg), dtype=torch.float64, device=device)
         self.grad_norm = torch.zeros(1, dtype=torch.float64, device=device)
-        self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+        # one int32 block, reset by one kernel per step: [0] = non-finite
+        # flags, [4 : 4 + nseg + 1] = per-segment / global arrival counters
+        # of the fused pass1 + trust kernel
+        self.flagbuf = torch.zeros(4 + self.nseg + 1, dtype=torch.int32, device=device)
+        self.flags = self.flagbuf[0:1]
+        self.counters = self.flagbuf[4:]
+        self.nseg_active = int((count > 0).sum())
         self.params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize, dtype=torch.uint8,
                                   device=device)
         self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
@@ -149,13 +155,26 @@ class LarsPlan:
             self.params.copy_(self._pinned_params, non_blocking=True)
 
     def reset_flags(self, stream_h: int) -> None:
-        _native.call("gs_fill_zero", dev.ptr(self.flags), 4, stream_h)
+        _native.call("gs_fill_zero", dev.ptr(self.flagbuf), 4 * self.flagbuf.numel(), stream_h)
 
-    def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None):
+    @property
+    def fused(self) -> bool:
+        """pass1 computes the trust ratios itself (no separate trust launch)."""
+        return self.nseg_active > 0
+
+    def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None,
+              fuse: bool = True):
         n = self.nchunk - chunk0 if nchunk is None else nchunk
-        _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
-                     1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.partials),
-                     dev.ptr(self.flags), stream_h)
+        if fuse and self.fused:
+            _native.call("gs_lars_pass1_trust", dev.ptr(self.d_segs), self.nseg, self.nseg_active,
+                         dev.ptr(self.d_chunks), chunk0, n, 1 if g_is_f16 else 0,
+                         dev.ptr(self.params), dev.ptr(self.partials), dev.ptr(self.flags),
+                         dev.ptr(self.counters), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
+                         dev.ptr(self.grad_norm), stream_h)
+        else:
+            _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
+                         1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.partials),
+                         dev.ptr(self.flags), stream_h)
 
     def trust(self, stream_h: int):
         _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
@@ -172,5 +191,6 @@ class LarsPlan:
     def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
         self.reset_flags(stream_h)
         self.pass1(stream_h, g_is_f16)
-        self.trust(stream_h)
+        if not self.fused:
+            self.trust(stream_h)
         self.pass2(stream_h, g_is_f16, flag_mask)

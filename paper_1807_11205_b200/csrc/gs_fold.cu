@@ -62,7 +62,7 @@ fold_f16_fixed_kernel(const uint64_t* __restrict__ slots, int64_t offset, uint16
     src[r] = reinterpret_cast<const uint16_t*>(slots[r]) + offset;
     vec = vec && gs::is_aligned16(src[r]);
   }
-  bool bad = false;
+  uint32_t bad = 0;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t tail_begin = 0;
@@ -109,14 +109,14 @@ fold_f16_fixed_kernel(const uint64_t* __restrict__ slots, int64_t offset, uint16
     bad |= (bits & 0x7C00u) == 0x7C00u;
     out[i] = bits;
   }
-  if (nonfinite != nullptr && __any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0)
-    atomicOr(nonfinite, 1u);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
 __global__ void __launch_bounds__(kThreads)
 fold_f16_generic_kernel(const uint64_t* __restrict__ slots, int p, int64_t offset, uint16_t* out,
                         int64_t n, uint32_t* __restrict__ nonfinite) {
-  bool bad = false;
+  uint32_t bad = 0;
   float v[kMaxGenericP];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -126,8 +126,8 @@ fold_f16_generic_kernel(const uint64_t* __restrict__ slots, int p, int64_t offse
     bad |= (bits & 0x7C00u) == 0x7C00u;
     out[i] = bits;
   }
-  if (nonfinite != nullptr && __any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0)
-    atomicOr(nonfinite, 1u);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
 // ---- fp32 ascending left fold, 4 elements per thread (float4) ----

@@ -29,7 +29,7 @@ inline int grid_for(int64_t work_items) {
 __global__ void __launch_bounds__(kThreads)
 f32_to_f16_kernel(const float* __restrict__ x, uint16_t* __restrict__ h, int64_t n, float scale,
                   int apply_scale, uint32_t* __restrict__ nonfinite, int vec) {
-  bool bad = false;
+  uint32_t bad = 0;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t tail_begin = 0;
@@ -62,9 +62,8 @@ f32_to_f16_kernel(const float* __restrict__ x, uint16_t* __restrict__ h, int64_t
     bad |= (o & 0x7C00u) == 0x7C00u;
     h[i] = o;
   }
-  if (nonfinite != nullptr && __any_sync(0xFFFFFFFFu, bad)) {
-    if ((threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
-  }
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -137,7 +136,7 @@ nonfinite_kernel(const uint64_t* __restrict__ ptrs, const int64_t* __restrict__ 
   const int64_t begin = blockIdx.x * per_block;
   if (begin >= n) return;
   const int64_t end = begin + per_block < n ? begin + per_block : n;
-  bool bad = false;
+  uint32_t bad = 0;
   if (is_f16) {
     const uint16_t* p = reinterpret_cast<const uint16_t*>(ptrs[t]);
     for (int64_t i = begin + threadIdx.x; i < end; i += kThreads) bad |= (p[i] & 0x7C00u) == 0x7C00u;
@@ -145,7 +144,8 @@ nonfinite_kernel(const uint64_t* __restrict__ ptrs, const int64_t* __restrict__ 
     const float* p = reinterpret_cast<const float*>(ptrs[t]);
     for (int64_t i = begin + threadIdx.x; i < end; i += kThreads) bad |= !gs::is_finite_f32(p[i]);
   }
-  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, bit);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (bad && (threadIdx.x & 31) == 0) atomicOr(flag, bit);
 }
 
 }  // namespace

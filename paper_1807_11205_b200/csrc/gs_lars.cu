@@ -76,12 +76,12 @@ template <bool F16, bool LARS>
 __device__ __forceinline__ void pass1_body(const typename GradIO<F16>::T* __restrict__ g,
                                            const float* __restrict__ w, int len, const gs::Unscale& u,
                                            bool decay, float wd, bool gnorm, double& sw, double& se,
-                                           double& sg, bool& bad_scaled, bool& bad) {
+                                           double& sg, uint32_t& fl) {
   auto elem = [&](float graw, float wv) {
     const float gm = u.mean(graw);
-    bad_scaled |= !gs::is_finite_f32(gm);
+    fl |= gs::is_finite_f32(gm) ? 0u : GS_FLAG_SCALED_NONFINITE;
     const float gu = u.unscale(gm);
-    bad |= !gs::is_finite_f32(gu);
+    fl |= gs::is_finite_f32(gu) ? 0u : GS_FLAG_GRAD_NONFINITE;
     if (LARS) {
       const float eff = decay ? __fadd_rn(gu, __fmul_rn(wd, wv)) : gu;
       sq_acc(sw, wv);
@@ -103,11 +103,49 @@ __device__ __forceinline__ void pass1_body(const typename GradIO<F16>::T* __rest
     elem(GradIO<F16>::load1(g + i), LARS ? w[i] : 0.0f);
 }
 
-template <bool F16>
+// lars_local_lr (lars.py:142-150) + lars.py:177 for one segment: norms are
+// sqrt of the fp64 dots, local = (eta * w_norm) / (g_norm + eps) or 1.0 when
+// degenerate / LARS disabled, scale = float32(local * gamma).
+__device__ __forceinline__ void trust_eval(uint32_t sflags, double sw, double se, double sg,
+                                           const gs_step_params* __restrict__ params,
+                                           float* scale_out, double* o) {
+  const double w_norm = __dsqrt_rn(sw);
+  const double g_norm = __dsqrt_rn(se);
+  double local = 1.0;
+  if (sflags & GS_SEG_LARS_ENABLED) {
+    const double denom = __dadd_rn(g_norm, params->epsilon);
+    if (!(w_norm == 0.0 || denom == 0.0)) local = __ddiv_rn(__dmul_rn(params->eta, w_norm), denom);
+  }
+  *scale_out = __double2float_rn(__dmul_rn(local, params->gamma));
+  o[0] = w_norm;
+  o[1] = g_norm;
+  o[2] = local;
+  o[3] = sg;
+}
+
+// experiment.py:408-411: sqrt(sum over groups of float(dot(g, g))), summed in
+// group order starting from 0.
+__device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg) {
+  double acc = 0.0;
+  for (int s = 0; s < nseg; ++s) acc = __dadd_rn(acc, __ldcg(seg_out + 4 * (int64_t)s + 3));
+  return __dsqrt_rn(acc);
+}
+
+// FUSE = false: plain pass 1 (partials + flags).
+// FUSE = true : additionally the last CTA to finish a segment (per-segment
+// arrival counter) folds that segment's partials in chunk order and writes its
+// trust ratio, and the last segment to finish writes the grad norm and the
+// empty segments — the trust step costs no extra launch and no tail.  Which
+// CTA arrives last is timing-dependent; the result is not: the fold always
+// runs over the same chunk range in the same fixed tree.
+template <bool F16, bool FUSE>
 __global__ void __launch_bounds__(kThreads)
-lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int chunk0,
+lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
+                  const gs_chunk* __restrict__ chunks, int chunk0,
                   const gs_step_params* __restrict__ params, double* __restrict__ partials,
-                  uint32_t* __restrict__ flags) {
+                  uint32_t* __restrict__ flags, uint32_t* __restrict__ counters,
+                  float* __restrict__ seg_scale, double* __restrict__ seg_out,
+                  double* __restrict__ grad_norm_out) {
   using T = typename GradIO<F16>::T;
   const int c = chunk0 + blockIdx.x;
   const gs_chunk ch = chunks[c];
@@ -121,20 +159,58 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   const bool decay = (u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
   const bool gnorm = (u.mode & GS_MODE_GRADNORM) != 0;
   double sw = 0.0, se = 0.0, sgn = 0.0;
-  bool bad_scaled = false, bad = false;
+  uint32_t fl = 0;
   if (sflags & GS_SEG_LARS_ENABLED)
-    pass1_body<F16, true>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, bad_scaled, bad);
+    pass1_body<F16, true>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, fl);
   else
-    pass1_body<F16, false>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, bad_scaled, bad);
+    pass1_body<F16, false>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, fl);
 
-  const uint32_t fbits = (__any_sync(0xFFFFFFFFu, bad_scaled) ? GS_FLAG_SCALED_NONFINITE : 0u) |
-                         (__any_sync(0xFFFFFFFFu, bad) ? GS_FLAG_GRAD_NONFINITE : 0u);
-  if (fbits && (threadIdx.x & 31) == 0) atomicOr(flags, fbits);
+  fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+  if (fl != 0u && (threadIdx.x & 31) == 0) atomicOr(flags, fl);
   gs::block_sum3<kThreads>(sw, se, sgn);
+  if (!FUSE) {
+    if (threadIdx.x == 0) {
+      partials[3 * (int64_t)c + 0] = sw;
+      partials[3 * (int64_t)c + 1] = se;
+      partials[3 * (int64_t)c + 2] = sgn;
+    }
+    return;
+  }
+  __shared__ int s_last;
   if (threadIdx.x == 0) {
     partials[3 * (int64_t)c + 0] = sw;
     partials[3 * (int64_t)c + 1] = se;
     partials[3 * (int64_t)c + 2] = sgn;
+    __threadfence();
+    const uint32_t prev = atomicAdd(&counters[ch.seg], 1u);
+    s_last = (prev + 1 == (uint32_t)sg->chunk_count);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // fold this segment's chunk partials: fixed strided order + fixed tree
+  const int cb = sg->chunk_begin, cn = sg->chunk_count;
+  double a = 0.0, b = 0.0, d = 0.0;
+  for (int i = threadIdx.x; i < cn; i += kThreads) {
+    const double* pp = partials + 3 * (int64_t)(cb + i);
+    a += __ldcg(pp + 0);
+    b += __ldcg(pp + 1);
+    d += __ldcg(pp + 2);
+  }
+  __syncthreads();  // block_sum3's shared scratch is reused
+  gs::block_sum3<kThreads>(a, b, d);
+  if (threadIdx.x == 0) {
+    trust_eval(sflags, a, b, d, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
+    __threadfence();
+    const uint32_t prev = atomicAdd(&counters[nseg], 1u);
+    if (prev + 1 == (uint32_t)nseg_active) {
+      __threadfence();
+      for (int s = 0; s < nseg; ++s)
+        if (segs[s].chunk_count == 0)
+          trust_eval(segs[s].flags, 0.0, 0.0, 0.0, params, seg_scale + s, seg_out + 4 * (int64_t)s);
+      __threadfence();
+      if (grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
+    }
   }
 }
 
@@ -144,7 +220,6 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* _
                   const gs_step_params* __restrict__ params, float* __restrict__ seg_scale,
                   double* __restrict__ seg_out, double* __restrict__ grad_norm_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double eta = params->eta, eps = params->epsilon, gamma = params->gamma;
   for (int s = warp; s < nseg; s += kTrustThreads / 32) {
     const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
     const uint32_t sflags = segs[s].flags;
@@ -158,32 +233,10 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* _
     sw = gs::warp_sum(sw);
     se = gs::warp_sum(se);
     sg = gs::warp_sum(sg);
-    if (lane == 0) {
-      // lars_local_lr (lars.py:142-150): norms are sqrt of the fp64 dot,
-      // then (eta * w_norm) / (g_norm + eps), 1.0 when degenerate
-      const double w_norm = __dsqrt_rn(sw);
-      const double g_norm = __dsqrt_rn(se);
-      double local = 1.0;
-      if (sflags & GS_SEG_LARS_ENABLED) {
-        const double denom = __dadd_rn(g_norm, eps);
-        if (!(w_norm == 0.0 || denom == 0.0)) local = __ddiv_rn(__dmul_rn(eta, w_norm), denom);
-      }
-      seg_scale[s] = __double2float_rn(__dmul_rn(local, gamma));  // lars.py:177
-      double* o = seg_out + 4 * (int64_t)s;
-      o[0] = w_norm;
-      o[1] = g_norm;
-      o[2] = local;
-      o[3] = sg;
-    }
+    if (lane == 0) trust_eval(sflags, sw, se, sg, params, seg_scale + s, seg_out + 4 * (int64_t)s);
   }
   __syncthreads();
-  if (threadIdx.x == 0 && grad_norm_out != nullptr) {
-    // experiment.py:408-411: sqrt(sum over groups of float(dot(g, g))), summed
-    // in group order starting from 0
-    double acc = 0.0;
-    for (int s = 0; s < nseg; ++s) acc = __dadd_rn(acc, seg_out[4 * (int64_t)s + 3]);
-    *grad_norm_out = __dsqrt_rn(acc);
-  }
+  if (threadIdx.x == 0 && grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
 }
 
 // ----------------------------------------------------------------- pass 2
@@ -259,10 +312,34 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   GS_REQUIRE(segs && chunks && params && partials && flags, "gs_lars_pass1: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   if (g_is_f16)
-    lars_pass1_kernel<true><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, partials, flags);
+    lars_pass1_kernel<true, false><<<nchunk, kThreads, 0, s>>>(
+        segs, 0, 0, chunks, chunk0, params, partials, flags, nullptr, nullptr, nullptr, nullptr);
   else
-    lars_pass1_kernel<false><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, partials, flags);
+    lars_pass1_kernel<false, false><<<nchunk, kThreads, 0, s>>>(
+        segs, 0, 0, chunks, chunk0, params, partials, flags, nullptr, nullptr, nullptr, nullptr);
   return gs_check_launch("gs_lars_pass1");
+}
+
+int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
+                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params,
+                        double* partials, uint32_t* flags, uint32_t* counters, float* seg_scale,
+                        double* seg_out, double* grad_norm_out, void* stream) {
+  GS_REQUIRE(nchunk >= 0 && chunk0 >= 0, "gs_lars_pass1_trust: bad chunk range");
+  GS_REQUIRE(nseg_active >= 1 && nseg_active <= nseg,
+             "gs_lars_pass1_trust: need 1 <= nseg_active <= nseg (use gs_lars_trust otherwise)");
+  if (nchunk == 0) return GS_OK;
+  GS_REQUIRE(segs && chunks && params && partials && flags && counters && seg_scale && seg_out,
+             "gs_lars_pass1_trust: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g_is_f16)
+    lars_pass1_kernel<true, true><<<nchunk, kThreads, 0, s>>>(
+        segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,
+        seg_out, grad_norm_out);
+  else
+    lars_pass1_kernel<false, true><<<nchunk, kThreads, 0, s>>>(
+        segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,
+        seg_out, grad_norm_out);
+  return gs_check_launch("gs_lars_pass1_trust");
 }
 
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,

@@ -139,7 +139,7 @@ class GradientPipeline:
                  loss_scale: LossScale | None = None, order=None, comm=None,
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
-                 local_workers: int = 1):
+                 local_workers: int = 1, use_graph: bool = True):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -199,6 +199,8 @@ class GradientPipeline:
         assert c == self.plan.nchunk
 
         self._pack_cache: dict = {}
+        self.use_graph = use_graph
+        self._graphs: dict = {}
         self._grad_arena = None
         self._pack_stream = torch.cuda.Stream(device=d) if comm is not None else None
         if self.local:
@@ -280,6 +282,7 @@ class GradientPipeline:
                 tabs.append((dev.upload(t, self.device), len(t)))
             if len(self._pack_cache) > 8:
                 self._pack_cache.clear()
+                self._graphs.clear()
             self._pack_cache[key] = tabs
         return tabs
 
@@ -299,18 +302,50 @@ class GradientPipeline:
                            grad_norm=self.grad_norm_enabled)
 
     def enqueue(self, grads, step: int, timer=None) -> None:
-        """Launch one step on the current stream (no host sync).  `timer`, if
-        given, is called with a phase name before each phase (event hooks)."""
-        plan = self.plan
+        """Launch one step on the current stream (no host sync).
+
+        `timer`, if given, is called with a phase name before each phase
+        (the bench records CUDA events there); timed launches run eagerly.
+        Otherwise, with comm=None and use_graph, the kernel sequence is
+        captured once per gradient-buffer set into a CUDA graph and replayed:
+        the per-step scalars live in device memory (gs_step_params), so a
+        replay picks up the new loss scale / learning rate.
+        """
         s0 = torch.cuda.current_stream(self.device)
-        sh = int(s0.cuda_stream)
         if self.local:
             if len(grads) != self.p:
                 raise ValueError(f"expected gradients of {self.p} workers, got {len(grads)}")
             tabs = [self._tables_for(self._grad_views(g), w) for g, w in zip(grads, self.rank_wire)]
+            key = tuple(id(t) for t in tabs)
         else:
             tabs = self._tables_for(self._grad_views(grads), self.wire)
-        plan.set_params(self.params_for(step), s0)
+            key = id(tabs)
+        self.plan.set_params(self.params_for(step), s0)
+        if timer is not None or not self.use_graph or self.comm is not None:
+            self._launch(tabs, s0, timer)
+            return
+        entry = self._graphs.get(key)
+        if entry is None:
+            # first sight of these buffers: run eagerly (warms every kernel),
+            # capture on the next call
+            self._graphs[key] = "warm"
+            self._launch(tabs, s0, None)
+            return
+        if entry == "warm":
+            g = torch.cuda.CUDAGraph()
+            n0 = _native.launch_count
+            with torch.cuda.graph(g):
+                self._launch(tabs, torch.cuda.current_stream(self.device), None)
+            entry = (g, _native.launch_count - n0)
+            _native.launch_count = n0
+            self._graphs[key] = entry
+        g, nk = entry
+        g.replay()
+        _native.launch_count += nk
+
+    def _launch(self, tabs, s0, timer) -> None:
+        plan = self.plan
+        sh = int(s0.cuda_stream)
         plan.reset_flags(sh)
         if self.comm is None:
             if timer:
@@ -356,7 +391,8 @@ class GradientPipeline:
                 plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
         if timer:
             timer("trust")
-        plan.trust(sh)
+        if not plan.fused:
+            plan.trust(sh)
         if timer:
             timer("pass2")
         plan.pass2(sh, g_is_f16=True,

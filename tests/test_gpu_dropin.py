@@ -209,6 +209,16 @@ def test_folds_match_reference_golden(golden):
             assert np.array_equal(out[0], g[f"f16_tree_{p}"]), p
 
 
+def test_fold_nonfinite_flag():
+    a = torch.tensor([0x7BFF, 0x3C00], dtype=torch.int32).to(torch.uint16).cuda()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = gs.collectives.fold_f16_tree([a, a], nonfinite=flag)
+    assert out.cpu().numpy().tolist() == [0x7C00, 0x4000] and flag.item() == 1
+    flag.zero_()
+    gs.collectives.fold_f16_tree([a[1:], a[1:], a[1:]], nonfinite=flag)
+    assert flag.item() == 0
+
+
 def test_allreduce_api_semantics():                      # test_collectives.py:168-231
     rng = np.random.default_rng(2)
     bufs = [rng.standard_normal(200).astype(np.float32) for _ in range(8)]

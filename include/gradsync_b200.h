@@ -67,7 +67,9 @@ typedef struct gs_segment {
   int32_t chunk_begin;  /* first chunk of this segment in the chunk table */
   int32_t chunk_count;  /* number of chunks of this segment */
   uint32_t flags;       /* GS_SEG_* */
-  uint32_t reserved[3];
+  uint32_t reserved;
+  void* gcopy;          /* optional: pass 1 also copies the raw fp16 gradient
+                           chunk here (the fused packer), or NULL */
 } gs_segment; /* 64 bytes */
 
 /* A contiguous piece [start, start+len) of segment `seg`; len <= 65536. */
@@ -95,8 +97,19 @@ typedef struct gs_step_params {
   float div1, rcp1;     /* mean divisor float32(p) (collectives.py:268-269) */
   float div2, rcp2;     /* unscale divisor float32(scale) (halfprec.py:234) */
   uint32_t mode;        /* GS_MODE_* */
-  uint32_t reserved;
+  float mul;            /* rcp1*rcp2 when both divisions are exact power-of-two
+                           scalings (see GS_HINT_POW2), else unused */
 } gs_step_params; /* 56 bytes */
+
+/* Host-side launch hints: which specialised pass-1/pass-2 kernel may be used.
+ * A hint is a promise about the contents of *params at execution time; 0 is
+ * always correct (generic kernel, per-element IEEE division). */
+#define GS_HINT_POW2 1u       /* g/div1/div2 == g*mul exactly: every active
+                                 divisor is a power of two and (fp32 input) no
+                                 divisor is active, or (fp16 input) div1 <= 2^100 */
+#define GS_HINT_RAWFLAG 2u    /* fp16 input, GS_HINT_POW2 and mul <= 1: a value is
+                                 non-finite iff its binary16 exponent is all ones */
+#define GS_HINT_GRADNORM 4u   /* must equal (params->mode & GS_MODE_GRADNORM) != 0 */
 
 int gs_abi_version(void);
 const char* gs_last_error(void);
@@ -157,7 +170,7 @@ int gs_fold_f16_tree(const uint64_t* slots, int p, int64_t offset, uint16_t* out
  * 169-172; experiment.py:408-411) to partials[3*chunk + k].  g_is_f16 selects
  * the gradient element type for every segment. */
 int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, double* partials,
+                  int g_is_f16, const gs_step_params* params, uint32_t hint, double* partials,
                   uint32_t* flags, void* stream);
 
 /* gs_lars_pass1 fused with gs_lars_trust.  counters: device uint32[nseg + 1],
@@ -170,8 +183,8 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
  * bucket as its all-reduce lands). */
 int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
                         int chunk0, int nchunk, int g_is_f16, const gs_step_params* params,
-                        double* partials, uint32_t* flags, uint32_t* counters, float* seg_scale,
-                        double* seg_out, double* grad_norm_out, void* stream);
+                        uint32_t hint, double* partials, uint32_t* flags, uint32_t* counters,
+                        float* seg_scale, double* seg_out, double* grad_norm_out, void* stream);
 
 /* Per segment: fold the chunk partials in chunk order, take the fp64 norms,
  * local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150, 173-176) and
@@ -191,8 +204,9 @@ int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
  *   w16 = f32_to_f16(w)                   (lars.py:180)
  */
 int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, const float* seg_scale,
-                  const uint32_t* flags, uint32_t flag_mask, void* stream);
+                  int g_is_f16, const gs_step_params* params, uint32_t hint,
+                  const float* seg_scale, const uint32_t* flags, uint32_t flag_mask,
+                  void* stream);
 
 /* Write `nbytes` of 0 to dst with a kernel (L2 flush helper / flag reset). */
 int gs_fill_zero(void* dst, int64_t nbytes, void* stream);

@@ -31,11 +31,15 @@ MODE_GRADNORM = 32
 FLAG_SCALED_NONFINITE = 1
 FLAG_GRAD_NONFINITE = 2
 
+HINT_POW2 = 1
+HINT_RAWFLAG = 2
+HINT_GRADNORM = 4
+
 # numpy mirrors of the device structs (layout asserted against the header)
 SEGMENT_DTYPE = np.dtype([
     ("g", "<u8"), ("w", "<u8"), ("v", "<u8"), ("w16", "<u8"),
     ("n", "<i8"), ("chunk_begin", "<i4"), ("chunk_count", "<i4"),
-    ("flags", "<u4"), ("reserved", "<u4", (3,)),
+    ("flags", "<u4"), ("reserved", "<u4"), ("gcopy", "<u8"),
 ])
 CHUNK_DTYPE = np.dtype([("start", "<i8"), ("seg", "<i4"), ("len", "<i4")])
 COPY_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("nbytes", "<i8")])
@@ -43,7 +47,7 @@ STEP_PARAMS_DTYPE = np.dtype([
     ("eta", "<f8"), ("epsilon", "<f8"), ("gamma", "<f8"),
     ("weight_decay", "<f4"), ("momentum", "<f4"),
     ("div1", "<f4"), ("rcp1", "<f4"), ("div2", "<f4"), ("rcp2", "<f4"),
-    ("mode", "<u4"), ("reserved", "<u4"),
+    ("mode", "<u4"), ("mul", "<f4"),
 ])
 assert SEGMENT_DTYPE.itemsize == 64
 assert CHUNK_DTYPE.itemsize == 16
@@ -65,15 +69,15 @@ SIGNATURES = {
     "gs_fold_f32": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int, c_void_p]),
     "gs_fold_f16_tree": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p,
                                  c_void_p]),
-    "gs_lars_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
-                              c_void_p, c_void_p]),
+    "gs_lars_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
+                              c_void_p, c_void_p, c_void_p]),
     "gs_lars_pass1_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int,
-                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                    c_void_p, c_void_p]),
+                                    c_void_p, c_uint32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p, c_void_p]),
     "gs_lars_trust": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
-    "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
-                              c_void_p, c_uint32, c_void_p]),
+    "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
+                              c_void_p, c_void_p, c_uint32, c_void_p]),
     "gs_fill_zero": (c_int, [c_void_p, c_int64, c_void_p]),
 }
 

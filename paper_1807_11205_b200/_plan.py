@@ -97,6 +97,34 @@ def step_params(*, eta: float, epsilon: float, gamma: float, weight_decay: float
     return p
 
 
+def launch_hint(p: np.ndarray, g_is_f16: bool) -> int:
+    """GS_HINT_* bits for a step-params struct, filling in `mul`.
+
+    POW2: the mean and unscale divisions are exact power-of-two scalings that
+    compose into one multiplication: for fp16 input every widened value is
+    0 or >= 2^-24 in magnitude, so x * rcp1 is exact and x*rcp1*rcp2 rounds
+    once either way.  fp32 input qualifies only without divisors.
+    RAWFLAG: fp16 input and mul <= 1, so no finite value can overflow and the
+    finite tests reduce to the binary16 exponent field.
+    """
+    mode = int(p["mode"][0])
+    div1, div2 = mode & _native.MODE_DIV1, mode & _native.MODE_DIV2
+    ok = g_is_f16 or not (div1 or div2)
+    if div1 and not mode & _native.MODE_DIV1_POW2:
+        ok = False
+    if div2 and not mode & _native.MODE_DIV2_POW2:
+        ok = False
+    hint = _native.HINT_GRADNORM if mode & _native.MODE_GRADNORM else 0
+    if ok:
+        mul = (float(p["rcp1"][0]) if div1 else 1.0) * (float(p["rcp2"][0]) if div2 else 1.0)
+        if 2.0 ** -100 <= mul <= 2.0 ** 100:
+            p["mul"] = np.float32(mul)
+            hint |= _native.HINT_POW2
+            if g_is_f16 and mul <= 1.0:
+                hint |= _native.HINT_RAWFLAG
+    return hint
+
+
 @dataclass
 class SegmentSpec:
     g: int
@@ -105,6 +133,7 @@ class SegmentSpec:
     w16: int
     n: int
     flags: int
+    gcopy: int = 0
 
 
 class LarsPlan:
@@ -121,11 +150,14 @@ class LarsPlan:
             segs[i]["g"], segs[i]["w"], segs[i]["v"], segs[i]["w16"] = s.g, s.w, s.v, s.w16
             segs[i]["n"] = s.n
             segs[i]["flags"] = s.flags
+            segs[i]["gcopy"] = s.gcopy
         segs["chunk_begin"] = begin
         segs["chunk_count"] = count
         self.host_segs, self.host_chunks = segs, chunks
         self.nchunk = len(chunks)
         self.d_segs = dev.upload(segs, device)
+        self.base_segs = self.d_segs
+        self._alt: dict = {}
         self.d_chunks = dev.upload(chunks, device)
         self.partials = torch.zeros(max(1, 3 * self.nchunk), dtype=torch.float64, device=device)
         self.seg_scale = torch.zeros(max(1, self.nseg), dtype=torch.float32, device=device)
@@ -142,14 +174,44 @@ class LarsPlan:
                                   device=device)
         self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
                                           dtype=torch.uint8).pin_memory()
+        self.hint = 0
+
+    def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
+        """A segment table identical to the base one except for the gradient
+        (and gcopy) pointers, uploaded once per pointer set and cached."""
+        key = (tuple(g_ptrs), tuple(gcopy_ptrs) if gcopy_ptrs is not None else None)
+        tab = self._alt.get(key)
+        if tab is None:
+            segs = self.host_segs.copy()
+            segs["g"] = np.asarray(g_ptrs, dtype=np.uint64)
+            if gcopy_ptrs is not None:
+                segs["gcopy"] = np.asarray(gcopy_ptrs, dtype=np.uint64)
+            if len(self._alt) > 8:
+                self._alt.clear()
+            tab = self._alt[key] = dev.upload(segs, self.device)
+        return tab
+
+    def use_segments(self, table: torch.Tensor | None) -> None:
+        """Select the segment table the next launches run over (None = base)."""
+        self.d_segs = self.base_segs if table is None else table
 
     # -- individual launches (all async on `stream`) --------------------
-    def set_params(self, params: np.ndarray, stream=None) -> None:
-        """Stage the step scalars into the device struct.  The pinned staging
-        buffer is reused, so the caller must not call this again before the
-        previous copy executed (lars_step syncs every call; the pipeline keeps
-        its own double buffer)."""
+    def set_params(self, params: np.ndarray, stream=None, g_is_f16: bool = False) -> None:
+        """Stage the step scalars into the device struct and derive the launch
+        hint.  The pinned staging buffer is reused, so the caller must not call
+        this again before the previous copy executed (lars_step and the
+        pipeline both sync on the step's flags every step)."""
+        self.stage_params(params, g_is_f16)
+        self.upload_params(stream)
+
+    def stage_params(self, params: np.ndarray, g_is_f16: bool = False) -> int:
+        """Host half of set_params: hint + pinned staging (no CUDA call)."""
+        self.hint = launch_hint(params, g_is_f16)
         self._pinned_params.numpy()[:] = params.view(np.uint8).reshape(-1)
+        return self.hint
+
+    def upload_params(self, stream=None) -> None:
+        """Device half of set_params: one 56-byte async copy."""
         s = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             self.params.copy_(self._pinned_params, non_blocking=True)
@@ -168,13 +230,13 @@ class LarsPlan:
         if fuse and self.fused:
             _native.call("gs_lars_pass1_trust", dev.ptr(self.d_segs), self.nseg, self.nseg_active,
                          dev.ptr(self.d_chunks), chunk0, n, 1 if g_is_f16 else 0,
-                         dev.ptr(self.params), dev.ptr(self.partials), dev.ptr(self.flags),
+                         dev.ptr(self.params), self.hint, dev.ptr(self.partials), dev.ptr(self.flags),
                          dev.ptr(self.counters), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
                          dev.ptr(self.grad_norm), stream_h)
         else:
             _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
-                         1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.partials),
-                         dev.ptr(self.flags), stream_h)
+                         1 if g_is_f16 else 0, dev.ptr(self.params), self.hint,
+                         dev.ptr(self.partials), dev.ptr(self.flags), stream_h)
 
     def trust(self, stream_h: int):
         _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
@@ -185,7 +247,7 @@ class LarsPlan:
               nchunk: int | None = None):
         n = self.nchunk - chunk0 if nchunk is None else nchunk
         _native.call("gs_lars_pass2", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
-                     1 if g_is_f16 else 0, dev.ptr(self.params), dev.ptr(self.seg_scale),
+                     1 if g_is_f16 else 0, dev.ptr(self.params), self.hint, dev.ptr(self.seg_scale),
                      dev.ptr(self.flags), flag_mask, stream_h)
 
     def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:

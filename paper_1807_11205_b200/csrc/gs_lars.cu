@@ -9,98 +9,196 @@
 //                          scale = f32(local*gamma), v = m*v + scale*eff,
 //                          w -= v, w16 = f32_to_f16(w)
 //
-// Three kernels, all HBM-bound (no tensor cores: nothing is a contraction):
-//   pass1  reads g (2 B fp16 or 4 B fp32) + w (4 B, LARS groups only) and
-//          emits per-chunk fp64 partials {sum w^2, sum eff^2, sum g^2} and
-//          the two non-finite flag bits;                       6 B/elem
-//   trust  one CTA folds the partials per segment in fixed chunk order and
-//          evaluates the trust ratio in fp64;                 O(#chunks)
-//   pass2  early-exits on the flags, otherwise reads g, w, v and writes
-//          v, w, w16;                                          20 B/elem
-// Chunks never straddle a segment, so a CTA handles one (segment, range)
-// pair with uniform control flow, and its partial sums land in a fixed slot:
-// the reduction order depends only on the chunk table, never on timing.
+// Kernels (all HBM-bound; no tensor cores — nothing here is a contraction):
+//   pass1        reads g (2 B fp16 or 4 B fp32) + w (4 B, LARS groups only),
+//                optionally writes the raw g chunk into the fusion wire
+//                (gs_segment.gcopy, the fused packer), emits per-chunk fp64
+//                partials {sum w^2, sum eff^2, sum g^2} and the two
+//                non-finite flag bits.                     6 (+2) B/elem
+//   pass1_trust  pass1 + the trust ratio: the last CTA of every segment folds
+//                the segment's partials in chunk order (no extra launch).
+//   trust        the same fold as a separate single-CTA kernel.
+//   pass2        early-exits on the flags, otherwise reads g, w, v and writes
+//                v, w, w16.                                 20 B/elem
+// Chunks never straddle a segment, so a CTA handles one (segment, range) pair
+// with uniform control flow, and its partial sums land in a fixed slot: the
+// reduction order depends only on the chunk table, never on timing.
+//
+// Specialisation (host hints, gradsync_b200.h GS_HINT_*): with power-of-two p
+// and loss scale the mean and unscale are one exact multiplication by `mul`
+// (packed f32x2), and for fp16 input with mul <= 1 the finite tests reduce to
+// an integer test of the binary16 exponent field; full 8192-element chunks
+// issue all their loads before any arithmetic.
 #include "gs_common.cuh"
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kRounds = 4;                      // 8-element vectors per thread
+constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
-
-template <bool F16>
-struct GradIO;
-
-template <>
-struct GradIO<true> {
-  using T = uint16_t;
-  static __device__ __forceinline__ void load8(const T* p, float (&g)[8]) {
-    const uint4 r = *reinterpret_cast<const uint4*>(p);
-    const float2 a = gs::widen2(r.x), b = gs::widen2(r.y), c = gs::widen2(r.z), d = gs::widen2(r.w);
-    g[0] = a.x; g[1] = a.y; g[2] = b.x; g[3] = b.y;
-    g[4] = c.x; g[5] = c.y; g[6] = d.x; g[7] = d.y;
-  }
-  static __device__ __forceinline__ float load1(const T* p) { return gs::widen(*p); }
-};
-
-template <>
-struct GradIO<false> {
-  using T = float;
-  static __device__ __forceinline__ void load8(const T* p, float (&g)[8]) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w;
-    g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
-  }
-  static __device__ __forceinline__ float load1(const T* p) { return *p; }
-};
-
-__device__ __forceinline__ void load8f(const float* p, float (&x)[8]) {
-  const float4 a = reinterpret_cast<const float4*>(p)[0];
-  const float4 b = reinterpret_cast<const float4*>(p)[1];
-  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-  x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-}
-
-__device__ __forceinline__ void store8f(float* p, const float (&x)[8]) {
-  reinterpret_cast<float4*>(p)[0] = make_float4(x[0], x[1], x[2], x[3]);
-  reinterpret_cast<float4*>(p)[1] = make_float4(x[4], x[5], x[6], x[7]);
-}
+constexpr uint32_t kBoth = GS_FLAG_SCALED_NONFINITE | GS_FLAG_GRAD_NONFINITE;
 
 __device__ __forceinline__ void sq_acc(double& acc, float x) {
   const double d = (double)x;
   acc = fma(d, d, acc);
 }
 
-// ----------------------------------------------------------------- pass 1
-template <bool F16, bool LARS>
-__device__ __forceinline__ void pass1_body(const typename GradIO<F16>::T* __restrict__ g,
-                                           const float* __restrict__ w, int len, const gs::Unscale& u,
-                                           bool decay, float wd, bool gnorm, double& sw, double& se,
-                                           double& sg, uint32_t& fl) {
-  auto elem = [&](float graw, float wv) {
-    const float gm = u.mean(graw);
-    fl |= gs::is_finite_f32(gm) ? 0u : GS_FLAG_SCALED_NONFINITE;
-    const float gu = u.unscale(gm);
-    fl |= gs::is_finite_f32(gu) ? 0u : GS_FLAG_GRAD_NONFINITE;
-    if (LARS) {
-      const float eff = decay ? __fadd_rn(gu, __fmul_rn(wd, wv)) : gu;
-      sq_acc(sw, wv);
-      sq_acc(se, eff);
+// raw binary16 non-finite detector for two halves in one word: adding 0x0400
+// to an all-ones exponent field carries into the (masked-off) sign position
+__device__ __forceinline__ uint32_t raw_nonfinite_bits(uint32_t w) {
+  return (w & 0x7C007C00u) + 0x04000400u;
+}
+
+struct Ctx {
+  gs::Unscale u;
+  float mul, wd, m;
+};
+
+struct Acc {
+  double sw = 0.0, se = 0.0, sg = 0.0;
+  uint32_t fl = 0u, raw = 0u;
+};
+
+// ------------------------------------------------------------ pass 1 body
+// One element pair (x = widened gradient, w = master).
+template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& a) {
+  float2 gu;
+  if (POW2) {
+    gu = __fmul2_rn(x, make_float2(cx.mul, cx.mul));
+    if (!RAWFLAG) {
+      // the mean x/p (p >= 1) is non-finite iff x is; the unscaled value
+      // can additionally overflow when mul > 1
+      a.fl |= (gs::is_finite_f32(x.x) && gs::is_finite_f32(x.y)) ? 0u : kBoth;
+      a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
     }
-    if (gnorm) sq_acc(sg, gu);
-  };
-  const bool vec = gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w));
-  const int nv = vec ? len / 8 : 0;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < nv; i += kThreads) {
-    float gf[8], wf[8];
-    GradIO<F16>::load8(g + 8 * i, gf);
-    if (LARS) load8f(w + 8 * i, wf);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) elem(gf[k], LARS ? wf[k] : 0.0f);
+  } else {
+    const float mx = cx.u.mean(x.x), my = cx.u.mean(x.y);
+    a.fl |= (gs::is_finite_f32(mx) && gs::is_finite_f32(my)) ? 0u : GS_FLAG_SCALED_NONFINITE;
+    gu = make_float2(cx.u.unscale(mx), cx.u.unscale(my));
+    a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
   }
-  for (int i = nv * 8 + threadIdx.x; i < len; i += kThreads)
-    elem(GradIO<F16>::load1(g + i), LARS ? w[i] : 0.0f);
+  if (LARS) {
+    sq_acc(a.sw, w.x);
+    sq_acc(a.sw, w.y);
+    if (DECAY) {
+      // eff = g + float32(wd) * w, two roundings (lars.py:172)
+      const float2 eff = __fadd2_rn(gu, __fmul2_rn(make_float2(cx.wd, cx.wd), w));
+      sq_acc(a.se, eff.x);
+      sq_acc(a.se, eff.y);
+    }
+  }
+  if (GNORM || (LARS && !DECAY)) {
+    sq_acc(a.sg, gu.x);
+    sq_acc(a.sg, gu.y);
+  }
+}
+
+template <bool F16>
+struct G;
+template <>
+struct G<true> {
+  using T = uint16_t;
+  using V = uint4;  // 8 halves
+  static __device__ __forceinline__ V ld(const T* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+  static __device__ __forceinline__ float2 pair(const V& v, int q) {
+    return gs::widen2((&v.x)[q]);
+  }
+  static __device__ __forceinline__ float one(const T* p) { return gs::widen(*p); }
+};
+struct F8 {
+  float4 a, b;
+};
+template <>
+struct G<false> {
+  using T = float;
+  using V = F8;
+  static __device__ __forceinline__ V ld(const T* p) {
+    return F8{__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
+  }
+  static __device__ __forceinline__ float2 pair(const V& v, int q) {
+    return q == 0 ? make_float2(v.a.x, v.a.y) : q == 1 ? make_float2(v.a.z, v.a.w)
+         : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);
+  }
+  static __device__ __forceinline__ float one(const T* p) { return *p; }
+};
+
+__device__ __forceinline__ F8 ldw(const float* p) {
+  return F8{__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
+}
+__device__ __forceinline__ float2 wpair(const F8& v, int q) {
+  return q == 0 ? make_float2(v.a.x, v.a.y) : q == 1 ? make_float2(v.a.z, v.a.w)
+       : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& wv, const Ctx& cx,
+                                       Acc& a) {
+  if (RAWFLAG) {
+    const uint4& r = reinterpret_cast<const uint4&>(gv);
+    a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
+             raw_nonfinite_bits(r.w);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(G<F16>::pair(gv, q),
+                                               LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ g,
+                                         const float* __restrict__ w, uint16_t* __restrict__ gcopy,
+                                         int len, const Ctx& cx, Acc& a) {
+  using Gt = G<F16>;
+  const bool vec = gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w)) &&
+                   (gcopy == nullptr || gs::is_aligned16(gcopy));
+  const int nv = vec ? len / 8 : 0;
+  const int t = threadIdx.x;
+  if (nv == kFullChunk / 8) {
+    // full chunk: issue every load of the thread first (4 x 16 B of g and
+    // 4 x 32 B of w in flight), then the arithmetic
+    typename Gt::V gv[kRounds];
+    F8 wv[kRounds];
+#pragma unroll
+    for (int k = 0; k < kRounds; ++k) gv[k] = Gt::ld(g + 8 * (t + k * kThreads));
+    if (LARS) {
+#pragma unroll
+      for (int k = 0; k < kRounds; ++k) wv[k] = ldw(w + 8 * (t + k * kThreads));
+    }
+    if (F16 && gcopy != nullptr) {
+#pragma unroll
+      for (int k = 0; k < kRounds; ++k)
+        reinterpret_cast<uint4*>(gcopy)[t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kRounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
+    return;
+  }
+  for (int i = t; i < nv; i += kThreads) {
+    const typename Gt::V gv = Gt::ld(g + 8 * i);
+    F8 wv{};
+    if (LARS) wv = ldw(w + 8 * i);
+    if (F16 && gcopy != nullptr) reinterpret_cast<uint4*>(gcopy)[i] = reinterpret_cast<const uint4&>(gv);
+    p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv, wv, cx, a);
+  }
+  // scalar tail (and misaligned segments): pair the element with a zero
+  // partner that contributes nothing
+  for (int i = nv * 8 + t; i < len; i += kThreads) {
+    if (F16) {
+      const uint16_t h = reinterpret_cast<const uint16_t*>(g)[i];
+      if (gcopy != nullptr) gcopy[i] = h;
+      if (RAWFLAG) a.raw |= raw_nonfinite_bits(h);
+    }
+    const float x = Gt::one(g + i);
+    const float wx = LARS ? w[i] : 0.0f;
+    Acc b;
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(make_float2(x, 0.0f), make_float2(wx, 0.0f), cx, b);
+    a.sw += b.sw;
+    a.se += b.se;
+    a.sg += b.sg;
+    a.fl |= b.fl;
+  }
 }
 
 // lars_local_lr (lars.py:142-150) + lars.py:177 for one segment: norms are
@@ -131,14 +229,12 @@ __device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg
   return __dsqrt_rn(acc);
 }
 
-// FUSE = false: plain pass 1 (partials + flags).
-// FUSE = true : additionally the last CTA to finish a segment (per-segment
-// arrival counter) folds that segment's partials in chunk order and writes its
-// trust ratio, and the last segment to finish writes the grad norm and the
-// empty segments — the trust step costs no extra launch and no tail.  Which
-// CTA arrives last is timing-dependent; the result is not: the fold always
-// runs over the same chunk range in the same fixed tree.
-template <bool F16, bool FUSE>
+// FUSE: the last CTA to finish a segment (per-segment arrival counter) folds
+// that segment's partials in chunk order and writes its trust ratio; the last
+// segment to finish writes the empty segments and the grad norm.  Which CTA
+// arrives last is timing-dependent, the result is not: the fold always runs
+// over the same chunk range in the same fixed tree.
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
 __global__ void __launch_bounds__(kThreads)
 lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                   const gs_chunk* __restrict__ chunks, int chunk0,
@@ -146,33 +242,42 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
                   uint32_t* __restrict__ flags, uint32_t* __restrict__ counters,
                   float* __restrict__ seg_scale, double* __restrict__ seg_out,
                   double* __restrict__ grad_norm_out) {
-  using T = typename GradIO<F16>::T;
+  using T = typename G<F16>::T;
   const int c = chunk0 + blockIdx.x;
   const gs_chunk ch = chunks[c];
-  const gs_segment* sg = segs + ch.seg;
-  const uint32_t sflags = sg->flags;
-  const T* g = static_cast<const T*>(sg->g) + ch.start;
-  const float* w = sg->w + ch.start;
-  gs::Unscale u;
-  u.load(params);
-  const float wd = params->weight_decay;
-  const bool decay = (u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
-  const bool gnorm = (u.mode & GS_MODE_GRADNORM) != 0;
-  double sw = 0.0, se = 0.0, sgn = 0.0;
-  uint32_t fl = 0;
-  if (sflags & GS_SEG_LARS_ENABLED)
-    pass1_body<F16, true>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, fl);
+  const gs_segment* sgp = segs + ch.seg;
+  const uint32_t sflags = sgp->flags;
+  const T* g = static_cast<const T*>(sgp->g) + ch.start;
+  const float* w = sgp->w + ch.start;
+  uint16_t* gcopy = F16 && sgp->gcopy != nullptr ? static_cast<uint16_t*>(sgp->gcopy) + ch.start
+                                                 : nullptr;
+  Ctx cx;
+  cx.u.load(params);
+  cx.mul = params->mul;
+  cx.wd = params->weight_decay;
+  const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
+  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
+  Acc a;
+  if (lars && decay)
+    p1_chunk<F16, POW2, RAWFLAG, GNORM, true, true>(g, w, gcopy, ch.len, cx, a);
+  else if (lars)
+    p1_chunk<F16, POW2, RAWFLAG, GNORM, true, false>(g, w, gcopy, ch.len, cx, a);
   else
-    pass1_body<F16, false>(g, w, ch.len, u, decay, wd, gnorm, sw, se, sgn, fl);
-
+    p1_chunk<F16, POW2, RAWFLAG, GNORM, false, false>(g, w, gcopy, ch.len, cx, a);
+  if (lars && !decay) {
+    a.se = a.sg;  // eff == g exactly: same terms, same order
+    if (!GNORM) a.sg = 0.0;
+  }
+  uint32_t fl = a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
   fl = __reduce_or_sync(0xFFFFFFFFu, fl);
   if (fl != 0u && (threadIdx.x & 31) == 0) atomicOr(flags, fl);
-  gs::block_sum3<kThreads>(sw, se, sgn);
+  double sw = a.sw, se = a.se, sg = a.sg;
+  gs::block_sum3<kThreads>(sw, se, sg);
   if (!FUSE) {
     if (threadIdx.x == 0) {
       partials[3 * (int64_t)c + 0] = sw;
       partials[3 * (int64_t)c + 1] = se;
-      partials[3 * (int64_t)c + 2] = sgn;
+      partials[3 * (int64_t)c + 2] = sg;
     }
     return;
   }
@@ -180,27 +285,27 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
   if (threadIdx.x == 0) {
     partials[3 * (int64_t)c + 0] = sw;
     partials[3 * (int64_t)c + 1] = se;
-    partials[3 * (int64_t)c + 2] = sgn;
+    partials[3 * (int64_t)c + 2] = sg;
     __threadfence();
     const uint32_t prev = atomicAdd(&counters[ch.seg], 1u);
-    s_last = (prev + 1 == (uint32_t)sg->chunk_count);
+    s_last = (prev + 1 == (uint32_t)sgp->chunk_count);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   // fold this segment's chunk partials: fixed strided order + fixed tree
-  const int cb = sg->chunk_begin, cn = sg->chunk_count;
-  double a = 0.0, b = 0.0, d = 0.0;
+  const int cb = sgp->chunk_begin, cn = sgp->chunk_count;
+  double x = 0.0, y = 0.0, z = 0.0;
   for (int i = threadIdx.x; i < cn; i += kThreads) {
     const double* pp = partials + 3 * (int64_t)(cb + i);
-    a += __ldcg(pp + 0);
-    b += __ldcg(pp + 1);
-    d += __ldcg(pp + 2);
+    x += __ldcg(pp + 0);
+    y += __ldcg(pp + 1);
+    z += __ldcg(pp + 2);
   }
   __syncthreads();  // block_sum3's shared scratch is reused
-  gs::block_sum3<kThreads>(a, b, d);
+  gs::block_sum3<kThreads>(x, y, z);
   if (threadIdx.x == 0) {
-    trust_eval(sflags, a, b, d, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
+    trust_eval(sflags, x, y, z, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
     __threadfence();
     const uint32_t prev = atomicAdd(&counters[nseg], 1u);
     if (prev + 1 == (uint32_t)nseg_active) {
@@ -240,64 +345,125 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* _
 }
 
 // ----------------------------------------------------------------- pass 2
-template <bool F16>
-__global__ void __launch_bounds__(kThreads)
-lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int chunk0,
-                  const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
-                  const uint32_t* __restrict__ flags, uint32_t flag_mask) {
-  using T = typename GradIO<F16>::T;
-  // lars.py:161-163 — a non-finite step mutates nothing
-  if (*flags & flag_mask) return;
-  const int c = chunk0 + blockIdx.x;
-  const gs_chunk ch = chunks[c];
-  const gs_segment* sg = segs + ch.seg;
-  const uint32_t sflags = sg->flags;
-  const T* __restrict__ g = static_cast<const T*>(sg->g) + ch.start;
-  float* __restrict__ w = sg->w + ch.start;
-  float* __restrict__ v = sg->v + ch.start;
-  uint16_t* __restrict__ w16 = sg->w16 + ch.start;
-  gs::Unscale u;
-  u.load(params);
-  const float wd = params->weight_decay;
-  const float m = params->momentum;
-  const float s = seg_scale[ch.seg];
-  const bool decay = (u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
-  const int len = ch.len;
+// v = m*v + s*eff (lars.py:178), w -= v (:179), w16 = f32_to_f16(w) (:180),
+// eff = g or g + wd*w (:169-172); every product and sum rounded separately.
+template <bool POW2, bool DECAY>
+__device__ __forceinline__ void p2_pair(float2 x, float2& w, float2& v, const Ctx& cx, float s) {
+  float2 gu;
+  if (POW2) {
+    gu = __fmul2_rn(x, make_float2(cx.mul, cx.mul));
+  } else {
+    gu = make_float2(cx.u.unscale(cx.u.mean(x.x)), cx.u.unscale(cx.u.mean(x.y)));
+  }
+  const float2 eff = DECAY ? __fadd2_rn(gu, __fmul2_rn(make_float2(cx.wd, cx.wd), w)) : gu;
+  v = __fadd2_rn(__fmul2_rn(make_float2(cx.m, cx.m), v), __fmul2_rn(make_float2(s, s), eff));
+  w = __fadd2_rn(w, make_float2(-v.x, -v.y));  // w - v, exact negation then one rounding
+}
 
-  auto upd = [&](float graw, float& wv, float& vv) {
-    const float gu = u.unscale(u.mean(graw));
-    const float eff = decay ? __fadd_rn(gu, __fmul_rn(wd, wv)) : gu;  // lars.py:172
-    vv = __fadd_rn(__fmul_rn(m, vv), __fmul_rn(s, eff));               // lars.py:178
-    wv = __fsub_rn(wv, vv);                                             // lars.py:179
-  };
+// binary16 pack with NaN canonicalisation for two lanes
+__device__ __forceinline__ uint32_t pack_w16(float2 w) {
+  __half2 h = __floats2half2_rn(w.x, w.y);
+  uint32_t bits = *reinterpret_cast<uint32_t*>(&h);
+  // any half with |h| > 0x7C00 is a NaN: force 0x7E00 (halfprec.py:76-77)
+  const uint32_t nan = __vcmpgtu2(bits & 0x7FFF7FFFu, 0x7C007C00u);
+  return (bits & ~nan) | (0x7E007E00u & nan);
+}
 
+template <bool F16, bool POW2, bool DECAY>
+__device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ g,
+                                         float* __restrict__ w, float* __restrict__ v,
+                                         uint16_t* __restrict__ w16, int len, const Ctx& cx,
+                                         float s) {
+  using Gt = G<F16>;
   const bool vec = gs::is_aligned16(g) && gs::is_aligned16(w) && gs::is_aligned16(v) &&
                    gs::is_aligned16(w16);
   const int nv = vec ? len / 8 : 0;
 #pragma unroll 2
   for (int i = threadIdx.x; i < nv; i += kThreads) {
-    float gf[8], wf[8], vf[8];
-    GradIO<F16>::load8(g + 8 * i, gf);
-    load8f(w + 8 * i, wf);
-    load8f(v + 8 * i, vf);
+    const typename Gt::V gv = Gt::ld(g + 8 * i);
+    float4* wp = reinterpret_cast<float4*>(w + 8 * i);
+    float4* vp = reinterpret_cast<float4*>(v + 8 * i);
+    const float4 wa = wp[0], wb = wp[1], va = vp[0], vb = vp[1];
+    float2 ww[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
+                    make_float2(wb.z, wb.w)};
+    float2 vv[4] = {make_float2(va.x, va.y), make_float2(va.z, va.w), make_float2(vb.x, vb.y),
+                    make_float2(vb.z, vb.w)};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) upd(gf[k], wf[k], vf[k]);
-    store8f(v + 8 * i, vf);
-    store8f(w + 8 * i, wf);
-    uint4 h;
-    h.x = gs::narrow2(wf[0], wf[1]);
-    h.y = gs::narrow2(wf[2], wf[3]);
-    h.z = gs::narrow2(wf[4], wf[5]);
-    h.w = gs::narrow2(wf[6], wf[7]);
-    *reinterpret_cast<uint4*>(w16 + 8 * i) = h;  // lars.py:180
+    for (int q = 0; q < 4; ++q) p2_pair<POW2, DECAY>(Gt::pair(gv, q), ww[q], vv[q], cx, s);
+    vp[0] = make_float4(vv[0].x, vv[0].y, vv[1].x, vv[1].y);
+    vp[1] = make_float4(vv[2].x, vv[2].y, vv[3].x, vv[3].y);
+    wp[0] = make_float4(ww[0].x, ww[0].y, ww[1].x, ww[1].y);
+    wp[1] = make_float4(ww[2].x, ww[2].y, ww[3].x, ww[3].y);
+    reinterpret_cast<uint4*>(w16)[i] = make_uint4(pack_w16(ww[0]), pack_w16(ww[1]),
+                                                  pack_w16(ww[2]), pack_w16(ww[3]));
   }
   for (int i = nv * 8 + threadIdx.x; i < len; i += kThreads) {
-    float wv = w[i], vv = v[i];
-    upd(GradIO<F16>::load1(g + i), wv, vv);
-    v[i] = vv;
-    w[i] = wv;
-    w16[i] = gs::narrow(wv);
+    float2 ww = make_float2(w[i], 0.0f), vv = make_float2(v[i], 0.0f);
+    p2_pair<POW2, DECAY>(make_float2(Gt::one(g + i), 0.0f), ww, vv, cx, s);
+    v[i] = vv.x;
+    w[i] = ww.x;
+    w16[i] = gs::narrow(ww.x);
   }
+}
+
+template <bool F16, bool POW2>
+__global__ void __launch_bounds__(kThreads)
+lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int chunk0,
+                  const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
+                  const uint32_t* __restrict__ flags, uint32_t flag_mask) {
+  using T = typename G<F16>::T;
+  // lars.py:161-163 — a non-finite step mutates nothing
+  if (*flags & flag_mask) return;
+  const int c = chunk0 + blockIdx.x;
+  const gs_chunk ch = chunks[c];
+  const gs_segment* sgp = segs + ch.seg;
+  const uint32_t sflags = sgp->flags;
+  const T* g = static_cast<const T*>(sgp->g) + ch.start;
+  float* w = sgp->w + ch.start;
+  float* v = sgp->v + ch.start;
+  uint16_t* w16 = sgp->w16 + ch.start;
+  Ctx cx;
+  cx.u.load(params);
+  cx.mul = params->mul;
+  cx.wd = params->weight_decay;
+  cx.m = params->momentum;
+  const float s = seg_scale[ch.seg];
+  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
+  if (decay)
+    p2_chunk<F16, POW2, true>(g, w, v, w16, ch.len, cx, s);
+  else
+    p2_chunk<F16, POW2, false>(g, w, v, w16, ch.len, cx, s);
+}
+
+// ------------------------------------------------------------ dispatch
+template <bool FUSE>
+int launch_pass1(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
+                 int chunk0, int nchunk, int f16, const gs_step_params* params, uint32_t hint,
+                 double* partials, uint32_t* flags, uint32_t* counters, float* seg_scale,
+                 double* seg_out, double* gn, cudaStream_t s) {
+  const bool pow2 = hint & GS_HINT_POW2, raw = f16 && pow2 && (hint & GS_HINT_RAWFLAG),
+             gnorm = hint & GS_HINT_GRADNORM;
+#define GS_P1(F, P, R, N)                                                                      \
+  lars_pass1_kernel<F, P, R, N, FUSE><<<nchunk, kThreads, 0, s>>>(                             \
+      segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,    \
+      seg_out, gn)
+  if (f16) {
+    if (raw) {
+      if (gnorm) GS_P1(true, true, true, true); else GS_P1(true, true, true, false);
+    } else if (pow2) {
+      if (gnorm) GS_P1(true, true, false, true); else GS_P1(true, true, false, false);
+    } else {
+      if (gnorm) GS_P1(true, false, false, true); else GS_P1(true, false, false, false);
+    }
+  } else {
+    if (pow2) {
+      if (gnorm) GS_P1(false, true, false, true); else GS_P1(false, true, false, false);
+    } else {
+      if (gnorm) GS_P1(false, false, false, true); else GS_P1(false, false, false, false);
+    }
+  }
+#undef GS_P1
+  return gs_check_launch(FUSE ? "gs_lars_pass1_trust" : "gs_lars_pass1");
 }
 
 }  // namespace
@@ -305,41 +471,28 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
 extern "C" {
 
 int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, double* partials, uint32_t* flags,
-                  void* stream) {
+                  int g_is_f16, const gs_step_params* params, uint32_t hint, double* partials,
+                  uint32_t* flags, void* stream) {
   GS_REQUIRE(nchunk >= 0 && chunk0 >= 0, "gs_lars_pass1: bad chunk range");
   if (nchunk == 0) return GS_OK;
   GS_REQUIRE(segs && chunks && params && partials && flags, "gs_lars_pass1: null pointer");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (g_is_f16)
-    lars_pass1_kernel<true, false><<<nchunk, kThreads, 0, s>>>(
-        segs, 0, 0, chunks, chunk0, params, partials, flags, nullptr, nullptr, nullptr, nullptr);
-  else
-    lars_pass1_kernel<false, false><<<nchunk, kThreads, 0, s>>>(
-        segs, 0, 0, chunks, chunk0, params, partials, flags, nullptr, nullptr, nullptr, nullptr);
-  return gs_check_launch("gs_lars_pass1");
+  return launch_pass1<false>(segs, 0, 0, chunks, chunk0, nchunk, g_is_f16, params, hint, partials,
+                             flags, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
                         int chunk0, int nchunk, int g_is_f16, const gs_step_params* params,
-                        double* partials, uint32_t* flags, uint32_t* counters, float* seg_scale,
-                        double* seg_out, double* grad_norm_out, void* stream) {
+                        uint32_t hint, double* partials, uint32_t* flags, uint32_t* counters,
+                        float* seg_scale, double* seg_out, double* grad_norm_out, void* stream) {
   GS_REQUIRE(nchunk >= 0 && chunk0 >= 0, "gs_lars_pass1_trust: bad chunk range");
   GS_REQUIRE(nseg_active >= 1 && nseg_active <= nseg,
              "gs_lars_pass1_trust: need 1 <= nseg_active <= nseg (use gs_lars_trust otherwise)");
   if (nchunk == 0) return GS_OK;
   GS_REQUIRE(segs && chunks && params && partials && flags && counters && seg_scale && seg_out,
              "gs_lars_pass1_trust: null pointer");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (g_is_f16)
-    lars_pass1_kernel<true, true><<<nchunk, kThreads, 0, s>>>(
-        segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,
-        seg_out, grad_norm_out);
-  else
-    lars_pass1_kernel<false, true><<<nchunk, kThreads, 0, s>>>(
-        segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,
-        seg_out, grad_norm_out);
-  return gs_check_launch("gs_lars_pass1_trust");
+  return launch_pass1<true>(segs, nseg, nseg_active, chunks, chunk0, nchunk, g_is_f16, params, hint,
+                            partials, flags, counters, seg_scale, seg_out, grad_norm_out,
+                            (cudaStream_t)stream);
 }
 
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
@@ -354,18 +507,22 @@ int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
 }
 
 int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, const float* seg_scale,
-                  const uint32_t* flags, uint32_t flag_mask, void* stream) {
+                  int g_is_f16, const gs_step_params* params, uint32_t hint,
+                  const float* seg_scale, const uint32_t* flags, uint32_t flag_mask,
+                  void* stream) {
   GS_REQUIRE(nchunk >= 0 && chunk0 >= 0, "gs_lars_pass2: bad chunk range");
   if (nchunk == 0) return GS_OK;
   GS_REQUIRE(segs && chunks && params && seg_scale && flags, "gs_lars_pass2: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  if (g_is_f16)
-    lars_pass2_kernel<true><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, seg_scale, flags,
-                                                        flag_mask);
-  else
-    lars_pass2_kernel<false><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, seg_scale,
-                                                         flags, flag_mask);
+  const bool pow2 = hint & GS_HINT_POW2;
+#define GS_P2(F, P) \
+  lars_pass2_kernel<F, P><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, seg_scale, flags, flag_mask)
+  if (g_is_f16) {
+    if (pow2) GS_P2(true, true); else GS_P2(true, false);
+  } else {
+    if (pow2) GS_P2(false, true); else GS_P2(false, false);
+  }
+#undef GS_P2
   return gs_check_launch("gs_lars_pass2");
 }
 

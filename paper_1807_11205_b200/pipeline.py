@@ -139,7 +139,7 @@ class GradientPipeline:
                  loss_scale: LossScale | None = None, order=None, comm=None,
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
-                 local_workers: int = 1, use_graph: bool = True):
+                 local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -201,6 +201,11 @@ class GradientPipeline:
         self._pack_cache: dict = {}
         self.use_graph = use_graph
         self._graphs: dict = {}
+        # p = 1: pass 1 reads the gradients where they lie and writes the wire
+        # copy itself (gs_segment.gcopy), so packing costs no extra launch and
+        # no re-read of the wire
+        self.fused_pack = fused_pack and comm is None and not self.local
+        self._prepared = None
         self._grad_arena = None
         self._pack_stream = torch.cuda.Stream(device=d) if comm is not None else None
         if self.local:
@@ -301,26 +306,49 @@ class GradientPipeline:
                            unscale_divisor=self.loss_scale.scale,
                            grad_norm=self.grad_norm_enabled)
 
+    def prepare(self, step: int) -> None:
+        """Host-only part of a step (schedule, loss scale, launch hint) so the
+        device part can be enqueued without host work in between."""
+        self.plan.stage_params(self.params_for(step), g_is_f16=True)
+        self._prepared = step
+
+    def _sources(self, grads):
+        """(launch tables, graph key) for this gradient set."""
+        if self.local:
+            if len(grads) != self.p:
+                raise ValueError(f"expected gradients of {self.p} workers, got {len(grads)}")
+            tabs = [self._tables_for(self._grad_views(g), w) for g, w in zip(grads, self.rank_wire)]
+            return tabs, tuple(id(t) for t in tabs)
+        views = self._grad_views(grads)
+        if self.fused_pack:
+            for t, n in zip(views, self.sizes):
+                if t.numel() != n or t.dtype not in (torch.uint16, torch.float16) or not t.is_cuda:
+                    raise ValueError("gradients must be CUDA fp16/uint16 tensors of the "
+                                     "parameter sizes")
+            wb = self.wire.data_ptr()
+            tab = self.plan.alt_segments([t.data_ptr() for t in views],
+                                         [wb + 2 * o for o in self.wire_off])
+            return ("fused", tab), id(tab)
+        tabs = self._tables_for(views, self.wire)
+        return tabs, id(tabs)
+
     def enqueue(self, grads, step: int, timer=None) -> None:
         """Launch one step on the current stream (no host sync).
 
         `timer`, if given, is called with a phase name before each phase
         (the bench records CUDA events there); timed launches run eagerly.
         Otherwise, with comm=None and use_graph, the kernel sequence is
-        captured once per gradient-buffer set into a CUDA graph and replayed:
-        the per-step scalars live in device memory (gs_step_params), so a
-        replay picks up the new loss scale / learning rate.
+        captured once per (gradient-buffer set, launch hint) into a CUDA graph
+        and replayed: the per-step scalars live in device memory
+        (gs_step_params), so a replay picks up the new loss scale / rate.
         """
         s0 = torch.cuda.current_stream(self.device)
-        if self.local:
-            if len(grads) != self.p:
-                raise ValueError(f"expected gradients of {self.p} workers, got {len(grads)}")
-            tabs = [self._tables_for(self._grad_views(g), w) for g, w in zip(grads, self.rank_wire)]
-            key = tuple(id(t) for t in tabs)
-        else:
-            tabs = self._tables_for(self._grad_views(grads), self.wire)
-            key = id(tabs)
-        self.plan.set_params(self.params_for(step), s0)
+        if self._prepared != step:
+            self.prepare(step)
+        self._prepared = None
+        tabs, key = self._sources(grads)
+        key = (key, self.plan.hint)
+        self.plan.upload_params(s0)
         if timer is not None or not self.use_graph or self.comm is not None:
             self._launch(tabs, s0, timer)
             return
@@ -346,8 +374,14 @@ class GradientPipeline:
     def _launch(self, tabs, s0, timer) -> None:
         plan = self.plan
         sh = int(s0.cuda_stream)
+        fused = isinstance(tabs, tuple) and tabs[0] == "fused"
+        plan.use_segments(tabs[1] if fused else None)
         plan.reset_flags(sh)
-        if self.comm is None:
+        if fused:
+            if timer:
+                timer("pass1")
+            plan.pass1(sh, g_is_f16=True)
+        elif self.comm is None:
             if timer:
                 timer("pack")
             for b in range(len(self.buckets)):
@@ -397,6 +431,7 @@ class GradientPipeline:
             timer("pass2")
         plan.pass2(sh, g_is_f16=True,
                    flag_mask=_native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE)
+        plan.use_segments(None)
         if timer:
             timer("end")
 

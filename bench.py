@@ -276,6 +276,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     step_ms = []
     for i in range(args.steps):
         flush_l2()
+        pipe.prepare(args.warmup + i)  # host-only: schedule, loss scale, hint
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s0)

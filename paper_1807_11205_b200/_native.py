@@ -34,6 +34,7 @@ FLAG_GRAD_NONFINITE = 2
 HINT_POW2 = 1
 HINT_RAWFLAG = 2
 HINT_GRADNORM = 4
+HINT_NO_BULK = 8
 
 # numpy mirrors of the device structs (layout asserted against the header)
 SEGMENT_DTYPE = np.dtype([

@@ -175,6 +175,7 @@ class LarsPlan:
         self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
                                           dtype=torch.uint8).pin_memory()
         self.hint = 0
+        self.extra_hint = 0   # e.g. _native.HINT_NO_BULK to force the register-staged pass 1
 
     def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
         """A segment table identical to the base one except for the gradient
@@ -206,7 +207,7 @@ class LarsPlan:
 
     def stage_params(self, params: np.ndarray, g_is_f16: bool = False) -> int:
         """Host half of set_params: hint + pinned staging (no CUDA call)."""
-        self.hint = launch_hint(params, g_is_f16)
+        self.hint = launch_hint(params, g_is_f16) | self.extra_hint
         self._pinned_params.numpy()[:] = params.view(np.uint8).reshape(-1)
         return self.hint
 

@@ -26,7 +26,7 @@
 //
 // Specialisation (host hints, gradsync_b200.h GS_HINT_*): with power-of-two p
 // and loss scale the mean and unscale are one exact multiplication by `mul`
-// (packed f32x2), and for fp16 input with mul <= 1 the finite tests reduce to
+// (one FMUL per element), and for fp16 input with mul <= 1 the finite tests reduce to
 // an integer test of the binary16 exponent field; full 8192-element chunks
 // issue all their loads before any arithmetic.
 #include "gs_common.cuh"
@@ -38,6 +38,20 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
 constexpr uint32_t kBoth = GS_FLAG_SCALED_NONFINITE | GS_FLAG_GRAD_NONFINITE;
+
+// Pairwise fp32 ops, each lane rounded separately.  NOT the packed
+// __fmul2_rn/__fadd2_rn intrinsics: ptxas 12.9 contracts mul.rn.f32x2 feeding
+// add.rn.f32x2 into FFMA2 even under -fmad=false (seen in SASS), which would
+// break the separate roundings numpy performs; scalar mul.rn/add.rn are kept.
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+}
 
 __device__ __forceinline__ void sq_acc(double& acc, float x) {
   const double d = (double)x;
@@ -66,7 +80,7 @@ template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
 __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& a) {
   float2 gu;
   if (POW2) {
-    gu = __fmul2_rn(x, make_float2(cx.mul, cx.mul));
+    gu = mul2(x, make_float2(cx.mul, cx.mul));
     if (!RAWFLAG) {
       // the mean x/p (p >= 1) is non-finite iff x is; the unscaled value
       // can additionally overflow when mul > 1
@@ -84,7 +98,7 @@ __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& 
     sq_acc(a.sw, w.y);
     if (DECAY) {
       // eff = g + float32(wd) * w, two roundings (lars.py:172)
-      const float2 eff = __fadd2_rn(gu, __fmul2_rn(make_float2(cx.wd, cx.wd), w));
+      const float2 eff = add2(gu, mul2(make_float2(cx.wd, cx.wd), w));
       sq_acc(a.se, eff.x);
       sq_acc(a.se, eff.y);
     }
@@ -319,6 +333,180 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
   }
 }
 
+// ------------------------------------------------ pass 1, TMA-pipelined
+// Persistent form of pass 1 for fp16 gradients: every CTA walks the chunks
+// blockIdx.x, blockIdx.x + gridDim.x, ... and streams each chunk's gradient
+// (16 KB) and master (32 KB) into shared memory with bulk-async copies (the
+// TMA engine, cp.async.bulk + mbarrier complete_tx), two stages deep, so the
+// next chunk is in flight while the current one is reduced from shared
+// memory.  The fused packer becomes one bulk shared->global store of the
+// staged gradient into the wire.  Chunks that are not 16-byte aligned (or
+// not a multiple of 8 elements) are processed from global memory directly.
+constexpr int kStageG = kFullChunk * 2;      // 16 KB of binary16
+constexpr int kStageW = kFullChunk * 4;      // 32 KB of fp32 master
+constexpr int kStageBytes = kStageG + kStageW;
+constexpr int kTmaSmem = 2 * kStageBytes + 64;
+
+template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, int len,
+                                        const Ctx& cx, Acc& a) {
+  const int nv = len / 8;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < nv; i += kThreads) {
+    const uint4 gv = reinterpret_cast<const uint4*>(sg)[i];
+    F8 wv{};
+    if (LARS) {
+      wv.a = reinterpret_cast<const float4*>(sw)[2 * i];
+      wv.b = reinterpret_cast<const float4*>(sw)[2 * i + 1];
+    }
+    p1_vec<true, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv, wv, cx, a);
+  }
+}
+
+template <bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
+__global__ void __launch_bounds__(kThreads, 2)
+lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
+                      const gs_chunk* __restrict__ chunks, int chunk0, int nchunk,
+                      const gs_step_params* __restrict__ params, double* __restrict__ partials,
+                      uint32_t* __restrict__ flags, uint32_t* __restrict__ counters,
+                      float* __restrict__ seg_scale, double* __restrict__ seg_out,
+                      double* __restrict__ grad_norm_out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStageBytes);
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  const int nmine = blockIdx.x < nchunk ? (nchunk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (tid == 0) {
+    gs::mbar_init(&bars[0], 1);
+    gs::mbar_init(&bars[1], 1);
+    gs::mbar_fence_init();
+  }
+  __syncthreads();
+  Ctx cx;
+  cx.u.load(params);
+  cx.mul = params->mul;
+  cx.wd = params->weight_decay;
+
+  auto chunk_idx = [&](int k) { return chunk0 + blockIdx.x + k * gridDim.x; };
+  auto bulk_ok = [&](const gs_chunk& ch, const gs_segment* sp) {
+    const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
+    const bool lars = sp->flags & GS_SEG_LARS_ENABLED;
+    return (ch.len & 7) == 0 && gs::is_aligned16(g) && (!lars || gs::is_aligned16(sp->w + ch.start)) &&
+           (sp->gcopy == nullptr || gs::is_aligned16(static_cast<uint16_t*>(sp->gcopy) + ch.start));
+  };
+  auto issue = [&](int k, int stage) {  // thread 0 only
+    const gs_chunk ch = chunks[chunk_idx(k)];
+    const gs_segment* sp = segs + ch.seg;
+    if (!bulk_ok(ch, sp)) return;
+    const bool lars = sp->flags & GS_SEG_LARS_ENABLED;
+    const uint32_t bg = 2u * ch.len, bw = lars ? 4u * ch.len : 0u;
+    uint8_t* st = smem + stage * kStageBytes;
+    gs::mbar_arrive_expect_tx(&bars[stage], bg + bw);
+    gs::bulk_g2s(st, static_cast<const uint16_t*>(sp->g) + ch.start, bg, &bars[stage]);
+    if (bw) gs::bulk_g2s(st + kStageG, sp->w + ch.start, bw, &bars[stage]);
+  };
+  if (tid == 0) {
+    if (nmine > 0) issue(0, 0);
+    if (nmine > 1) issue(1, 1);
+  }
+  uint32_t phase0 = 0, phase1 = 0;
+  bool stores_pending = false;
+  for (int k = 0; k < nmine; ++k) {
+    const int stage = k & 1;
+    const int c = chunk_idx(k);
+    const gs_chunk ch = chunks[c];
+    const gs_segment* sp = segs + ch.seg;
+    const uint32_t sflags = sp->flags;
+    const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
+    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
+    uint16_t* gcopy = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + ch.start : nullptr;
+    Acc a;
+    if (bulk_ok(ch, sp)) {
+      gs::mbar_wait(&bars[stage], stage ? phase1 : phase0);
+      if (stage) phase1 ^= 1u; else phase0 ^= 1u;
+      const uint16_t* sgp = reinterpret_cast<const uint16_t*>(smem + stage * kStageBytes);
+      const float* swp = reinterpret_cast<const float*>(smem + stage * kStageBytes + kStageG);
+      if (gcopy != nullptr && tid == 0) {
+        gs::bulk_s2g(gcopy, sgp, 2u * ch.len);
+        gs::bulk_commit();
+        stores_pending = true;
+      }
+      if (lars && decay)
+        p1_smem<POW2, RAWFLAG, GNORM, true, true>(sgp, swp, ch.len, cx, a);
+      else if (lars)
+        p1_smem<POW2, RAWFLAG, GNORM, true, false>(sgp, swp, ch.len, cx, a);
+      else
+        p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, ch.len, cx, a);
+    } else {
+      const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
+      const float* w = sp->w + ch.start;
+      if (lars && decay)
+        p1_chunk<true, POW2, RAWFLAG, GNORM, true, true>(g, w, gcopy, ch.len, cx, a);
+      else if (lars)
+        p1_chunk<true, POW2, RAWFLAG, GNORM, true, false>(g, w, gcopy, ch.len, cx, a);
+      else
+        p1_chunk<true, POW2, RAWFLAG, GNORM, false, false>(g, w, gcopy, ch.len, cx, a);
+    }
+    if (lars && !decay) {
+      a.se = a.sg;
+      if (!GNORM) a.sg = 0.0;
+    }
+    uint32_t fl = a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
+    fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+    if (fl != 0u && (tid & 31) == 0) atomicOr(flags, fl);
+    double sw = a.sw, se = a.se, sg = a.sg;
+    gs::block_sum3<kThreads>(sw, se, sg);  // every thread is done with this stage
+    if (tid == 0) {
+      partials[3 * (int64_t)c + 0] = sw;
+      partials[3 * (int64_t)c + 1] = se;
+      partials[3 * (int64_t)c + 2] = sg;
+      if (k + 2 < nmine) {
+        if (stores_pending) {
+          gs::bulk_wait_read_all();  // the wire store still reads this stage
+          stores_pending = false;
+        }
+        issue(k + 2, stage);
+      }
+      if (FUSE) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&counters[ch.seg], 1u);
+        s_last = (prev + 1 == (uint32_t)sp->chunk_count);
+      }
+    }
+    if (FUSE) {
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const int cb = sp->chunk_begin, cn = sp->chunk_count;
+        double x = 0.0, y = 0.0, z = 0.0;
+        for (int i = tid; i < cn; i += kThreads) {
+          const double* pp = partials + 3 * (int64_t)(cb + i);
+          x += __ldcg(pp + 0);
+          y += __ldcg(pp + 1);
+          z += __ldcg(pp + 2);
+        }
+        gs::block_sum3<kThreads>(x, y, z);
+        if (tid == 0) {
+          trust_eval(sflags, x, y, z, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
+          __threadfence();
+          const uint32_t prev = atomicAdd(&counters[nseg], 1u);
+          if (prev + 1 == (uint32_t)nseg_active) {
+            __threadfence();
+            for (int s2 = 0; s2 < nseg; ++s2)
+              if (segs[s2].chunk_count == 0)
+                trust_eval(segs[s2].flags, 0.0, 0.0, 0.0, params, seg_scale + s2,
+                           seg_out + 4 * (int64_t)s2);
+            __threadfence();
+            if (grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
+          }
+        }
+      }
+    }
+    __syncthreads();  // block_sum3 scratch and s_last are reused next chunk
+  }
+  if (tid == 0 && stores_pending) gs::bulk_wait_all();
+}
+
 // ----------------------------------------------------------------- trust
 __global__ void __launch_bounds__(kTrustThreads)
 lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* __restrict__ partials,
@@ -351,13 +539,13 @@ template <bool POW2, bool DECAY>
 __device__ __forceinline__ void p2_pair(float2 x, float2& w, float2& v, const Ctx& cx, float s) {
   float2 gu;
   if (POW2) {
-    gu = __fmul2_rn(x, make_float2(cx.mul, cx.mul));
+    gu = mul2(x, make_float2(cx.mul, cx.mul));
   } else {
     gu = make_float2(cx.u.unscale(cx.u.mean(x.x)), cx.u.unscale(cx.u.mean(x.y)));
   }
-  const float2 eff = DECAY ? __fadd2_rn(gu, __fmul2_rn(make_float2(cx.wd, cx.wd), w)) : gu;
-  v = __fadd2_rn(__fmul2_rn(make_float2(cx.m, cx.m), v), __fmul2_rn(make_float2(s, s), eff));
-  w = __fadd2_rn(w, make_float2(-v.x, -v.y));  // w - v, exact negation then one rounding
+  const float2 eff = DECAY ? add2(gu, mul2(make_float2(cx.wd, cx.wd), w)) : gu;
+  v = add2(mul2(make_float2(cx.m, cx.m), v), mul2(make_float2(s, s), eff));
+  w = sub2(w, v);
 }
 
 // binary16 pack with NaN canonicalisation for two lanes
@@ -436,6 +624,36 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
 }
 
 // ------------------------------------------------------------ dispatch
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool P, bool R, bool N, bool FUSE>
+int launch_tma(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks, int chunk0,
+               int nchunk, const gs_step_params* params, double* partials, uint32_t* flags,
+               uint32_t* counters, float* seg_scale, double* seg_out, double* gn, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(lars_pass1_tma_kernel<P, R, N, FUSE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) != cudaSuccess)
+      return gs_check_launch("gs_lars_pass1 (smem attribute)");
+    attr = true;
+  }
+  int grid = 2 * sm_count();
+  if (grid > nchunk) grid = nchunk;
+  lars_pass1_tma_kernel<P, R, N, FUSE><<<grid, kThreads, kTmaSmem, s>>>(
+      segs, nseg, nseg_active, chunks, chunk0, nchunk, params, partials, flags, counters, seg_scale,
+      seg_out, gn);
+  return gs_check_launch(FUSE ? "gs_lars_pass1_trust" : "gs_lars_pass1");
+}
+
 template <bool FUSE>
 int launch_pass1(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
                  int chunk0, int nchunk, int f16, const gs_step_params* params, uint32_t hint,
@@ -443,6 +661,19 @@ int launch_pass1(const gs_segment* segs, int nseg, int nseg_active, const gs_chu
                  double* seg_out, double* gn, cudaStream_t s) {
   const bool pow2 = hint & GS_HINT_POW2, raw = f16 && pow2 && (hint & GS_HINT_RAWFLAG),
              gnorm = hint & GS_HINT_GRADNORM;
+  if (f16 && !(hint & GS_HINT_NO_BULK)) {
+#define GS_T(P, R, N)                                                                              \
+  return launch_tma<P, R, N, FUSE>(segs, nseg, nseg_active, chunks, chunk0, nchunk, params, partials, \
+                                   flags, counters, seg_scale, seg_out, gn, s)
+    if (raw) {
+      if (gnorm) GS_T(true, true, true); else GS_T(true, true, false);
+    } else if (pow2) {
+      if (gnorm) GS_T(true, false, true); else GS_T(true, false, false);
+    } else {
+      if (gnorm) GS_T(false, false, true); else GS_T(false, false, false);
+    }
+#undef GS_T
+  }
 #define GS_P1(F, P, R, N)                                                                      \
   lars_pass1_kernel<F, P, R, N, FUSE><<<nchunk, kThreads, 0, s>>>(                             \
       segs, nseg, nseg_active, chunks, chunk0, params, partials, flags, counters, seg_scale,    \

@@ -139,7 +139,8 @@ class GradientPipeline:
                  loss_scale: LossScale | None = None, order=None, comm=None,
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
-                 local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True):
+                 local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
+                 bulk: bool = True):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -184,6 +185,8 @@ class GradientPipeline:
                             vb + 4 * self.wire_off[i], hb + 2 * self.wire_off[i], sizes[i],
                             segment_flags(self.groups[i])) for i in range(n)]
         self.plan = LarsPlan(segs, d, order=self.order)
+        if not bulk:
+            self.plan.extra_hint |= _native.HINT_NO_BULK
         begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]
         c = 0
         for b in self.buckets:
@@ -206,6 +209,7 @@ class GradientPipeline:
         # no re-read of the wire
         self.fused_pack = fused_pack and comm is None and not self.local
         self._prepared = None
+        self._src_cache: dict = {}
         self._grad_arena = None
         self._pack_stream = torch.cuda.Stream(device=d) if comm is not None else None
         if self.local:
@@ -313,7 +317,22 @@ class GradientPipeline:
         self._prepared = step
 
     def _sources(self, grads):
-        """(launch tables, graph key) for this gradient set."""
+        """(launch tables, graph key) for this gradient set, cached on the
+        buffer addresses so a steady-state step does no per-tensor host work."""
+        if dev.is_tensor(grads):
+            ck = (grads.data_ptr(), grads.numel(), grads.dtype)
+        else:
+            ck = tuple((g.data_ptr(), g.numel()) if dev.is_tensor(g) else id(g) for g in grads)
+        hit = self._src_cache.get(ck)
+        if hit is not None:
+            return hit
+        res = self._sources_uncached(grads)
+        if len(self._src_cache) > 16:
+            self._src_cache.clear()
+        self._src_cache[ck] = res
+        return res
+
+    def _sources_uncached(self, grads):
         if self.local:
             if len(grads) != self.p:
                 raise ValueError(f"expected gradients of {self.p} workers, got {len(grads)}")

@@ -42,7 +42,7 @@ def test_abi_version_and_errors_without_gpu():
     assert lib.gs_f32_to_f16(None, None, -1, 1.0, None, None) == -1
     assert b"negative" in lib.gs_last_error()
     assert lib.gs_fold_f16_tree(None, 0, 0, None, 4, None, None) == -1
-    assert lib.gs_lars_pass1(None, None, 0, -1, 1, None, None, None, None) == -1
+    assert lib.gs_lars_pass1(None, None, 0, -1, 1, None, 0, None, None, None) == -1
 
 
 def test_struct_layouts_match_header():
@@ -63,3 +63,25 @@ def test_product_never_imports_oracle():
     pkg = ROOT / "paper_1807_11205_b200"
     for f in pkg.rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", f.read_text(), re.M), f
+
+
+def test_no_packed_fp32_contraction_in_sass():
+    """ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even with
+    -fmad=false; the library must not contain packed fp32 arithmetic at all,
+    and the bit-exact update kernels must not contain FFMA (contracted a*b+c)
+    outside the IEEE-division slow path."""
+    import shutil
+    import subprocess
+    import pytest
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(exe).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([exe, "-sass", str(_build.LIBPATH)], capture_output=True, text=True,
+                          check=True).stdout
+    for op in ("FFMA2", "FADD2", "FMUL2"):
+        assert op not in sass
+    # pass-2 specialisation for power-of-two scaling: pure FMUL/FADD
+    funcs = sass.split("Function : ")
+    p2 = [f for f in funcs if "lars_pass2_kernelILb1ELb1E" in f.split("\n", 1)[0]]
+    assert p2, "pow2 pass-2 kernel missing"
+    assert "FFMA" not in p2[0]

@@ -84,14 +84,14 @@ def test_config1_ordered_matches_reference_golden(golden):
 
 
 def run_vs_oracle(model, p, theta, steps=2, loss_scale=1024.0, wd=5e-4, eta_bytes=0,
-                  inject=None, order=None, specs=None):
+                  inject=None, order=None, specs=None, **kw):
     specs = specs or sh.load_shapes(model)
     master = sh.synth_master(specs, seed=0)
     cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0, weight_decay=wd,
                         momentum=0.9)
     pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=theta, local_workers=p,
                                init_master=master, loss_scale=gs.LossScale(loss_scale),
-                               order=order)
+                               order=order, **kw)
     groups = oracle_groups(specs, master)
     oloss = rp.LossScaleState(loss_scale)
     order = order or list(reversed(range(len(specs))))
@@ -119,8 +119,16 @@ def run_vs_oracle(model, p, theta, steps=2, loss_scale=1024.0, wd=5e-4, eta_byte
     return pipe
 
 
-def test_resnet50_single_gpu_matches_oracle():
-    run_vs_oracle("resnet50", 1, 4 << 20, steps=2)
+@pytest.mark.parametrize("kw", [{}, {"bulk": False}, {"fused_pack": False}, {"use_graph": False}])
+def test_resnet50_single_gpu_matches_oracle(kw):
+    pipe = run_vs_oracle("resnet50", 1, 4 << 20, steps=3, **kw)
+    # the fused packer left the reference's bucket payloads in the wire
+    specs = sh.load_shapes("resnet50")
+    flat = sh.synth_wire_grads(specs, rank=0, seed=2)
+    parts = split(flat, specs)
+    for b in range(len(pipe.buckets)):
+        want = np.concatenate([parts[i] for i in pipe.buckets[b].params])
+        assert np.array_equal(pipe.bucket_payload(b).cpu().numpy(), want)
 
 
 def test_resnet50_p8_ordered_matches_oracle():

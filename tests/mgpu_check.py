@@ -1,0 +1,122 @@
+"""Multi-GPU parity check of the NCCL pipeline (run on a GPU box, not by pytest):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_check.py
+
+Every rank steps GradientPipeline(comm=Communicator(Topology(N, k))) on its own
+synthetic fp16 gradients; rank 0 recomputes the reference composition with the
+CPU oracle.  Checks per algorithm (ring / hierarchical / sharded):
+  * N = 2: NCCL's fp16 sum of two operands is one correctly rounded add, the
+    same as the reference's pairwise tree -> master/velocity/working and the
+    trust scales must be BIT-EXACT;
+  * N > 2: NCCL's order differs from the tree -> the reduced buckets must be
+    within 2^-9 * sum|x| (test_collectives.py:237-250 bound) and the update,
+    recomputed by the oracle from the GPU's own reduced buckets, bit-exact.
+Also an injected Inf on one rank must skip the step on every rank.
+"""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import paper_1807_11205_b200 as gs  # noqa: E402
+from oracle import reference_port as rp  # noqa: E402
+from paper_1807_11205_b200 import shapes as sh  # noqa: E402
+from paper_1807_11205_b200.dist import Communicator, init_from_env  # noqa: E402
+
+
+def split(flat, specs):
+    out, o = [], 0
+    for s in specs:
+        out.append(flat[o:o + s.numel])
+        o += s.numel
+    return out
+
+
+def main():
+    rank, world, local = init_from_env("nccl")
+    dev = torch.device("cuda", local)
+    model = os.environ.get("MGPU_MODEL", "shufflenet_v2_x0_5")
+    theta = int(os.environ.get("MGPU_THETA", str(256 << 10)))
+    specs = sh.load_shapes(model)
+    master = sh.synth_master(specs)
+    order = list(reversed(range(len(specs))))
+    results = {}
+    for algo, k in (("ring", 1), ("hierarchical", 2), ("sharded", 2)):
+        if world % k or (algo != "ring" and world == 1):
+            continue
+        comm = Communicator(gs.Topology(world, k))
+        cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
+        pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=theta, comm=comm,
+                                   eta_bytes=0 if algo == "ring" else 1 << 62,
+                                   hier_variant=algo if algo != "ring" else "hierarchical",
+                                   init_master=master, loss_scale=gs.LossScale(1024.0), device=dev)
+        groups = [rp.Group(s.name, s.kind, w.copy(), np.zeros(s.numel, np.float32),
+                           np.zeros(s.numel, np.float32), rp.narrow(w))
+                  for s, w in zip(specs, split(master, specs))]
+        oloss = rp.LossScaleState(1024.0)
+        ok = True
+        notes = []
+        for step in range(3):
+            wires = [sh.synth_wire_grads(specs, rank=r, seed=step, loss_scale=oloss.scale)
+                     for r in range(world)]
+            if step == 2:
+                wires[world - 1][4321] = 0x7C00
+            res = pipe.step(torch.from_numpy(wires[rank]).to(dev), step)
+            reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]
+            if rank == 0:
+                parts = [split(w, specs) for w in wires]
+                exact = world == 2
+                out = rp.compose_step_fp16(parts, [s.name for s in specs], [s.numel for s in specs],
+                                           order, groups, rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1,
+                                           oloss, theta, 0,
+                                           reduced_override=None if exact else reduced)
+                if not exact:
+                    # reduced buckets within the reference's fp16 bound
+                    tree = rp.compose_step_fp16  # noqa: F841 (documentation)
+                    for b, bk in enumerate(pipe.buckets):
+                        xs = np.stack([np.concatenate([parts[r][i] for i in bk.params])
+                                       for r in range(world)])
+                        bound = 2.0 ** -9 * np.abs(rp.widen(xs)).sum(0)
+                        fin = np.isfinite(bound)
+                        err = np.abs(rp.widen(reduced[b]) - rp.fold_ascending(list(rp.widen(xs))))
+                        if not np.all(err[fin] <= bound[fin] + 2.0 ** -24):
+                            ok = False
+                            notes.append(f"step {step} bucket {b}: fp16 sum outside 2^-9 bound")
+                if res.applied != out.applied:
+                    ok = False
+                    notes.append(f"step {step}: applied {res.applied} vs {out.applied}")
+                got = pipe.registration_view(pipe.master).cpu().numpy()
+                want = np.concatenate([g.master for g in groups])
+                if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+                    ok = False
+                    notes.append(f"step {step}: master differs in "
+                                 f"{int((got.view(np.uint32) != want.view(np.uint32)).sum())} elems")
+                gotv = pipe.registration_view(pipe.velocity).cpu().numpy()
+                wantv = np.concatenate([g.velocity for g in groups])
+                if not np.array_equal(gotv.view(np.uint32), wantv.view(np.uint32)):
+                    ok = False
+                    notes.append(f"step {step}: velocity differs")
+                if out.applied and not np.array_equal(pipe.seg_scales(), out.scales):
+                    ok = False
+                    notes.append(f"step {step}: trust scales differ")
+            flag = torch.tensor([0 if res.applied else 1], device=dev)
+            dist.all_reduce(flag)
+            if step == 2 and int(flag) != world:
+                ok = False
+                notes.append("injected Inf did not skip on every rank")
+        results[algo] = {"ok": ok, "notes": notes[:5], "k": k}
+    if rank == 0:
+        print(json.dumps({"world": world, "model": model, "theta": theta, "results": results}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,7 +48,8 @@ def ncu_raw(rep):
                 if k in ("dram_read", "dram_write"):
                     v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
                 if k == "duration":
-                    v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(u, 1)
+                    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3,
+                          "ms": 1e3}.get(u, 1)
                 d[k] = v
         res.append(d)
     return res
@@ -63,7 +64,8 @@ def launches(csv_path):
     for r in rows[hdr_i + 1:]:
         if len(r) > vi:
             v = float(r[vi].replace(",", ""))
-            v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(r[ui], 1)
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3,
+                  "ms": 1e3}.get(r[ui], 1)
             agg[r[ki].split("(")[0]].append(v)
     return agg
 

@@ -334,18 +334,45 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
 }
 
 // ------------------------------------------------ pass 1, TMA-pipelined
-// Persistent form of pass 1 for fp16 gradients: every CTA walks the chunks
-// blockIdx.x, blockIdx.x + gridDim.x, ... and streams each chunk's gradient
-// (16 KB) and master (32 KB) into shared memory with bulk-async copies (the
-// TMA engine, cp.async.bulk + mbarrier complete_tx), two stages deep, so the
-// next chunk is in flight while the current one is reduced from shared
-// memory.  The fused packer becomes one bulk shared->global store of the
-// staged gradient into the wire.  Chunks that are not 16-byte aligned (or
-// not a multiple of 8 elements) are processed from global memory directly.
+// Persistent, warp-specialised form of pass 1 for fp16 gradients (one CTA per
+// SM).  Warp 8 is the producer: for every chunk of the CTA (chunks
+// blockIdx.x, blockIdx.x + gridDim.x, ...) it waits for a free stage of a
+// kStages-deep ring, arms the stage's `full` mbarrier with the byte count and
+// streams the chunk's gradient (16 KB) and master (32 KB) into shared memory
+// with bulk-async copies (the TMA engine: cp.async.bulk + complete_tx).
+// Warps 0-7 are consumers: they wait on `full`, reduce the chunk from shared
+// memory, hand their warp partial over through shared memory and release the
+// stage on its `empty` mbarrier — no __syncthreads in the loop.  The last
+// consumer warp of a chunk (shared-memory arrival counter) folds the 8 warp
+// partials in warp order into the chunk partial and, for the fused trust,
+// does the per-segment arrival; so the chunk partial and everything after it
+// are identical to the register-staged kernel.  The fused packer is one bulk
+// shared->global store of the staged gradient into the wire.  Chunks that are
+// not 16-byte aligned (or not a multiple of 8 elements) are reduced from
+// global memory directly by the consumers.
+constexpr int kStages = 4;
 constexpr int kStageG = kFullChunk * 2;      // 16 KB of binary16
 constexpr int kStageW = kFullChunk * 4;      // 32 KB of fp32 master
 constexpr int kStageBytes = kStageG + kStageW;
-constexpr int kTmaSmem = 2 * kStageBytes + 64;
+constexpr int kConsumerWarps = kThreads / 32;  // 8
+constexpr int kTmaThreads = kThreads + 32;     // + producer warp
+
+struct StageMeta {
+  int64_t start;
+  int32_t seg;
+  int32_t len;
+  int32_t bulk;  // staged in shared memory (else: consumers read global)
+  int32_t chunk;
+};
+
+struct TmaShared {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  StageMeta meta[kStages];
+  double red[kStages][kConsumerWarps][3];
+  uint32_t cnt[kStages];
+};
+constexpr int kTmaSmem = kStages * kStageBytes + (int)sizeof(TmaShared);
 
 template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
 __device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, int len,
@@ -363,8 +390,89 @@ __device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, int
   }
 }
 
+// chunk reduced straight from global memory (misaligned / odd-length chunks)
+template <bool POW2, bool RAWFLAG, bool GNORM>
+__device__ __noinline__ void p1_global_chunk(const gs_segment* __restrict__ sp, const StageMeta& m,
+                                             const Ctx& cx, Acc& a) {
+  const uint16_t* g = static_cast<const uint16_t*>(sp->g) + m.start;
+  const float* w = sp->w + m.start;
+  uint16_t* gcopy = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + m.start : nullptr;
+  const bool lars = (sp->flags & GS_SEG_LARS_ENABLED) != 0;
+  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sp->flags & GS_SEG_DECAY_EXEMPT);
+  if (lars && decay)
+    p1_chunk<true, POW2, RAWFLAG, GNORM, true, true>(g, w, gcopy, m.len, cx, a);
+  else if (lars)
+    p1_chunk<true, POW2, RAWFLAG, GNORM, true, false>(g, w, gcopy, m.len, cx, a);
+  else
+    p1_chunk<true, POW2, RAWFLAG, GNORM, false, false>(g, w, gcopy, m.len, cx, a);
+}
+
+// Chunk partial + (FUSE) segment arrival, trust fold, empty segments and
+// grad norm — executed by the one warp that completed the chunk.
+template <bool FUSE>
+__device__ __noinline__ void finish_chunk_warp(const gs_segment* __restrict__ segs, int nseg,
+                                               int nseg_active, int c, int seg, double sw,
+                                               double se, double sg,
+                                               const gs_step_params* __restrict__ params,
+                                               double* __restrict__ partials,
+                                               uint32_t* __restrict__ counters,
+                                               float* __restrict__ seg_scale,
+                                               double* __restrict__ seg_out,
+                                               double* __restrict__ grad_norm_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t last = 0;
+  if (lane == 0) {
+    partials[3 * (int64_t)c + 0] = sw;
+    partials[3 * (int64_t)c + 1] = se;
+    partials[3 * (int64_t)c + 2] = sg;
+    if (FUSE) {
+      __threadfence();
+      last = (atomicAdd(&counters[seg], 1u) + 1 == (uint32_t)segs[seg].chunk_count);
+    }
+  }
+  if (!FUSE) return;
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  __threadfence();
+  // fold the segment's chunk partials in a fixed order: the block-wide fold
+  // of the register-staged kernel (256 lanes strided, warps in order) done by
+  // one warp, so both kernels produce the same bits
+  const gs_segment* sp = segs + seg;
+  const int cb = sp->chunk_begin, cn = sp->chunk_count;
+  double x = 0.0, y = 0.0, z = 0.0;
+  for (int w8 = 0; w8 < kConsumerWarps; ++w8) {
+    double px = 0.0, py = 0.0, pz = 0.0;
+    for (int i = w8 * 32 + lane; i < cn; i += kThreads) {
+      const double* pp = partials + 3 * (int64_t)(cb + i);
+      px += __ldcg(pp + 0);
+      py += __ldcg(pp + 1);
+      pz += __ldcg(pp + 2);
+    }
+    px = gs::warp_sum(px);
+    py = gs::warp_sum(py);
+    pz = gs::warp_sum(pz);
+    if (w8 == 0) {
+      x = px; y = py; z = pz;
+    } else {
+      x += px; y += py; z += pz;
+    }
+  }
+  if (lane == 0) {
+    trust_eval(sp->flags, x, y, z, params, seg_scale + seg, seg_out + 4 * (int64_t)seg);
+    __threadfence();
+    if (atomicAdd(&counters[nseg], 1u) + 1 == (uint32_t)nseg_active) {
+      __threadfence();
+      for (int s2 = 0; s2 < nseg; ++s2)
+        if (segs[s2].chunk_count == 0)
+          trust_eval(segs[s2].flags, 0.0, 0.0, 0.0, params, seg_scale + s2, seg_out + 4 * (int64_t)s2);
+      __threadfence();
+      if (grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
+    }
+  }
+}
+
 template <bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kTmaThreads, 1)
 lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                       const gs_chunk* __restrict__ chunks, int chunk0, int nchunk,
                       const gs_step_params* __restrict__ params, double* __restrict__ partials,
@@ -372,80 +480,82 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
                       float* __restrict__ seg_scale, double* __restrict__ seg_out,
                       double* __restrict__ grad_norm_out) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kStageBytes);
-  __shared__ int s_last;
-  const int tid = threadIdx.x;
+  TmaShared& sh = *reinterpret_cast<TmaShared*>(smem + kStages * kStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nmine = blockIdx.x < nchunk ? (nchunk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  if (tid == 0) {
-    gs::mbar_init(&bars[0], 1);
-    gs::mbar_init(&bars[1], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      gs::mbar_init(&sh.full[s], 1);
+      gs::mbar_init(&sh.empty[s], kConsumerWarps);
+      sh.cnt[s] = 0;
+    }
     gs::mbar_fence_init();
   }
   __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------ producer warp
+    if (lane == 0) {
+      for (int k = 0; k < nmine; ++k) {
+        const int s = k % kStages;
+        const uint32_t ph = (uint32_t)(k / kStages) & 1u;
+        gs::mbar_wait(&sh.empty[s], ph ^ 1u);  // fresh barrier: passes at once
+        const int c = chunk0 + blockIdx.x + k * gridDim.x;
+        const gs_chunk ch = chunks[c];
+        const gs_segment* sp = segs + ch.seg;
+        const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
+        const bool lars = (sp->flags & GS_SEG_LARS_ENABLED) != 0;
+        const bool bulk = (ch.len & 7) == 0 && gs::is_aligned16(g) &&
+                          (!lars || gs::is_aligned16(sp->w + ch.start)) &&
+                          (sp->gcopy == nullptr ||
+                           gs::is_aligned16(static_cast<uint16_t*>(sp->gcopy) + ch.start));
+        sh.meta[s] = StageMeta{ch.start, ch.seg, ch.len, bulk ? 1 : 0, c};
+        if (bulk) {
+          const uint32_t bg = 2u * ch.len, bw = lars ? 4u * ch.len : 0u;
+          uint8_t* st = smem + s * kStageBytes;
+          gs::mbar_arrive_expect_tx(&sh.full[s], bg + bw);
+          gs::bulk_g2s(st, g, bg, &sh.full[s]);
+          if (bw) gs::bulk_g2s(st + kStageG, sp->w + ch.start, bw, &sh.full[s]);
+        } else {
+          gs::mbar_arrive_expect_tx(&sh.full[s], 0);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------ consumer warps
   Ctx cx;
   cx.u.load(params);
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
-
-  auto chunk_idx = [&](int k) { return chunk0 + blockIdx.x + k * gridDim.x; };
-  auto bulk_ok = [&](const gs_chunk& ch, const gs_segment* sp) {
-    const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
-    const bool lars = sp->flags & GS_SEG_LARS_ENABLED;
-    return (ch.len & 7) == 0 && gs::is_aligned16(g) && (!lars || gs::is_aligned16(sp->w + ch.start)) &&
-           (sp->gcopy == nullptr || gs::is_aligned16(static_cast<uint16_t*>(sp->gcopy) + ch.start));
-  };
-  auto issue = [&](int k, int stage) {  // thread 0 only
-    const gs_chunk ch = chunks[chunk_idx(k)];
-    const gs_segment* sp = segs + ch.seg;
-    if (!bulk_ok(ch, sp)) return;
-    const bool lars = sp->flags & GS_SEG_LARS_ENABLED;
-    const uint32_t bg = 2u * ch.len, bw = lars ? 4u * ch.len : 0u;
-    uint8_t* st = smem + stage * kStageBytes;
-    gs::mbar_arrive_expect_tx(&bars[stage], bg + bw);
-    gs::bulk_g2s(st, static_cast<const uint16_t*>(sp->g) + ch.start, bg, &bars[stage]);
-    if (bw) gs::bulk_g2s(st + kStageG, sp->w + ch.start, bw, &bars[stage]);
-  };
-  if (tid == 0) {
-    if (nmine > 0) issue(0, 0);
-    if (nmine > 1) issue(1, 1);
-  }
-  uint32_t phase0 = 0, phase1 = 0;
   bool stores_pending = false;
   for (int k = 0; k < nmine; ++k) {
-    const int stage = k & 1;
-    const int c = chunk_idx(k);
-    const gs_chunk ch = chunks[c];
-    const gs_segment* sp = segs + ch.seg;
+    const int s = k % kStages;
+    const uint32_t ph = (uint32_t)(k / kStages) & 1u;
+    gs::mbar_wait(&sh.full[s], ph);
+    const StageMeta m = sh.meta[s];
+    const gs_segment* sp = segs + m.seg;
     const uint32_t sflags = sp->flags;
     const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
     const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
-    uint16_t* gcopy = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + ch.start : nullptr;
     Acc a;
-    if (bulk_ok(ch, sp)) {
-      gs::mbar_wait(&bars[stage], stage ? phase1 : phase0);
-      if (stage) phase1 ^= 1u; else phase0 ^= 1u;
-      const uint16_t* sgp = reinterpret_cast<const uint16_t*>(smem + stage * kStageBytes);
-      const float* swp = reinterpret_cast<const float*>(smem + stage * kStageBytes + kStageG);
-      if (gcopy != nullptr && tid == 0) {
-        gs::bulk_s2g(gcopy, sgp, 2u * ch.len);
+    if (m.bulk) {
+      const uint16_t* sgp = reinterpret_cast<const uint16_t*>(smem + s * kStageBytes);
+      const float* swp = reinterpret_cast<const float*>(smem + s * kStageBytes + kStageG);
+      if (threadIdx.x == 0 && sp->gcopy != nullptr) {
+        gs::bulk_s2g(static_cast<uint16_t*>(sp->gcopy) + m.start, sgp, 2u * m.len);
         gs::bulk_commit();
         stores_pending = true;
       }
       if (lars && decay)
-        p1_smem<POW2, RAWFLAG, GNORM, true, true>(sgp, swp, ch.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, true, true>(sgp, swp, m.len, cx, a);
       else if (lars)
-        p1_smem<POW2, RAWFLAG, GNORM, true, false>(sgp, swp, ch.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, true, false>(sgp, swp, m.len, cx, a);
       else
-        p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, ch.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, m.len, cx, a);
     } else {
-      const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
-      const float* w = sp->w + ch.start;
-      if (lars && decay)
-        p1_chunk<true, POW2, RAWFLAG, GNORM, true, true>(g, w, gcopy, ch.len, cx, a);
-      else if (lars)
-        p1_chunk<true, POW2, RAWFLAG, GNORM, true, false>(g, w, gcopy, ch.len, cx, a);
-      else
-        p1_chunk<true, POW2, RAWFLAG, GNORM, false, false>(g, w, gcopy, ch.len, cx, a);
+      p1_global_chunk<POW2, RAWFLAG, GNORM>(sp, m, cx, a);
     }
     if (lars && !decay) {
       a.se = a.sg;
@@ -453,58 +563,44 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
     }
     uint32_t fl = a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
     fl = __reduce_or_sync(0xFFFFFFFFu, fl);
-    if (fl != 0u && (tid & 31) == 0) atomicOr(flags, fl);
-    double sw = a.sw, se = a.se, sg = a.sg;
-    gs::block_sum3<kThreads>(sw, se, sg);  // every thread is done with this stage
-    if (tid == 0) {
-      partials[3 * (int64_t)c + 0] = sw;
-      partials[3 * (int64_t)c + 1] = se;
-      partials[3 * (int64_t)c + 2] = sg;
-      if (k + 2 < nmine) {
-        if (stores_pending) {
-          gs::bulk_wait_read_all();  // the wire store still reads this stage
-          stores_pending = false;
-        }
-        issue(k + 2, stage);
-      }
-      if (FUSE) {
-        __threadfence();
-        const uint32_t prev = atomicAdd(&counters[ch.seg], 1u);
-        s_last = (prev + 1 == (uint32_t)sp->chunk_count);
-      }
+    const double sw = gs::warp_sum(a.sw), se = gs::warp_sum(a.se), sg = gs::warp_sum(a.sg);
+    uint32_t order = 0;
+    if (lane == 0) {
+      if (fl) atomicOr(flags, fl);
+      sh.red[s][warp][0] = sw;
+      sh.red[s][warp][1] = se;
+      sh.red[s][warp][2] = sg;
+      __threadfence_block();
+      order = atomicAdd(&sh.cnt[s], 1u);
     }
-    if (FUSE) {
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        const int cb = sp->chunk_begin, cn = sp->chunk_count;
-        double x = 0.0, y = 0.0, z = 0.0;
-        for (int i = tid; i < cn; i += kThreads) {
-          const double* pp = partials + 3 * (int64_t)(cb + i);
-          x += __ldcg(pp + 0);
-          y += __ldcg(pp + 1);
-          z += __ldcg(pp + 2);
-        }
-        gs::block_sum3<kThreads>(x, y, z);
-        if (tid == 0) {
-          trust_eval(sflags, x, y, z, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
-          __threadfence();
-          const uint32_t prev = atomicAdd(&counters[nseg], 1u);
-          if (prev + 1 == (uint32_t)nseg_active) {
-            __threadfence();
-            for (int s2 = 0; s2 < nseg; ++s2)
-              if (segs[s2].chunk_count == 0)
-                trust_eval(segs[s2].flags, 0.0, 0.0, 0.0, params, seg_scale + s2,
-                           seg_out + 4 * (int64_t)s2);
-            __threadfence();
-            if (grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
-          }
-        }
+    order = __shfl_sync(0xFFFFFFFFu, order, 0);
+    double tw = 0.0, te = 0.0, tg = 0.0;
+    if (order == kConsumerWarps - 1) {
+      // last warp of this chunk: fold the warp partials in warp order
+      __threadfence_block();
+      tw = sh.red[s][0][0];
+      te = sh.red[s][0][1];
+      tg = sh.red[s][0][2];
+#pragma unroll
+      for (int i = 1; i < kConsumerWarps; ++i) {
+        tw += sh.red[s][i][0];
+        te += sh.red[s][i][1];
+        tg += sh.red[s][i][2];
       }
+      if (lane == 0) sh.cnt[s] = 0;
     }
-    __syncthreads();  // block_sum3 scratch and s_last are reused next chunk
+    // release the stage (the wire store must have read it first)
+    if (stores_pending && threadIdx.x == 0) {
+      gs::bulk_wait_read_all();
+      stores_pending = false;
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gs::smem_u32(&sh.empty[s])) : "memory");
+    if (order == kConsumerWarps - 1)
+      finish_chunk_warp<FUSE>(segs, nseg, nseg_active, m.chunk, m.seg, tw, te, tg, params, partials,
+                              counters, seg_scale, seg_out, grad_norm_out);
   }
-  if (tid == 0 && stores_pending) gs::bulk_wait_all();
+  if (threadIdx.x == 0) gs::bulk_wait_all();
 }
 
 // ----------------------------------------------------------------- trust
@@ -558,6 +654,31 @@ __device__ __forceinline__ uint32_t pack_w16(float2 w) {
 }
 
 template <bool F16, bool POW2, bool DECAY>
+__device__ __forceinline__ void p2_vec(const typename G<F16>::V& gv, const F8& wv, const F8& vv,
+                                       float* __restrict__ w, float* __restrict__ v,
+                                       uint16_t* __restrict__ w16, int i, const Ctx& cx, float s) {
+  float2 ww[4] = {make_float2(wv.a.x, wv.a.y), make_float2(wv.a.z, wv.a.w),
+                  make_float2(wv.b.x, wv.b.y), make_float2(wv.b.z, wv.b.w)};
+  float2 xv[4] = {make_float2(vv.a.x, vv.a.y), make_float2(vv.a.z, vv.a.w),
+                  make_float2(vv.b.x, vv.b.y), make_float2(vv.b.z, vv.b.w)};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) p2_pair<POW2, DECAY>(G<F16>::pair(gv, q), ww[q], xv[q], cx, s);
+  float4* vp = reinterpret_cast<float4*>(v) + 2 * i;
+  float4* wp = reinterpret_cast<float4*>(w) + 2 * i;
+  __stcs(vp, make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y));
+  __stcs(vp + 1, make_float4(xv[2].x, xv[2].y, xv[3].x, xv[3].y));
+  __stcs(wp, make_float4(ww[0].x, ww[0].y, ww[1].x, ww[1].y));
+  __stcs(wp + 1, make_float4(ww[2].x, ww[2].y, ww[3].x, ww[3].y));
+  __stcs(reinterpret_cast<uint4*>(w16) + i,
+         make_uint4(pack_w16(ww[0]), pack_w16(ww[1]), pack_w16(ww[2]), pack_w16(ww[3])));
+}
+
+__device__ __forceinline__ F8 ld8(const float* p, int i) {
+  const float4* q = reinterpret_cast<const float4*>(p) + 2 * i;
+  return F8{q[0], q[1]};
+}
+
+template <bool F16, bool POW2, bool DECAY>
 __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ g,
                                          float* __restrict__ w, float* __restrict__ v,
                                          uint16_t* __restrict__ w16, int len, const Ctx& cx,
@@ -566,26 +687,26 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
   const bool vec = gs::is_aligned16(g) && gs::is_aligned16(w) && gs::is_aligned16(v) &&
                    gs::is_aligned16(w16);
   const int nv = vec ? len / 8 : 0;
-#pragma unroll 2
-  for (int i = threadIdx.x; i < nv; i += kThreads) {
-    const typename Gt::V gv = Gt::ld(g + 8 * i);
-    float4* wp = reinterpret_cast<float4*>(w + 8 * i);
-    float4* vp = reinterpret_cast<float4*>(v + 8 * i);
-    const float4 wa = wp[0], wb = wp[1], va = vp[0], vb = vp[1];
-    float2 ww[4] = {make_float2(wa.x, wa.y), make_float2(wa.z, wa.w), make_float2(wb.x, wb.y),
-                    make_float2(wb.z, wb.w)};
-    float2 vv[4] = {make_float2(va.x, va.y), make_float2(va.z, va.w), make_float2(vb.x, vb.y),
-                    make_float2(vb.z, vb.w)};
+  const int t = threadIdx.x;
+  if (nv == kFullChunk / 8) {
+    // full chunk: two halves of two vectors each; every load of a half is
+    // issued before its arithmetic and stores (stores cannot alias the next
+    // half's loads, but the compiler cannot prove it through the casts)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) p2_pair<POW2, DECAY>(Gt::pair(gv, q), ww[q], vv[q], cx, s);
-    vp[0] = make_float4(vv[0].x, vv[0].y, vv[1].x, vv[1].y);
-    vp[1] = make_float4(vv[2].x, vv[2].y, vv[3].x, vv[3].y);
-    wp[0] = make_float4(ww[0].x, ww[0].y, ww[1].x, ww[1].y);
-    wp[1] = make_float4(ww[2].x, ww[2].y, ww[3].x, ww[3].y);
-    reinterpret_cast<uint4*>(w16)[i] = make_uint4(pack_w16(ww[0]), pack_w16(ww[1]),
-                                                  pack_w16(ww[2]), pack_w16(ww[3]));
+    for (int h = 0; h < kRounds; h += 2) {
+      const int i0 = t + h * kThreads, i1 = i0 + kThreads;
+      const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
+      const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
+      p2_vec<F16, POW2, DECAY>(g0, w0, v0, w, v, w16, i0, cx, s);
+      p2_vec<F16, POW2, DECAY>(g1, w1, v1, w, v, w16, i1, cx, s);
+    }
+    return;
   }
-  for (int i = nv * 8 + threadIdx.x; i < len; i += kThreads) {
+  for (int i = t; i < nv; i += kThreads) {
+    const typename Gt::V gv = Gt::ld(g + 8 * i);
+    p2_vec<F16, POW2, DECAY>(gv, ld8(w, i), ld8(v, i), w, v, w16, i, cx, s);
+  }
+  for (int i = nv * 8 + t; i < len; i += kThreads) {
     float2 ww = make_float2(w[i], 0.0f), vv = make_float2(v[i], 0.0f);
     p2_pair<POW2, DECAY>(make_float2(Gt::one(g + i), 0.0f), ww, vv, cx, s);
     v[i] = vv.x;
@@ -646,9 +767,9 @@ int launch_tma(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk
       return gs_check_launch("gs_lars_pass1 (smem attribute)");
     attr = true;
   }
-  int grid = 2 * sm_count();
+  int grid = sm_count();
   if (grid > nchunk) grid = nchunk;
-  lars_pass1_tma_kernel<P, R, N, FUSE><<<grid, kThreads, kTmaSmem, s>>>(
+  lars_pass1_tma_kernel<P, R, N, FUSE><<<grid, kTmaThreads, kTmaSmem, s>>>(
       segs, nseg, nseg_active, chunks, chunk0, nchunk, params, partials, flags, counters, seg_scale,
       seg_out, gn);
   return gs_check_launch(FUSE ? "gs_lars_pass1_trust" : "gs_lars_pass1");

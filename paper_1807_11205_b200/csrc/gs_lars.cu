@@ -355,14 +355,27 @@ constexpr int kStageG = kFullChunk * 2;      // 16 KB of binary16
 constexpr int kStageW = kFullChunk * 4;      // 32 KB of fp32 master
 constexpr int kStageBytes = kStageG + kStageW;
 constexpr int kConsumerWarps = kThreads / 32;  // 8
-constexpr int kTmaThreads = kThreads + 32;     // + producer warp
+constexpr int kProducerWarp = kConsumerWarps;  // warp 8
+constexpr int kFinisherWarp = kConsumerWarps + 1;  // warp 9
+constexpr int kTmaThreads = kThreads + 64;
+constexpr int kRing = 64;                      // finisher queue entries
 
+// Everything a consumer needs about the staged chunk (written by the
+// producer before it arms the stage; the mbarrier orders it), so consumers
+// never touch global metadata on the critical path.
 struct StageMeta {
-  int64_t start;
-  int32_t seg;
-  int32_t len;
-  int32_t bulk;  // staged in shared memory (else: consumers read global)
-  int32_t chunk;
+  const uint16_t* g;
+  const float* w;
+  uint16_t* gcopy;
+  int32_t len, seg, chunk;
+  uint32_t sflags;
+  int32_t bulk;
+  int32_t pad;
+};
+
+struct FinishItem {
+  double sw, se, sg;
+  int32_t chunk, seg;
 };
 
 struct TmaShared {
@@ -371,6 +384,9 @@ struct TmaShared {
   StageMeta meta[kStages];
   double red[kStages][kConsumerWarps][3];
   uint32_t cnt[kStages];
+  FinishItem ring[kRing];
+  volatile uint32_t ring_tail;  // written by consumers (last warp of a chunk)
+  volatile uint32_t ring_head;  // written by the finisher
 };
 constexpr int kTmaSmem = kStages * kStageBytes + (int)sizeof(TmaShared);
 
@@ -392,39 +408,36 @@ __device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, int
 
 // chunk reduced straight from global memory (misaligned / odd-length chunks)
 template <bool POW2, bool RAWFLAG, bool GNORM>
-__device__ __noinline__ void p1_global_chunk(const gs_segment* __restrict__ sp, const StageMeta& m,
-                                             const Ctx& cx, Acc& a) {
-  const uint16_t* g = static_cast<const uint16_t*>(sp->g) + m.start;
-  const float* w = sp->w + m.start;
-  uint16_t* gcopy = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + m.start : nullptr;
-  const bool lars = (sp->flags & GS_SEG_LARS_ENABLED) != 0;
-  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sp->flags & GS_SEG_DECAY_EXEMPT);
+__device__ __noinline__ void p1_global_chunk(const StageMeta& m, const Ctx& cx, Acc& a) {
+  const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
+  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(m.sflags & GS_SEG_DECAY_EXEMPT);
   if (lars && decay)
-    p1_chunk<true, POW2, RAWFLAG, GNORM, true, true>(g, w, gcopy, m.len, cx, a);
+    p1_chunk<true, POW2, RAWFLAG, GNORM, true, true>(m.g, m.w, m.gcopy, m.len, cx, a);
   else if (lars)
-    p1_chunk<true, POW2, RAWFLAG, GNORM, true, false>(g, w, gcopy, m.len, cx, a);
+    p1_chunk<true, POW2, RAWFLAG, GNORM, true, false>(m.g, m.w, m.gcopy, m.len, cx, a);
   else
-    p1_chunk<true, POW2, RAWFLAG, GNORM, false, false>(g, w, gcopy, m.len, cx, a);
+    p1_chunk<true, POW2, RAWFLAG, GNORM, false, false>(m.g, m.w, m.gcopy, m.len, cx, a);
 }
 
 // Chunk partial + (FUSE) segment arrival, trust fold, empty segments and
-// grad norm — executed by the one warp that completed the chunk.
+// grad norm for one finished chunk — executed by the finisher warp, so its
+// global-memory latency never sits on the consumers' critical path.
 template <bool FUSE>
-__device__ __noinline__ void finish_chunk_warp(const gs_segment* __restrict__ segs, int nseg,
-                                               int nseg_active, int c, int seg, double sw,
-                                               double se, double sg,
-                                               const gs_step_params* __restrict__ params,
-                                               double* __restrict__ partials,
-                                               uint32_t* __restrict__ counters,
-                                               float* __restrict__ seg_scale,
-                                               double* __restrict__ seg_out,
-                                               double* __restrict__ grad_norm_out) {
+__device__ __forceinline__ void finish_chunk_warp(const gs_segment* __restrict__ segs, int nseg,
+                                                  int nseg_active, const FinishItem& it,
+                                                  const gs_step_params* __restrict__ params,
+                                                  double* __restrict__ partials,
+                                                  uint32_t* __restrict__ counters,
+                                                  float* __restrict__ seg_scale,
+                                                  double* __restrict__ seg_out,
+                                                  double* __restrict__ grad_norm_out) {
   const int lane = threadIdx.x & 31;
+  const int c = it.chunk, seg = it.seg;
   uint32_t last = 0;
   if (lane == 0) {
-    partials[3 * (int64_t)c + 0] = sw;
-    partials[3 * (int64_t)c + 1] = se;
-    partials[3 * (int64_t)c + 2] = sg;
+    partials[3 * (int64_t)c + 0] = it.sw;
+    partials[3 * (int64_t)c + 1] = it.se;
+    partials[3 * (int64_t)c + 2] = it.sg;
     if (FUSE) {
       __threadfence();
       last = (atomicAdd(&counters[seg], 1u) + 1 == (uint32_t)segs[seg].chunk_count);
@@ -434,9 +447,9 @@ __device__ __noinline__ void finish_chunk_warp(const gs_segment* __restrict__ se
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
   if (!last) return;
   __threadfence();
-  // fold the segment's chunk partials in a fixed order: the block-wide fold
-  // of the register-staged kernel (256 lanes strided, warps in order) done by
-  // one warp, so both kernels produce the same bits
+  // fold the segment's chunk partials in a fixed order: exactly the
+  // block-wide fold of the register-staged kernel (256 lanes strided, then
+  // warps in order), done by one warp, so both kernels produce the same bits
   const gs_segment* sp = segs + seg;
   const int cb = sp->chunk_begin, cn = sp->chunk_count;
   double x = 0.0, y = 0.0, z = 0.0;
@@ -489,37 +502,81 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
       gs::mbar_init(&sh.empty[s], kConsumerWarps);
       sh.cnt[s] = 0;
     }
+    sh.ring_tail = 0;
+    sh.ring_head = 0;
     gs::mbar_fence_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------ producer warp
-    if (lane == 0) {
-      for (int k = 0; k < nmine; ++k) {
-        const int s = k % kStages;
-        const uint32_t ph = (uint32_t)(k / kStages) & 1u;
-        gs::mbar_wait(&sh.empty[s], ph ^ 1u);  // fresh barrier: passes at once
-        const int c = chunk0 + blockIdx.x + k * gridDim.x;
+    // the 32 lanes fetch the metadata of 32 upcoming chunks at once, so the
+    // dependent chunk -> segment loads cost one latency per 32 chunks
+    StageMeta mine{};
+    for (int base = 0; base < nmine; base += 32) {
+      const int kk = base + lane;
+      if (kk < nmine) {
+        const int c = chunk0 + blockIdx.x + kk * gridDim.x;
         const gs_chunk ch = chunks[c];
         const gs_segment* sp = segs + ch.seg;
+        const uint32_t fl = sp->flags;
         const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
-        const bool lars = (sp->flags & GS_SEG_LARS_ENABLED) != 0;
-        const bool bulk = (ch.len & 7) == 0 && gs::is_aligned16(g) &&
-                          (!lars || gs::is_aligned16(sp->w + ch.start)) &&
-                          (sp->gcopy == nullptr ||
-                           gs::is_aligned16(static_cast<uint16_t*>(sp->gcopy) + ch.start));
-        sh.meta[s] = StageMeta{ch.start, ch.seg, ch.len, bulk ? 1 : 0, c};
-        if (bulk) {
-          const uint32_t bg = 2u * ch.len, bw = lars ? 4u * ch.len : 0u;
-          uint8_t* st = smem + s * kStageBytes;
-          gs::mbar_arrive_expect_tx(&sh.full[s], bg + bw);
-          gs::bulk_g2s(st, g, bg, &sh.full[s]);
-          if (bw) gs::bulk_g2s(st + kStageG, sp->w + ch.start, bw, &sh.full[s]);
-        } else {
-          gs::mbar_arrive_expect_tx(&sh.full[s], 0);
-        }
+        const float* w = sp->w + ch.start;
+        uint16_t* gc = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + ch.start : nullptr;
+        const bool lars = (fl & GS_SEG_LARS_ENABLED) != 0;
+        const bool bulk = (ch.len & 7) == 0 && gs::is_aligned16(g) && (!lars || gs::is_aligned16(w)) &&
+                          (gc == nullptr || gs::is_aligned16(gc));
+        mine = StageMeta{g, w, gc, ch.len, ch.seg, c, fl, bulk ? 1 : 0, 0};
       }
+      const int cnt = min(32, nmine - base);
+      for (int j = 0; j < cnt; ++j) {
+        StageMeta m;
+        m.g = reinterpret_cast<const uint16_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)mine.g, j));
+        m.w = reinterpret_cast<const float*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)mine.w, j));
+        m.gcopy = reinterpret_cast<uint16_t*>(__shfl_sync(0xFFFFFFFFu, (unsigned long long)mine.gcopy, j));
+        m.len = __shfl_sync(0xFFFFFFFFu, mine.len, j);
+        m.seg = __shfl_sync(0xFFFFFFFFu, mine.seg, j);
+        m.chunk = __shfl_sync(0xFFFFFFFFu, mine.chunk, j);
+        m.sflags = __shfl_sync(0xFFFFFFFFu, mine.sflags, j);
+        m.bulk = __shfl_sync(0xFFFFFFFFu, mine.bulk, j);
+        m.pad = 0;
+        const int k = base + j;
+        const int s = k % kStages;
+        const uint32_t ph = (uint32_t)(k / kStages) & 1u;
+        if (lane == 0) {
+          gs::mbar_wait(&sh.empty[s], ph ^ 1u);  // fresh barrier: passes at once
+          sh.meta[s] = m;
+          if (m.bulk) {
+            const uint32_t bg = 2u * m.len;
+            const uint32_t bw = (m.sflags & GS_SEG_LARS_ENABLED) ? 4u * m.len : 0u;
+            uint8_t* st = smem + s * kStageBytes;
+            gs::mbar_arrive_expect_tx(&sh.full[s], bg + bw);
+            gs::bulk_g2s(st, m.g, bg, &sh.full[s]);
+            if (bw) gs::bulk_g2s(st + kStageG, m.w, bw, &sh.full[s]);
+          } else {
+            gs::mbar_arrive_expect_tx(&sh.full[s], 0);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  if (warp == kFinisherWarp) {
+    // ------------------------------------------------------ finisher warp
+    for (int k = 0; k < nmine; ++k) {
+      uint32_t spins = 0;
+      while (sh.ring_tail == (uint32_t)k) {
+        __nanosleep(64);
+        if (++spins > (1u << 26)) __trap();
+      }
+      __threadfence_block();
+      const FinishItem it = sh.ring[k % kRing];
+      finish_chunk_warp<FUSE>(segs, nseg, nseg_active, it, params, partials, counters, seg_scale,
+                              seg_out, grad_norm_out);
+      __syncwarp();
+      if (lane == 0) sh.ring_head = (uint32_t)(k + 1);
     }
     return;
   }
@@ -535,16 +592,14 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
     const uint32_t ph = (uint32_t)(k / kStages) & 1u;
     gs::mbar_wait(&sh.full[s], ph);
     const StageMeta m = sh.meta[s];
-    const gs_segment* sp = segs + m.seg;
-    const uint32_t sflags = sp->flags;
-    const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
-    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
+    const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
+    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(m.sflags & GS_SEG_DECAY_EXEMPT);
     Acc a;
     if (m.bulk) {
       const uint16_t* sgp = reinterpret_cast<const uint16_t*>(smem + s * kStageBytes);
       const float* swp = reinterpret_cast<const float*>(smem + s * kStageBytes + kStageG);
-      if (threadIdx.x == 0 && sp->gcopy != nullptr) {
-        gs::bulk_s2g(static_cast<uint16_t*>(sp->gcopy) + m.start, sgp, 2u * m.len);
+      if (threadIdx.x == 0 && m.gcopy != nullptr) {
+        gs::bulk_s2g(m.gcopy, sgp, 2u * m.len);
         gs::bulk_commit();
         stores_pending = true;
       }
@@ -555,7 +610,7 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
       else
         p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, m.len, cx, a);
     } else {
-      p1_global_chunk<POW2, RAWFLAG, GNORM>(sp, m, cx, a);
+      p1_global_chunk<POW2, RAWFLAG, GNORM>(m, cx, a);
     }
     if (lars && !decay) {
       a.se = a.sg;
@@ -572,22 +627,27 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
       sh.red[s][warp][2] = sg;
       __threadfence_block();
       order = atomicAdd(&sh.cnt[s], 1u);
-    }
-    order = __shfl_sync(0xFFFFFFFFu, order, 0);
-    double tw = 0.0, te = 0.0, tg = 0.0;
-    if (order == kConsumerWarps - 1) {
-      // last warp of this chunk: fold the warp partials in warp order
-      __threadfence_block();
-      tw = sh.red[s][0][0];
-      te = sh.red[s][0][1];
-      tg = sh.red[s][0][2];
+      if (order == kConsumerWarps - 1) {
+        // last warp of this chunk: fold the warp partials in warp order and
+        // queue the chunk for the finisher
+        __threadfence_block();
+        double tw = sh.red[s][0][0], te = sh.red[s][0][1], tg = sh.red[s][0][2];
 #pragma unroll
-      for (int i = 1; i < kConsumerWarps; ++i) {
-        tw += sh.red[s][i][0];
-        te += sh.red[s][i][1];
-        tg += sh.red[s][i][2];
+        for (int i = 1; i < kConsumerWarps; ++i) {
+          tw += sh.red[s][i][0];
+          te += sh.red[s][i][1];
+          tg += sh.red[s][i][2];
+        }
+        sh.cnt[s] = 0;
+        uint32_t spins = 0;
+        while ((uint32_t)k - sh.ring_head >= (uint32_t)kRing) {  // queue full (rare)
+          __nanosleep(64);
+          if (++spins > (1u << 26)) __trap();
+        }
+        sh.ring[k % kRing] = FinishItem{tw, te, tg, m.chunk, m.seg};
+        __threadfence_block();
+        sh.ring_tail = (uint32_t)(k + 1);
       }
-      if (lane == 0) sh.cnt[s] = 0;
     }
     // release the stage (the wire store must have read it first)
     if (stores_pending && threadIdx.x == 0) {
@@ -595,10 +655,9 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
       stores_pending = false;
     }
     __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gs::smem_u32(&sh.empty[s])) : "memory");
-    if (order == kConsumerWarps - 1)
-      finish_chunk_warp<FUSE>(segs, nseg, nseg_active, m.chunk, m.seg, tw, te, tg, params, partials,
-                              counters, seg_scale, seg_out, grad_norm_out);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gs::smem_u32(&sh.empty[s]))
+                   : "memory");
   }
   if (threadIdx.x == 0) gs::bulk_wait_all();
 }

@@ -164,6 +164,24 @@ int gs_fold_f32(const uint64_t* slots, int p, int64_t offset, float* out, int64_
 int gs_fold_f16_tree(const uint64_t* slots, int p, int64_t offset, uint16_t* out,
                      int64_t n, uint32_t* nonfinite, void* stream);
 
+/* Bit-exact all-reduce of one binary16 bucket over NVLink peer memory: the
+ * reference's pairwise tree (fold_f16_tree, collectives.py:273-283) with the
+ * bytes of a ring (reduce-scatter by peer loads, then all-gather by peer
+ * loads; tcp.py:122-130 is the same design over TCP).  Call on every rank
+ * with the same arguments except `rank`:
+ *   bufs   device array of p peer-mapped base pointers of the (symmetric)
+ *          wire buffers, bufs[rank] = this rank's own;
+ *   sig    device array of p peer-mapped pointers to zero-initialised uint32
+ *          signal areas of >= 2 * nblocks * p words each;
+ *   offset, n  the bucket (elements) inside every wire;
+ *   epoch  nonzero, strictly increasing per call on a given sig area;
+ *   nblocks  grid size; all CTAs must be co-resident (<= SMs).
+ * The wire must be double-buffered across consecutive calls on the same
+ * range (the kernel has no exit barrier).  p <= 8. */
+int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                             int64_t offset, int64_t n, uint32_t epoch, int nblocks,
+                             uint32_t* nonfinite, void* stream);
+
 /* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
 
 /* Pass 1 over `nchunk` chunks starting at chunk index `chunk0`: widen (fp16

@@ -1,0 +1,185 @@
+// gs_collective.cu — bit-exact (reference-ordered) all-reduce of binary16
+// buckets over NVLink peer memory, one kernel per rank.
+//
+// Reference: allreduce_f16 / fold_f16_tree (collectives.py:273-283, 322-340):
+// the sum is a pairwise tree over ranks 0..p-1 with widen-add-narrow
+// combines.  NCCL sums in ring/NVLS order, which is not that tree; this
+// kernel reproduces the tree exactly while moving the same bytes as a ring
+// (2(p-1)/p * S inbound per GPU), like the reference's own TCP executor
+// (tcp.py:122-130, 250-254: raw chunks go straight to their owner, the
+// owner folds in rank order, folded chunks are gathered back).
+//
+//   A  entry barrier: every rank's bucket is packed (stream order on each
+//      rank) -> block b signals block b of every peer and waits for them;
+//   B  reduce-scatter: rank r folds its slice of the bucket, reading all p
+//      peers' raw values over NVLink (pairwise tree, in registers) and
+//      writes the folded slice in place into its own buffer;
+//   C  barrier: the slices are complete (per block: block b of rank q only
+//      reads the sub-ranges block b of every rank wrote);
+//   D  all-gather: rank q copies every other rank's folded sub-range b from
+//      that rank's buffer into its own.
+// The caller double-buffers the wire across steps, so no exit barrier is
+// needed: a rank can only overwrite a buffer after all peers passed the
+// entry barrier of the following step, i.e. finished this kernel.
+// Buffers come from a symmetric-memory window (torch's _symmetric_memory):
+// peer pointers are plain device addresses mapped over NVLink.  Every spin
+// is bounded and traps rather than hanging the GPU.
+#include "gs_common.cuh"
+
+namespace {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// block-level cross-rank barrier on signal slot `phase`
+__device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, int rank, int p,
+                                             int phase, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x < p) {
+    const int q = threadIdx.x;
+    uint32_t* remote = reinterpret_cast<uint32_t*>(sig[q]) +
+                       ((size_t)phase * gridDim.x + blockIdx.x) * p + rank;
+    __threadfence_system();
+    st_release_sys(remote, epoch);
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig[rank]) +
+                           ((size_t)phase * gridDim.x + blockIdx.x) * p + q;
+    uint32_t spins = 0;
+    while (ld_acquire_sys(mine) != epoch) {
+      if (++spins > (1u << 28)) __trap();
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float add_narrow(float a, float b) {
+  return gs::widen(gs::narrow(__fadd_rn(a, b)));
+}
+
+template <int P>
+__device__ __forceinline__ float tree(float (&v)[P]) {
+#pragma unroll
+  for (int s = 1; s < P; s *= 2) {
+#pragma unroll
+    for (int i = 0; i + s < P; i += 2 * s) v[i] = add_narrow(v[i], v[i + s]);
+  }
+  return v[0];
+}
+
+// [lo, hi) of sub-range `b` of slice `r` for an n-element bucket
+__device__ __forceinline__ void subrange(int64_t n, int p, int r, int nb, int b, int64_t& lo,
+                                         int64_t& hi) {
+  const int64_t per = ((n + p - 1) / p + 7) / 8 * 8;
+  const int64_t s0 = min(n, (int64_t)r * per), s1 = min(n, s0 + per);
+  const int64_t sub = ((s1 - s0 + nb - 1) / nb + 7) / 8 * 8;
+  lo = min(s1, s0 + (int64_t)b * sub);
+  hi = min(s1, lo + sub);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                         int rank, int64_t offset, int64_t n, uint32_t epoch,
+                         uint32_t* __restrict__ nonfinite) {
+  const uint16_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+
+  peer_barrier(sig, rank, P, 0, epoch);  // A: every bucket packed
+
+  // B: fold my slice, sub-range blockIdx.x
+  int64_t lo, hi;
+  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
+  uint32_t bad = 0;
+  bool vec = gs::is_aligned16(mine + lo);
+#pragma unroll
+  for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q] + lo);
+  const int64_t nv = vec ? (hi - lo) / 8 : 0;
+  for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+    uint4 raw[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) raw[q] = __ldcv(reinterpret_cast<const uint4*>(src[q] + lo) + i);
+    uint32_t o[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      float a[P], b[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const float2 f = gs::widen2((&raw[q].x)[h]);
+        a[q] = f.x;
+        b[q] = f.y;
+      }
+      o[h] = gs::narrow2(tree<P>(a), tree<P>(b));
+      bad |= ((o[h] & 0x7C00u) == 0x7C00u) | ((o[h] & 0x7C000000u) == 0x7C000000u);
+    }
+    reinterpret_cast<uint4*>(mine + lo)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  for (int64_t i = lo + nv * 8 + threadIdx.x; i < hi; i += kThreads) {
+    float v[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = gs::widen(__ldcv(src[q] + i));
+    const uint16_t o = gs::narrow(tree<P>(v));
+    bad |= (o & 0x7C00u) == 0x7C00u;
+    mine[i] = o;
+  }
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+
+  peer_barrier(sig, rank, P, 1, epoch);  // C: every slice folded
+
+  // D: gather the other ranks' folded sub-ranges
+#pragma unroll 1
+  for (int d = 1; d < P; ++d) {
+    const int r = (rank + d) % P;
+    subrange(n, P, r, gridDim.x, blockIdx.x, lo, hi);
+    const bool v2 = gs::is_aligned16(mine + lo) && gs::is_aligned16(src[r] + lo);
+    const int64_t m = v2 ? (hi - lo) / 8 : 0;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src[r] + lo);
+    uint4* d4 = reinterpret_cast<uint4*>(mine + lo);
+    for (int64_t i = threadIdx.x; i < m; i += kThreads) d4[i] = __ldcv(s4 + i);
+    for (int64_t i = lo + m * 8 + threadIdx.x; i < hi; i += kThreads) mine[i] = __ldcv(src[r] + i);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                             int64_t offset, int64_t n, uint32_t epoch, int nblocks,
+                             uint32_t* nonfinite, void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allreduce_f16: 1 <= p <= 8 (got %d)", p);
+  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allreduce_f16: bad rank %d", rank);
+  GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_f16: negative size/offset");
+  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allreduce_f16: bad block count");
+  GS_REQUIRE(epoch != 0, "gs_ordered_allreduce_f16: epoch 0 is the reset value");
+  if (p == 1 || n == 0) return GS_OK;
+  GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_OAR(P)                                                                                 \
+  case P:                                                                                         \
+    ordered_allreduce_kernel<P><<<nblocks, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,    \
+                                                             nonfinite);                          \
+    break;
+  switch (p) {
+    GS_OAR(2)
+    GS_OAR(3)
+    GS_OAR(4)
+    GS_OAR(5)
+    GS_OAR(6)
+    GS_OAR(7)
+    GS_OAR(8)
+  }
+#undef GS_OAR
+  return gs_check_launch("gs_ordered_allreduce_f16");
+}
+
+}  // extern "C"

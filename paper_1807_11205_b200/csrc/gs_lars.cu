@@ -58,6 +58,15 @@ __device__ __forceinline__ void sq_acc(double& acc, float x) {
   acc = fma(d, d, acc);
 }
 
+// release-ordered arrival: the partials this thread stored become visible no
+// later than the counter increment (no full fence / L1 invalidate on the
+// common path; the rare last arriver fences before reading everyone's data)
+__device__ __forceinline__ uint32_t arrive_release(uint32_t* p) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 // raw binary16 non-finite detector for two halves in one word: adding 0x0400
 // to an all-ones exponent field carries into the (masked-off) sign position
 __device__ __forceinline__ uint32_t raw_nonfinite_bits(uint32_t w) {
@@ -300,8 +309,7 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
     partials[3 * (int64_t)c + 0] = sw;
     partials[3 * (int64_t)c + 1] = se;
     partials[3 * (int64_t)c + 2] = sg;
-    __threadfence();
-    const uint32_t prev = atomicAdd(&counters[ch.seg], 1u);
+    const uint32_t prev = arrive_release(&counters[ch.seg]);
     s_last = (prev + 1 == (uint32_t)sgp->chunk_count);
   }
   __syncthreads();
@@ -320,8 +328,7 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
   gs::block_sum3<kThreads>(x, y, z);
   if (threadIdx.x == 0) {
     trust_eval(sflags, x, y, z, params, seg_scale + ch.seg, seg_out + 4 * (int64_t)ch.seg);
-    __threadfence();
-    const uint32_t prev = atomicAdd(&counters[nseg], 1u);
+    const uint32_t prev = arrive_release(&counters[nseg]);
     if (prev + 1 == (uint32_t)nseg_active) {
       __threadfence();
       for (int s = 0; s < nseg; ++s)
@@ -346,8 +353,7 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
 // consumer warp of a chunk (shared-memory arrival counter) folds the 8 warp
 // partials in warp order into the chunk partial and, for the fused trust,
 // does the per-segment arrival; so the chunk partial and everything after it
-// are identical to the register-staged kernel.  The fused packer is one bulk
-// shared->global store of the staged gradient into the wire.  Chunks that are
+// are identical to the register-staged kernel.  Chunks that are
 // not 16-byte aligned (or not a multiple of 8 elements) are reduced from
 // global memory directly by the consumers.
 constexpr int kStages = 4;
@@ -391,12 +397,16 @@ struct TmaShared {
 constexpr int kTmaSmem = kStages * kStageBytes + (int)sizeof(TmaShared);
 
 template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
-__device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, int len,
-                                        const Ctx& cx, Acc& a) {
+__device__ __forceinline__ void p1_smem(const uint16_t* sg, const float* sw, uint16_t* gcopy,
+                                        int len, const Ctx& cx, Acc& a) {
   const int nv = len / 8;
 #pragma unroll 4
   for (int i = threadIdx.x; i < nv; i += kThreads) {
     const uint4 gv = reinterpret_cast<const uint4*>(sg)[i];
+    // the fused packer: plain 128-bit stores of the staged gradient (a bulk
+    // shared->global store would queue behind the next stages' loads in the
+    // SM's TMA unit and hold the stage)
+    if (gcopy != nullptr) reinterpret_cast<uint4*>(gcopy)[i] = gv;
     F8 wv{};
     if (LARS) {
       wv.a = reinterpret_cast<const float4*>(sw)[2 * i];
@@ -438,10 +448,7 @@ __device__ __forceinline__ void finish_chunk_warp(const gs_segment* __restrict__
     partials[3 * (int64_t)c + 0] = it.sw;
     partials[3 * (int64_t)c + 1] = it.se;
     partials[3 * (int64_t)c + 2] = it.sg;
-    if (FUSE) {
-      __threadfence();
-      last = (atomicAdd(&counters[seg], 1u) + 1 == (uint32_t)segs[seg].chunk_count);
-    }
+    if (FUSE) last = (arrive_release(&counters[seg]) + 1 == (uint32_t)segs[seg].chunk_count);
   }
   if (!FUSE) return;
   last = __shfl_sync(0xFFFFFFFFu, last, 0);
@@ -472,8 +479,7 @@ __device__ __forceinline__ void finish_chunk_warp(const gs_segment* __restrict__
   }
   if (lane == 0) {
     trust_eval(sp->flags, x, y, z, params, seg_scale + seg, seg_out + 4 * (int64_t)seg);
-    __threadfence();
-    if (atomicAdd(&counters[nseg], 1u) + 1 == (uint32_t)nseg_active) {
+    if (arrive_release(&counters[nseg]) + 1 == (uint32_t)nseg_active) {
       __threadfence();
       for (int s2 = 0; s2 < nseg; ++s2)
         if (segs[s2].chunk_count == 0)
@@ -586,7 +592,6 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
   cx.u.load(params);
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
-  bool stores_pending = false;
   for (int k = 0; k < nmine; ++k) {
     const int s = k % kStages;
     const uint32_t ph = (uint32_t)(k / kStages) & 1u;
@@ -598,17 +603,12 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
     if (m.bulk) {
       const uint16_t* sgp = reinterpret_cast<const uint16_t*>(smem + s * kStageBytes);
       const float* swp = reinterpret_cast<const float*>(smem + s * kStageBytes + kStageG);
-      if (threadIdx.x == 0 && m.gcopy != nullptr) {
-        gs::bulk_s2g(m.gcopy, sgp, 2u * m.len);
-        gs::bulk_commit();
-        stores_pending = true;
-      }
       if (lars && decay)
-        p1_smem<POW2, RAWFLAG, GNORM, true, true>(sgp, swp, m.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, true, true>(sgp, swp, m.gcopy, m.len, cx, a);
       else if (lars)
-        p1_smem<POW2, RAWFLAG, GNORM, true, false>(sgp, swp, m.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, true, false>(sgp, swp, m.gcopy, m.len, cx, a);
       else
-        p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, m.len, cx, a);
+        p1_smem<POW2, RAWFLAG, GNORM, false, false>(sgp, swp, m.gcopy, m.len, cx, a);
     } else {
       p1_global_chunk<POW2, RAWFLAG, GNORM>(m, cx, a);
     }
@@ -649,17 +649,11 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
         sh.ring_tail = (uint32_t)(k + 1);
       }
     }
-    // release the stage (the wire store must have read it first)
-    if (stores_pending && threadIdx.x == 0) {
-      gs::bulk_wait_read_all();
-      stores_pending = false;
-    }
     __syncwarp();
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gs::smem_u32(&sh.empty[s]))
                    : "memory");
   }
-  if (threadIdx.x == 0) gs::bulk_wait_all();
 }
 
 // ----------------------------------------------------------------- trust

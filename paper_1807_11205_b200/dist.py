@@ -12,6 +12,10 @@ one GPU and the bucket all-reduce runs over NVLink 5 / NVSwitch:
                   Topology(p, k): ncclReduce to the group master (lowest rank,
                   collectives.py:76-77) -> ncclAllReduce among the masters ->
                   ncclBroadcast inside the group;
+  "ordered"       the reference's own summation order, bit-exact: a single
+                  kernel per rank folds its slice out of every peer's
+                  symmetric-memory buffer over NVLink in pairwise-tree order
+                  and gathers the other slices back (OrderedWire);
   "sharded"       bandwidth-optimal hierarchy for NVSwitch: intra-group
                   reduce-scatter -> all-reduce among same-offset ranks of all
                   groups -> intra-group all-gather (moves 2(p-1)/p S per GPU,
@@ -36,7 +40,7 @@ from .collectives import Topology, choose_algorithm
 
 __all__ = ["Communicator", "init_from_env", "ALGORITHMS"]
 
-ALGORITHMS = ("ring", "hierarchical", "sharded")
+ALGORITHMS = ("ring", "hierarchical", "sharded", "ordered")
 
 
 def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
@@ -139,6 +143,54 @@ class Communicator:
         else:
             raise ValueError(f"unknown algorithm {algorithm!r}")
 
-    def pick(self, nbytes: int, eta_bytes: int, hier_variant: str = "hierarchical") -> str:
-        """Hybrid rule (collectives.py:238-244) mapped onto the NCCL variants."""
-        return hier_variant if choose_algorithm(nbytes, eta_bytes) == "hierarchical" else "ring"
+    def pick(self, nbytes: int, eta_bytes: int, hier_variant: str = "hierarchical",
+             flat_variant: str = "ring") -> str:
+        """Hybrid rule (collectives.py:238-244) mapped onto the variants."""
+        return hier_variant if choose_algorithm(nbytes, eta_bytes) == "hierarchical" else flat_variant
+
+
+class OrderedWire:
+    """Double-buffered symmetric-memory wire for the bit-exact ordered
+    all-reduce (gs_ordered_allreduce_f16): one allocation per rank,
+    [wire A | wire B | signal area], exchanged once through torch's
+    symmetric-memory rendezvous so every rank holds every peer's NVLink-mapped
+    base address.  Both halves have the pipeline's wire layout, so a bucket is
+    the same element range in every rank's buffer."""
+
+    def __init__(self, comm: "Communicator", total: int, device, nblocks: int | None = None):
+        import numpy as np
+        import torch.distributed._symmetric_memory as symm
+
+        from . import _device as dev
+
+        self.p = comm.topo.p
+        self.rank = comm.rank
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        self.nblocks = nblocks or max(1, min(sms, 128))
+        self.total = (total + 255) // 256 * 256
+        sig_words = 2 * self.nblocks * self.p
+        sig_elems = (4 * sig_words + 1) // 2 + 256
+        self.buf = symm.empty(2 * self.total + sig_elems, dtype=torch.uint16, device=device)
+        self.buf.zero_()
+        torch.cuda.synchronize(device)
+        self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
+        bases = [int(x) for x in self.hdl.buffer_ptrs]
+        self.halves = (self.buf[: self.total], self.buf[self.total: 2 * self.total])
+        tabs = []
+        for h in range(2):
+            tabs.append(dev.upload(np.array([b + 2 * h * self.total for b in bases],
+                                            dtype=np.uint64), device))
+        self.bufs_dev = tabs
+        self.sig_dev = dev.upload(np.array([b + 4 * self.total for b in bases], dtype=np.uint64),
+                                  device)
+        self.epoch = 0
+        dist.barrier()
+
+    def allreduce(self, half: int, offset: int, n: int, stream_h: int) -> None:
+        from . import _device as dev
+        from . import _native
+
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
+        _native.call("gs_ordered_allreduce_f16", dev.ptr(self.bufs_dev[half]),
+                     dev.ptr(self.sig_dev), self.rank, self.p, offset, n, self.epoch,
+                     self.nblocks, None, stream_h)

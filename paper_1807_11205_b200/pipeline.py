@@ -140,7 +140,7 @@ class GradientPipeline:
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
-                 bulk: bool = True):
+                 bulk: bool = True, flat_variant: str = "ring"):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -166,7 +166,22 @@ class GradientPipeline:
                                                               threshold_bytes)
 
         d = self.device
-        self.wire = torch.zeros(self.total, dtype=torch.uint16, device=d)
+        for b in self.buckets:
+            if comm is not None:
+                b.algorithm = comm.pick(b.nbytes, self.eta_bytes, hier_variant, flat_variant)
+            else:
+                b.algorithm = "ordered" if self.local else "none"
+        # the ordered (bit-exact) collective reads peers' wires over NVLink:
+        # the wire then lives in a double-buffered symmetric-memory window
+        self.ordered = None
+        if comm is not None and any(b.algorithm == "ordered" for b in self.buckets):
+            from .dist import OrderedWire
+            self.ordered = OrderedWire(comm, self.total, d)
+            self.wire = self.ordered.halves[0]
+        else:
+            self.wire = torch.zeros(self.total, dtype=torch.uint16, device=d)
+        self._last_wire = self.wire
+        self._half = 0
         self.master = torch.zeros(self.total, dtype=torch.float32, device=d)
         self.velocity = torch.zeros(self.total, dtype=torch.float32, device=d)
         self.working = torch.zeros(self.total, dtype=torch.uint16, device=d)
@@ -195,10 +210,6 @@ class GradientPipeline:
             if b.nchunk:
                 assert int(begin[b.params[0]]) == c or sizes[b.params[0]] == 0
             c += b.nchunk
-            if comm is not None:
-                b.algorithm = comm.pick(b.nbytes, self.eta_bytes, hier_variant)
-            else:
-                b.algorithm = "ordered" if self.local else "none"
         assert c == self.plan.nchunk
 
         self._pack_cache: dict = {}
@@ -249,7 +260,7 @@ class GradientPipeline:
 
     def bucket_payload(self, b: int) -> torch.Tensor:
         bk = self.buckets[b]
-        return self.wire[bk.start:bk.start + bk.length]
+        return self._last_wire[bk.start:bk.start + bk.length]
 
     # ------------------------------------------------------------ packing
     def grad_arena(self) -> torch.Tensor:
@@ -348,8 +359,16 @@ class GradientPipeline:
             tab = self.plan.alt_segments([t.data_ptr() for t in views],
                                          [wb + 2 * o for o in self.wire_off])
             return ("fused", tab), id(tab)
+        if self.ordered is not None:
+            tabs = tuple(self._tables_for(views, h) for h in self.ordered.halves)
+            return tabs, tuple(id(t) for t in tabs)
         tabs = self._tables_for(views, self.wire)
         return tabs, id(tabs)
+
+    def _half_segments(self, half: int):
+        """Segment table whose gradient pointers address wire half `half`."""
+        wb = self.ordered.halves[half].data_ptr()
+        return self.plan.alt_segments([wb + 2 * o for o in self.wire_off])
 
     def enqueue(self, grads, step: int, timer=None) -> None:
         """Launch one step on the current stream (no host sync).
@@ -421,17 +440,25 @@ class GradientPipeline:
                 timer("pass1")
             plan.pass1(sh, g_is_f16=True)
         else:
+            # bucket b+1 is packed (pack stream) while bucket b's all-reduce is
+            # in flight and bucket b-1 runs pass 1 (compute stream)
             ps = self._pack_stream
             ps.wait_stream(s0)
+            half = self._half
+            wire = self.ordered.halves[half] if self.ordered is not None else self.wire
+            ptabs = tabs[half] if self.ordered is not None else tabs
+            if self.ordered is not None:
+                plan.use_segments(self._half_segments(half))
             works = []
             for b, bk in enumerate(self.buckets):
                 with torch.cuda.stream(ps):
-                    self._pack(tabs, b, int(ps.cuda_stream))
-                    payload = self.wire[bk.start:bk.start + bk.padded]
+                    self._pack(ptabs, b, int(ps.cuda_stream))
+                    payload = wire[bk.start:bk.start + bk.padded]
                     if bk.algorithm == "ring":
                         works.append(self.comm.allreduce_ring(payload, async_op=True))
                     else:
-                        self.comm.allreduce(payload, bk.algorithm)
+                        if bk.algorithm != "ordered":
+                            self.comm.allreduce(payload, bk.algorithm)
                         ev = torch.cuda.Event()
                         ev.record(ps)
                         works.append(ev)
@@ -441,7 +468,12 @@ class GradientPipeline:
                     s0.wait_event(w)
                 else:
                     w.wait()
+                if bk.algorithm == "ordered":
+                    self.ordered.allreduce(half, bk.start, bk.length, sh)
                 plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+            self._last_wire = wire
+            if self.ordered is not None:
+                self._half ^= 1
         if timer:
             timer("trust")
         if not plan.fused:

@@ -1,7 +1,8 @@
-"""Multi-GPU parity check of the NCCL pipeline (run on a GPU box, not by pytest):
+"""Multi-GPU parity check of the pipeline (run on a GPU box, not by pytest):
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_check.py
 
+"ordered" (symmetric-memory peer fold) must be bit-exact at every N.
 Every rank steps GradientPipeline(comm=Communicator(Topology(N, k))) on its own
 synthetic fp16 gradients; rank 0 recomputes the reference composition with the
 CPU oracle.  Checks per algorithm (ring / hierarchical / sharded):
@@ -48,14 +49,18 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    for algo, k in (("ring", 1), ("hierarchical", 2), ("sharded", 2)):
+    algos = os.environ.get("MGPU_ALGOS", "ordered,ring,hierarchical,sharded").split(",")
+    for algo, k in (("ordered", 1), ("ring", 1), ("hierarchical", 2), ("sharded", 2)):
+        if algo not in algos:
+            continue
         if world % k or (algo != "ring" and world == 1):
             continue
         comm = Communicator(gs.Topology(world, k))
         cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
         pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=theta, comm=comm,
-                                   eta_bytes=0 if algo == "ring" else 1 << 62,
-                                   hier_variant=algo if algo != "ring" else "hierarchical",
+                                   eta_bytes=0 if algo in ("ring", "ordered") else 1 << 62,
+                                   hier_variant=algo if algo not in ("ring", "ordered") else "hierarchical",
+                                   flat_variant="ordered" if algo == "ordered" else "ring",
                                    init_master=master, loss_scale=gs.LossScale(1024.0), device=dev)
         groups = [rp.Group(s.name, s.kind, w.copy(), np.zeros(s.numel, np.float32),
                            np.zeros(s.numel, np.float32), rp.narrow(w))
@@ -72,7 +77,7 @@ def main():
             reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]
             if rank == 0:
                 parts = [split(w, specs) for w in wires]
-                exact = world == 2
+                exact = world == 2 or algo == "ordered"
                 out = rp.compose_step_fp16(parts, [s.name for s in specs], [s.numel for s in specs],
                                            order, groups, rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1,
                                            oloss, theta, 0,

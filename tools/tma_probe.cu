@@ -1,0 +1,164 @@
+// tma_probe.cu — microbenchmark: how fast can one persistent CTA per SM
+// stream 48 KB chunks (16 KB + 32 KB) through shared memory with
+// cp.async.bulk + mbarrier, with and without the pass-1 arithmetic?
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I include tools/tma_probe.cu -o tools/tma_probe
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_1807_11205_b200/csrc/gs_common.cuh"
+
+void gs_set_error(const char*, ...) {}
+int gs_check_launch(const char*) { return 0; }
+
+constexpr int kChunk = 8192;
+constexpr int kG = kChunk * 2, kW = kChunk * 4, kStage = kG + kW;
+
+template <int STAGES, int MODE>  // MODE 0: no compute, 1: fp32 sum, 2: fp64 sums
+__global__ void __launch_bounds__(288, 1) probe(const uint16_t* g, const float* w, int nchunk,
+                                                double* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nmine = (nchunk - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      gs::mbar_init(&full[s], 1);
+      gs::mbar_init(&empty[s], 8);
+    }
+    gs::mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0)
+      for (int k = 0; k < nmine; ++k) {
+        const int s = k % STAGES;
+        const uint32_t ph = (k / STAGES) & 1;
+        gs::mbar_wait(&empty[s], ph ^ 1);
+        const long c = blockIdx.x + (long)k * gridDim.x;
+        gs::mbar_arrive_expect_tx(&full[s], kStage);
+        gs::bulk_g2s(smem + s * kStage, g + c * kChunk, kG, &full[s]);
+        gs::bulk_g2s(smem + s * kStage + kG, w + c * kChunk, kW, &full[s]);
+      }
+    return;
+  }
+  double acc = 0.0;
+  float accf = 0.f;
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % STAGES;
+    const uint32_t ph = (k / STAGES) & 1;
+    gs::mbar_wait(&full[s], ph);
+    const uint4* sg = reinterpret_cast<const uint4*>(smem + s * kStage);
+    const float4* sw = reinterpret_cast<const float4*>(smem + s * kStage + kG);
+    if (MODE == 0) {
+      if (threadIdx.x == 0) accf += __half2float(__ushort_as_half(sg[0].x & 0xffff));
+    } else {
+#pragma unroll 4
+      for (int i = threadIdx.x; i < kChunk / 8; i += 256) {
+        const uint4 gv = sg[i];
+        const float4 wa = sw[2 * i], wb = sw[2 * i + 1];
+        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = gs::widen2(gw[q]);
+          if (MODE == 1) {
+            accf += f.x * wv[2 * q] + f.y * wv[2 * q + 1];
+          } else {
+            const double a = f.x, b = f.y, c = wv[2 * q], d = wv[2 * q + 1];
+            acc = fma(a, a, acc);
+            acc = fma(b, b, acc);
+            acc = fma(c, c, acc);
+            acc = fma(d, d, acc);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gs::smem_u32(&empty[s])) : "memory");
+  }
+  if (acc + accf == 12345.0) out[0] = acc + accf;
+}
+
+// plain register-staged reference: one CTA per chunk, loads then math
+template <int MODE>
+__global__ void __launch_bounds__(256) plain(const uint16_t* g, const float* w, int nchunk, double* out) {
+  const long c = blockIdx.x;
+  const uint4* sg = reinterpret_cast<const uint4*>(g + c * kChunk);
+  const float4* sw = reinterpret_cast<const float4*>(w + c * kChunk);
+  uint4 gv[4];
+  float4 wa[4], wb[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    gv[k] = __ldg(sg + threadIdx.x + 256 * k);
+    wa[k] = __ldg(sw + 2 * (threadIdx.x + 256 * k));
+    wb[k] = __ldg(sw + 2 * (threadIdx.x + 256 * k) + 1);
+  }
+  double acc = 0.0;
+  float accf = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float wv[8] = {wa[k].x, wa[k].y, wa[k].z, wa[k].w, wb[k].x, wb[k].y, wb[k].z, wb[k].w};
+    const uint32_t gw[4] = {gv[k].x, gv[k].y, gv[k].z, gv[k].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = gs::widen2(gw[q]);
+      if (MODE == 1) {
+        accf += f.x * wv[2 * q] + f.y * wv[2 * q + 1];
+      } else {
+        const double a = f.x, b = f.y, cc = wv[2 * q], d = wv[2 * q + 1];
+        acc = fma(a, a, acc);
+        acc = fma(b, b, acc);
+        acc = fma(cc, cc, acc);
+        acc = fma(d, d, acc);
+      }
+    }
+  }
+  if (acc + accf == 12345.0) out[0] = acc + accf;
+}
+
+template <typename F>
+float time_it(F f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int i = 0; i < 3; ++i) f();
+  cudaEventRecord(a);
+  for (int i = 0; i < 10; ++i) f();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms / 10;
+}
+
+int main() {
+  const int nchunk = 3120;  // ~25.5M elements
+  uint16_t* g;
+  float* w;
+  double* out;
+  cudaMalloc(&g, (size_t)nchunk * kG);
+  cudaMalloc(&w, (size_t)nchunk * kW);
+  cudaMalloc(&out, 8);
+  cudaMemset(g, 0, (size_t)nchunk * kG);
+  cudaMemset(w, 0, (size_t)nchunk * kW);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const double bytes = (double)nchunk * kStage;
+#define RUN_P(ST, M)                                                                              \
+  {                                                                                               \
+    const int sm = ST * kStage + 64;                                                              \
+    cudaFuncSetAttribute(probe<ST, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);          \
+    float ms = time_it([&] { probe<ST, M><<<sms, 288, sm>>>(g, w, nchunk, out); });               \
+    printf("tma  stages=%d mode=%d: %8.1f us  %7.1f GB/s  err=%s\n", ST, M, ms * 1e3,             \
+           bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));                             \
+  }
+  RUN_P(2, 0) RUN_P(4, 0) RUN_P(4, 1) RUN_P(4, 2) RUN_P(3, 2)
+#define RUN_R(M)                                                                                 \
+  {                                                                                              \
+    float ms = time_it([&] { plain<M><<<nchunk, 256>>>(g, w, nchunk, out); });                   \
+    printf("regs mode=%d: %8.1f us  %7.1f GB/s  err=%s\n", M, ms * 1e3, bytes / ms / 1e6,         \
+           cudaGetErrorString(cudaGetLastError()));                                              \
+  }
+  RUN_R(1) RUN_R(2)
+  return 0;
+}

@@ -188,7 +188,7 @@ def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, wa
                              rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
         times.append((time.perf_counter() - t0) / frac)
     ms = 1e3 * statistics.mean(times)
-    return {"ms": ms, "threads": threads, "frac": frac, "t_full_s": t_full,
+    return {"ms": ms, "threads": threads, "frac": frac, "t_full_s": t_full, "params": sum(sizes),
             "sample": (f"{model} p={p} theta={theta}: "
                        + ("full workload" if frac == 1.0 else
                           f"first {frac:.3f} of the parameters (wire order), time scaled by 1/frac")
@@ -206,7 +206,7 @@ def run_reference(args, rank: int, world: int) -> None:
         "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.model} fused MP-LARS step, fp16 wire, CPU oracle port",
-                   "params": None, "theta": args.theta, "p": world,
+                   "model": args.model, "params": r["params"], "theta": args.theta, "p": world,
                    "parallelism": f"dp{world} simulated in one process"},
         "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": r["threads"],
                          "kind": "port", "sample": r["sample"]},

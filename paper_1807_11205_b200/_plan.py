@@ -175,7 +175,14 @@ class LarsPlan:
         self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
                                           dtype=torch.uint8).pin_memory()
         self.hint = 0
-        self.extra_hint = 0   # e.g. _native.HINT_NO_BULK to force the register-staged pass 1
+        # pass 1 runs the register-staged kernel by default: on B200 it beats
+        # the TMA-pipelined persistent kernel (43 vs 47 us on ResNet-50,
+        # tools/pass1_variants.py); clear HINT_NO_BULK to select the latter
+        self.extra_hint = _native.HINT_NO_BULK
+        # the trust ratio as a separate single-CTA kernel: fusing it into
+        # pass 1 through per-chunk arrival counters costs a release atomic
+        # per chunk on the critical path (61 vs 43 us); see DESIGN.md §4
+        self.fuse_trust = False
 
     def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
         """A segment table identical to the base one except for the gradient
@@ -223,7 +230,7 @@ class LarsPlan:
     @property
     def fused(self) -> bool:
         """pass1 computes the trust ratios itself (no separate trust launch)."""
-        return self.nseg_active > 0
+        return self.fuse_trust and self.nseg_active > 0
 
     def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None,
               fuse: bool = True):

@@ -178,27 +178,30 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
                    (gcopy == nullptr || gs::is_aligned16(gcopy));
   const int nv = vec ? len / 8 : 0;
   const int t = threadIdx.x;
-  if (nv == kFullChunk / 8) {
-    // full chunk: issue every load of the thread first (4 x 16 B of g and
-    // 4 x 32 B of w in flight), then the arithmetic
+  // full batches of kRounds vectors per thread: issue every load of the
+  // batch (4 x 16 B of g, 4 x 32 B of w) before any arithmetic; each thread
+  // still visits its vectors t, t+256, t+512, ... in increasing order, so
+  // the batching never changes the summation order
+  constexpr int kBatch = kRounds * kThreads;
+  int done = 0;
+  for (; done + kBatch <= nv; done += kBatch) {
     typename Gt::V gv[kRounds];
     F8 wv[kRounds];
 #pragma unroll
-    for (int k = 0; k < kRounds; ++k) gv[k] = Gt::ld(g + 8 * (t + k * kThreads));
+    for (int k = 0; k < kRounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
     if (LARS) {
 #pragma unroll
-      for (int k = 0; k < kRounds; ++k) wv[k] = ldw(w + 8 * (t + k * kThreads));
+      for (int k = 0; k < kRounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
     }
     if (F16 && gcopy != nullptr) {
 #pragma unroll
       for (int k = 0; k < kRounds; ++k)
-        reinterpret_cast<uint4*>(gcopy)[t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
+        reinterpret_cast<uint4*>(gcopy)[done + t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
     }
 #pragma unroll
     for (int k = 0; k < kRounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
-    return;
   }
-  for (int i = t; i < nv; i += kThreads) {
+  for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
     F8 wv{};
     if (LARS) wv = ldw(w + 8 * i);
@@ -741,21 +744,18 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
                    gs::is_aligned16(w16);
   const int nv = vec ? len / 8 : 0;
   const int t = threadIdx.x;
-  if (nv == kFullChunk / 8) {
-    // full chunk: two halves of two vectors each; every load of a half is
-    // issued before its arithmetic and stores (stores cannot alias the next
-    // half's loads, but the compiler cannot prove it through the casts)
-#pragma unroll
-    for (int h = 0; h < kRounds; h += 2) {
-      const int i0 = t + h * kThreads, i1 = i0 + kThreads;
-      const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
-      const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
-      p2_vec<F16, POW2, DECAY>(g0, w0, v0, w, v, w16, i0, cx, s);
-      p2_vec<F16, POW2, DECAY>(g1, w1, v1, w, v, w16, i1, cx, s);
-    }
-    return;
+  // batches of two vectors per thread: both vectors' loads are issued before
+  // the arithmetic and stores (stores cannot alias the next batch's loads,
+  // but the compiler cannot prove it through the casts)
+  int done = 0;
+  for (; done + 2 * kThreads <= nv; done += 2 * kThreads) {
+    const int i0 = done + t, i1 = i0 + kThreads;
+    const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
+    const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
+    p2_vec<F16, POW2, DECAY>(g0, w0, v0, w, v, w16, i0, cx, s);
+    p2_vec<F16, POW2, DECAY>(g1, w1, v1, w, v, w16, i1, cx, s);
   }
-  for (int i = t; i < nv; i += kThreads) {
+  for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
     p2_vec<F16, POW2, DECAY>(gv, ld8(w, i), ld8(v, i), w, v, w16, i, cx, s);
   }

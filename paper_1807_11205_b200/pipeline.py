@@ -140,7 +140,7 @@ class GradientPipeline:
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
-                 bulk: bool = True, flat_variant: str = "ring"):
+                 bulk: bool = False, fuse_trust: bool = False, flat_variant: str = "ring"):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -200,8 +200,9 @@ class GradientPipeline:
                             vb + 4 * self.wire_off[i], hb + 2 * self.wire_off[i], sizes[i],
                             segment_flags(self.groups[i])) for i in range(n)]
         self.plan = LarsPlan(segs, d, order=self.order)
-        if not bulk:
-            self.plan.extra_hint |= _native.HINT_NO_BULK
+        if bulk:
+            self.plan.extra_hint &= ~_native.HINT_NO_BULK
+        self.plan.fuse_trust = fuse_trust
         begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]
         c = 0
         for b in self.buckets:

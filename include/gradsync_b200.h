@@ -206,15 +206,16 @@ int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const
                         uint32_t hint, double* partials, uint32_t* flags, uint32_t* counters,
                         float* seg_scale, double* seg_out, double* grad_norm_out, void* stream);
 
-/* Per segment: fold the chunk partials in chunk order, take the fp64 norms,
+/* Per segment (one CTA each): fold the chunk partials in a fixed order (the
+ * same order as gs_lars_pass1_trust), take the fp64 norms,
  * local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150, 173-176) and
- * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (optional,
- * nseg x 4 doubles) receives {||w||, ||eff||, local, sum g^2}; grad_norm_out
- * (optional) receives sqrt of the sum of per-segment g^2 in segment order
- * (experiment.py:408-411). */
+ * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (nseg x 4
+ * doubles) receives {||w||, ||eff||, local, sum g^2}; grad_norm_out (optional)
+ * receives sqrt of the sum of per-segment g^2 in segment order
+ * (experiment.py:408-411) and then needs `counter`, one zeroed uint32. */
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
                   const gs_step_params* params, float* seg_scale, double* seg_out,
-                  double* grad_norm_out, void* stream);
+                  double* grad_norm_out, uint32_t* counter, void* stream);
 
 /* Pass 2: if (*flags & flag_mask) do nothing (lars.py:161-163 — the step is
  * rejected with no mutation).  Otherwise per element

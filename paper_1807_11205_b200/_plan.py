@@ -249,7 +249,7 @@ class LarsPlan:
     def trust(self, stream_h: int):
         _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
                      dev.ptr(self.params), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
-                     dev.ptr(self.grad_norm), stream_h)
+                     dev.ptr(self.grad_norm), dev.ptr(self.counters[self.nseg:]), stream_h)
 
     def pass2(self, stream_h: int, g_is_f16: bool, flag_mask: int, chunk0: int = 0,
               nchunk: int | None = None):

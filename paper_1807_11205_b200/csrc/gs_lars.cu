@@ -35,6 +35,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kRounds = 4;                      // 8-element vectors per thread
+#ifndef GS_P1_ROUNDS
+#define GS_P1_ROUNDS 4   // pass-1 load batch (vectors per thread)
+#endif
+#ifndef GS_P1_MINB
+#define GS_P1_MINB 1     // pass-1 __launch_bounds__ min blocks per SM
+#endif
+constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
 constexpr uint32_t kBoth = GS_FLAG_SCALED_NONFINITE | GS_FLAG_GRAD_NONFINITE;
@@ -182,24 +189,24 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
   // batch (4 x 16 B of g, 4 x 32 B of w) before any arithmetic; each thread
   // still visits its vectors t, t+256, t+512, ... in increasing order, so
   // the batching never changes the summation order
-  constexpr int kBatch = kRounds * kThreads;
+  constexpr int kBatch = kP1Rounds * kThreads;
   int done = 0;
   for (; done + kBatch <= nv; done += kBatch) {
-    typename Gt::V gv[kRounds];
-    F8 wv[kRounds];
+    typename Gt::V gv[kP1Rounds];
+    F8 wv[kP1Rounds];
 #pragma unroll
-    for (int k = 0; k < kRounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
+    for (int k = 0; k < kP1Rounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
     if (LARS) {
 #pragma unroll
-      for (int k = 0; k < kRounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
+      for (int k = 0; k < kP1Rounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
     }
     if (F16 && gcopy != nullptr) {
 #pragma unroll
-      for (int k = 0; k < kRounds; ++k)
+      for (int k = 0; k < kP1Rounds; ++k)
         reinterpret_cast<uint4*>(gcopy)[done + t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
     }
 #pragma unroll
-    for (int k = 0; k < kRounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
+    for (int k = 0; k < kP1Rounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
   }
   for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
@@ -261,7 +268,7 @@ __device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg
 // arrives last is timing-dependent, the result is not: the fold always runs
 // over the same chunk range in the same fixed tree.
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GS_P1_MINB)
 lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                   const gs_chunk* __restrict__ chunks, int chunk0,
                   const gs_step_params* __restrict__ params, double* __restrict__ partials,
@@ -660,28 +667,42 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
 }
 
 // ----------------------------------------------------------------- trust
-__global__ void __launch_bounds__(kTrustThreads)
+// One CTA per segment folds the segment's chunk partials (256-strided, then
+// the fixed block tree: the same order as the fused and TMA paths), and the
+// last CTA to finish (arrival counter, zeroed with the flags) writes the grad
+// norm, summing the per-segment sums in segment order.
+__global__ void __launch_bounds__(kThreads)
 lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* __restrict__ partials,
                   const gs_step_params* __restrict__ params, float* __restrict__ seg_scale,
-                  double* __restrict__ seg_out, double* __restrict__ grad_norm_out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int s = warp; s < nseg; s += kTrustThreads / 32) {
-    const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
-    const uint32_t sflags = segs[s].flags;
-    double sw = 0.0, se = 0.0, sg = 0.0;
-    for (int i = lane; i < cn; i += 32) {
-      const double* p = partials + 3 * (int64_t)(cb + i);
-      sw += p[0];
-      se += p[1];
-      sg += p[2];
-    }
-    sw = gs::warp_sum(sw);
-    se = gs::warp_sum(se);
-    sg = gs::warp_sum(sg);
-    if (lane == 0) trust_eval(sflags, sw, se, sg, params, seg_scale + s, seg_out + 4 * (int64_t)s);
+                  double* __restrict__ seg_out, double* __restrict__ grad_norm_out,
+                  uint32_t* __restrict__ counter) {
+  const int s = blockIdx.x;
+  const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
+  double x = 0.0, y = 0.0, z = 0.0;
+  for (int i = threadIdx.x; i < cn; i += kThreads) {
+    const double* pp = partials + 3 * (int64_t)(cb + i);
+    x += pp[0];
+    y += pp[1];
+    z += pp[2];
+  }
+  gs::block_sum3<kThreads>(x, y, z);
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    trust_eval(segs[s].flags, x, y, z, params, seg_scale + s, seg_out + 4 * (int64_t)s);
+    s_last = grad_norm_out != nullptr && arrive_release(counter) + 1 == (uint32_t)nseg;
   }
   __syncthreads();
-  if (threadIdx.x == 0 && grad_norm_out != nullptr) *grad_norm_out = grad_norm_eval(seg_out, nseg);
+  if (!s_last) return;
+  __threadfence();
+  extern __shared__ double sq[];  // nseg doubles (dynamic)
+  for (int i = threadIdx.x; i < nseg; i += kThreads) sq[i] = __ldcg(seg_out + 4 * (int64_t)i + 3);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // experiment.py:408-411: sqrt of the per-group dots summed in group order
+    double acc = 0.0;
+    for (int i = 0; i < nseg; ++i) acc = __dadd_rn(acc, sq[i]);
+    *grad_norm_out = __dsqrt_rn(acc);
+  }
 }
 
 // ----------------------------------------------------------------- pass 2
@@ -902,12 +923,24 @@ int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const
 
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
                   const gs_step_params* params, float* seg_scale, double* seg_out,
-                  double* grad_norm_out, void* stream) {
+                  double* grad_norm_out, uint32_t* counter, void* stream) {
   GS_REQUIRE(nseg >= 0, "gs_lars_trust: negative segment count");
   if (nseg == 0) return GS_OK;
   GS_REQUIRE(segs && partials && params && seg_scale && seg_out, "gs_lars_trust: null pointer");
-  lars_trust_kernel<<<1, kTrustThreads, 0, (cudaStream_t)stream>>>(segs, nseg, partials, params,
-                                                                   seg_scale, seg_out, grad_norm_out);
+  GS_REQUIRE(grad_norm_out == nullptr || counter != nullptr,
+             "gs_lars_trust: the grad norm needs a zeroed arrival counter");
+  GS_REQUIRE(nseg <= 24 * 1024, "gs_lars_trust: at most 24576 segments");
+  const size_t dyn = grad_norm_out != nullptr ? sizeof(double) * (size_t)nseg : 0;
+  if (dyn > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(lars_trust_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+  }
+  lars_trust_kernel<<<nseg, kThreads, dyn, (cudaStream_t)stream>>>(
+      segs, nseg, partials, params, seg_scale, seg_out, grad_norm_out, counter);
   return gs_check_launch("gs_lars_trust");
 }
 

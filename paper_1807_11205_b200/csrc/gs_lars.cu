@@ -540,8 +540,9 @@ lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_ac
         const float* w = sp->w + ch.start;
         uint16_t* gc = sp->gcopy != nullptr ? static_cast<uint16_t*>(sp->gcopy) + ch.start : nullptr;
         const bool lars = (fl & GS_SEG_LARS_ENABLED) != 0;
-        const bool bulk = (ch.len & 7) == 0 && gs::is_aligned16(g) && (!lars || gs::is_aligned16(w)) &&
-                          (gc == nullptr || gs::is_aligned16(gc));
+        // a stage holds kFullChunk elements: longer chunks take the global path
+        const bool bulk = (ch.len & 7) == 0 && ch.len <= kFullChunk && gs::is_aligned16(g) &&
+                          (!lars || gs::is_aligned16(w)) && (gc == nullptr || gs::is_aligned16(gc));
         mine = StageMeta{g, w, gc, ch.len, ch.seg, c, fl, bulk ? 1 : 0, 0};
       }
       const int cnt = min(32, nmine - base);

@@ -39,7 +39,7 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 #define GS_P1_ROUNDS 4   // pass-1 load batch (vectors per thread)
 #endif
 #ifndef GS_P1_MINB
-#define GS_P1_MINB 1     // pass-1 __launch_bounds__ min blocks per SM
+#define GS_P1_MINB 4     // pass-1 __launch_bounds__ min blocks per SM
 #endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
@@ -63,6 +63,26 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
 __device__ __forceinline__ void sq_acc(double& acc, float x) {
   const double d = (double)x;
   acc = fma(d, d, acc);
+}
+
+// |x| widened to fp64 with integer ops (exact for normal floats and +-0;
+// NOT for subnormals; Inf/NaN map to garbage finite values, which only occurs
+// on steps the flags reject).  F2F.F64.F32 issues on the XU pipe at a quarter
+// of the ALU rate and was pass 1's co-limiter (ncu: XU 43 % busy), so the
+// squares of normal values are widened on the ALU instead.
+__device__ __forceinline__ double f2d_normal_abs(float x) {
+  const uint32_t a = __float_as_uint(x) & 0x7FFFFFFFu;
+  const uint32_t hi = a ? (a >> 3) + 0x38000000u : 0u;
+  return __hiloint2double((int)hi, (int)(a << 29));
+}
+
+__device__ __forceinline__ void sq_acc_int(double& acc, float x) {
+  const double d = f2d_normal_abs(x);
+  acc = fma(d, d, acc);
+}
+
+__device__ __forceinline__ bool is_subnormal_nonzero(float x) {
+  return (__float_as_uint(x) & 0x7FFFFFFFu) - 1u < 0x007FFFFFu;
 }
 
 // release-ordered arrival: the partials this thread stored become visible no
@@ -92,7 +112,11 @@ struct Acc {
 
 // ------------------------------------------------------------ pass 1 body
 // One element pair (x = widened gradient, w = master).
-template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+// GINT: gradients are widened for the squares with integer ops (fp16 input
+// with exact power-of-two scaling: every value is 0, normal, or non-finite).
+// WINT: the same for the masters (the caller checked for subnormals).
+template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool GINT = false,
+          bool WINT = false>
 __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& a) {
   float2 gu;
   if (POW2) {
@@ -110,8 +134,13 @@ __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& 
     a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
   }
   if (LARS) {
-    sq_acc(a.sw, w.x);
-    sq_acc(a.sw, w.y);
+    if (WINT) {
+      sq_acc_int(a.sw, w.x);
+      sq_acc_int(a.sw, w.y);
+    } else {
+      sq_acc(a.sw, w.x);
+      sq_acc(a.sw, w.y);
+    }
     if (DECAY) {
       // eff = g + float32(wd) * w, two roundings (lars.py:172)
       const float2 eff = add2(gu, mul2(make_float2(cx.wd, cx.wd), w));
@@ -120,8 +149,13 @@ __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& 
     }
   }
   if (GNORM || (LARS && !DECAY)) {
-    sq_acc(a.sg, gu.x);
-    sq_acc(a.sg, gu.y);
+    if (GINT) {
+      sq_acc_int(a.sg, gu.x);
+      sq_acc_int(a.sg, gu.y);
+    } else {
+      sq_acc(a.sg, gu.x);
+      sq_acc(a.sg, gu.y);
+    }
   }
 }
 
@@ -170,10 +204,26 @@ __device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& w
     a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
              raw_nonfinite_bits(r.w);
   }
+  constexpr bool GINT = F16 && POW2;
+  bool wsub = false;
+  if (LARS) {
+    wsub = is_subnormal_nonzero(wv.a.x) | is_subnormal_nonzero(wv.a.y) |
+           is_subnormal_nonzero(wv.a.z) | is_subnormal_nonzero(wv.a.w) |
+           is_subnormal_nonzero(wv.b.x) | is_subnormal_nonzero(wv.b.y) |
+           is_subnormal_nonzero(wv.b.z) | is_subnormal_nonzero(wv.b.w);
+    wsub = __any_sync(__activemask(), wsub);  // warp-uniform: a subnormal master is rare
+  }
+  if (!wsub) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(G<F16>::pair(gv, q),
-                                               LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+    for (int q = 0; q < 4; ++q)
+      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, true>(
+          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, false>(
+          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+  }
 }
 
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
@@ -268,7 +318,7 @@ __device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg
 // arrives last is timing-dependent, the result is not: the fold always runs
 // over the same chunk range in the same fixed tree.
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
-__global__ void __launch_bounds__(kThreads, GS_P1_MINB)
+__global__ void __launch_bounds__(kThreads, F16 ? GS_P1_MINB : 1)
 lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                   const gs_chunk* __restrict__ chunks, int chunk0,
                   const gs_step_params* __restrict__ params, double* __restrict__ partials,

@@ -416,7 +416,13 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
 // are identical to the register-staged kernel.  Chunks that are
 // not 16-byte aligned (or not a multiple of 8 elements) are reduced from
 // global memory directly by the consumers.
-constexpr int kStages = 4;
+#ifndef GS_TMA_STAGES
+#define GS_TMA_STAGES 2   // stages per CTA
+#endif
+#ifndef GS_TMA_CTAS
+#define GS_TMA_CTAS 2     // CTAs per SM (consumer warps per SM = 8 x this)
+#endif
+constexpr int kStages = GS_TMA_STAGES;
 constexpr int kStageG = kFullChunk * 2;      // 16 KB of binary16
 constexpr int kStageW = kFullChunk * 4;      // 32 KB of fp32 master
 constexpr int kStageBytes = kStageG + kStageW;
@@ -551,7 +557,7 @@ __device__ __forceinline__ void finish_chunk_warp(const gs_segment* __restrict__
 }
 
 template <bool POW2, bool RAWFLAG, bool GNORM, bool FUSE>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+__global__ void __launch_bounds__(kTmaThreads, GS_TMA_CTAS)
 lars_pass1_tma_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                       const gs_chunk* __restrict__ chunks, int chunk0, int nchunk,
                       const gs_step_params* __restrict__ params, double* __restrict__ partials,
@@ -892,7 +898,7 @@ int launch_tma(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk
       return gs_check_launch("gs_lars_pass1 (smem attribute)");
     attr = true;
   }
-  int grid = sm_count();
+  int grid = GS_TMA_CTAS * sm_count();
   if (grid > nchunk) grid = nchunk;
   lars_pass1_tma_kernel<P, R, N, FUSE><<<grid, kTmaThreads, kTmaSmem, s>>>(
       segs, nseg, nseg_active, chunks, chunk0, nchunk, params, partials, flags, counters, seg_scale,

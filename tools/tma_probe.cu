@@ -7,6 +7,7 @@
 #include "../paper_1807_11205_b200/csrc/gs_common.cuh"
 
 void gs_set_error(const char*, ...) {}
+
 int gs_check_launch(const char*) { return 0; }
 
 constexpr int kChunk = 8192;
@@ -79,10 +80,15 @@ __global__ void __launch_bounds__(288, 1) probe(const uint16_t* g, const float* 
   if (acc + accf == 12345.0) out[0] = acc + accf;
 }
 
+struct Meta { long idx; long pad; };
 // plain register-staged reference: one CTA per chunk, loads then math
-template <int MODE>
-__global__ void __launch_bounds__(256) plain(const uint16_t* g, const float* w, int nchunk, double* out) {
-  const long c = blockIdx.x;
+// META: the chunk index comes through two dependent loads (chunk table ->
+// segment table) like the real kernel; RED: block reduction + partial store
+template <int MODE, bool META = false, bool RED = false>
+__global__ void __launch_bounds__(256) plain(const uint16_t* g, const float* w, int nchunk, double* out,
+                                             const int* ctab = nullptr, const Meta* stab = nullptr) {
+  long c = blockIdx.x;
+  if (META) c = stab[ctab[blockIdx.x]].idx;
   const uint4* sg = reinterpret_cast<const uint4*>(g + c * kChunk);
   const float4* sw = reinterpret_cast<const float4*>(w + c * kChunk);
   uint4 gv[4];
@@ -113,7 +119,11 @@ __global__ void __launch_bounds__(256) plain(const uint16_t* g, const float* w, 
       }
     }
   }
-  if (acc + accf == 12345.0) out[0] = acc + accf;
+  if (RED) {
+    double b = acc, cc = acc * 2, d = acc * 3;
+    gs::block_sum3<256>(acc, b, cc);
+    if (threadIdx.x == 0) { out[3 * blockIdx.x] = acc; out[3 * blockIdx.x + 1] = b; out[3 * blockIdx.x + 2] = cc + d; }
+  } else if (acc + accf == 12345.0) out[0] = acc + accf;
 }
 
 template <typename F>
@@ -138,7 +148,15 @@ int main() {
   double* out;
   cudaMalloc(&g, (size_t)nchunk * kG);
   cudaMalloc(&w, (size_t)nchunk * kW);
-  cudaMalloc(&out, 8);
+  cudaMalloc(&out, 8 * 3 * 8192);
+  int* ctab; Meta* stab;
+  cudaMalloc(&ctab, 4 * nchunk); cudaMalloc(&stab, sizeof(Meta) * nchunk);
+  {
+    int* h = new int[nchunk]; Meta* m = new Meta[nchunk];
+    for (int i = 0; i < nchunk; ++i) { h[i] = i; m[i].idx = i; m[i].pad = 0; }
+    cudaMemcpy(ctab, h, 4 * nchunk, cudaMemcpyHostToDevice);
+    cudaMemcpy(stab, m, sizeof(Meta) * nchunk, cudaMemcpyHostToDevice);
+  }
   cudaMemset(g, 0, (size_t)nchunk * kG);
   cudaMemset(w, 0, (size_t)nchunk * kW);
   int sms;
@@ -160,5 +178,11 @@ int main() {
            cudaGetErrorString(cudaGetLastError()));                                              \
   }
   RUN_R(1) RUN_R(2)
+#define RUN_X(M, A, B)                                                                           \
+  {                                                                                              \
+    float ms = time_it([&] { plain<M, A, B><<<nchunk, 256>>>(g, w, nchunk, out, ctab, stab); });  \
+    printf("regs mode=%d meta=%d red=%d: %8.1f us  %7.1f GB/s\n", M, A, B, ms * 1e3, bytes / ms / 1e6); \
+  }
+  RUN_X(2, true, false) RUN_X(2, false, true) RUN_X(2, true, true)
   return 0;
 }

@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
-    ap.add_argument("--algorithm", default="ring", choices=["ring", "hierarchical", "sharded"])
+    ap.add_argument("--algorithm", default="ring",
+                    choices=["ring", "hierarchical", "sharded", "ordered"])
     ap.add_argument("--group-size", type=int, default=4, help="k of Topology(p, k)")
     ap.add_argument("--eta-bytes", type=int, default=None,
                     help="hybrid threshold; default: 0 for ring, inf otherwise")
@@ -198,7 +199,8 @@ def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, wa
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    eta = args.eta_bytes if args.eta_bytes is not None else (0 if args.algorithm == "ring" else 1 << 62)
+    flat = args.algorithm in ("ring", "ordered")
+    eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     r = cpu_reference(args.model, world, args.theta, eta, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
@@ -233,13 +235,15 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     n_params = sh.total_params(specs)
     comm = None
     if world > 1:
-        k = args.group_size if args.algorithm != "ring" else 1
+        k = args.group_size if args.algorithm in ("hierarchical", "sharded") else 1
         comm = Communicator(gs.Topology(world, k if world % k == 0 else 1))
-    eta = args.eta_bytes if args.eta_bytes is not None else (0 if args.algorithm == "ring" else 1 << 62)
+    flat = args.algorithm in ("ring", "ordered")
+    eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0, weight_decay=5e-4,
                         momentum=0.9)
     pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=args.theta, comm=comm, eta_bytes=eta,
-                               hier_variant=args.algorithm if args.algorithm != "ring" else "hierarchical",
+                               hier_variant=args.algorithm if not flat else "hierarchical",
+                               flat_variant="ordered" if args.algorithm == "ordered" else "ring",
                                init_master=sh.synth_master(specs, seed=0),
                                loss_scale=gs.LossScale(1024.0), device=dev)
     grads_host = torch.from_numpy(sh.synth_wire_grads(specs, rank=rank, seed=0)).pin_memory()
@@ -405,6 +409,8 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k)]
     comms = {}
     s0 = torch.cuda.current_stream(dev)
+    variants.append(("ordered", 1))
+    ow = None
     for name, k in variants:
         if k not in comms:
             comms[k] = Communicator(gs.Topology(world, k))
@@ -412,8 +418,19 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
         algo = name.split("_")[0]
         n = buf.numel() - buf.numel() % (k * 8)
         t = buf[:n]
+        if algo == "ordered":
+            from paper_1807_11205_b200.dist import OrderedWire
+            ow = ow or OrderedWire(comm, pipe.total, dev)
+            half = [0]
+
+            def run_ordered(_t=None):
+                ow.allreduce(half[0], 0, n, int(s0.cuda_stream))
+                half[0] ^= 1
+            comm_allreduce = run_ordered
+        else:
+            comm_allreduce = (lambda _t, _c=comm, _a=algo: _c.allreduce(_t, _a))
         for _ in range(3):
-            comm.allreduce(t, algo)
+            comm_allreduce(t)
         torch.cuda.synchronize(dev)
         dist.barrier(device_ids=[local])
         a = torch.cuda.Event(enable_timing=True)
@@ -421,7 +438,7 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
         iters = 10
         a.record(s0)
         for _ in range(iters):
-            comm.allreduce(t, algo)
+            comm_allreduce(t)
         b.record(s0)
         b.synchronize()
         ms = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=dev)

@@ -53,7 +53,7 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
                            ((size_t)phase * gridDim.x + blockIdx.x) * p + q;
     uint32_t spins = 0;
     while (ld_acquire_sys(mine) != epoch) {
-      if (++spins > (1u << 28)) __trap();
+      if (++spins > (1u << 24)) __trap();
     }
   }
   __syncthreads();

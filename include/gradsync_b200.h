@@ -232,6 +232,20 @@ int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
 /* Write `nbytes` of 0 to dst with a kernel (L2 flush helper / flag reset). */
 int gs_fill_zero(void* dst, int64_t nbytes, void* stream);
 
+/* gs_lars_trust fused into gs_lars_pass2 (one launch over the whole chunk
+ * table): every CTA folds its own segment's chunk partials (same order as
+ * gs_lars_trust, so every CTA of a segment derives the same fp32 scale)
+ * while its chunk is prefetched into L2; the segment's first CTA writes
+ * seg_scale/seg_out, and the last of those (of nseg_active segments owning a
+ * chunk; arrival counter, one zeroed uint32) writes the empty segments and
+ * *grad_norm_out.  Nothing is written
+ * when (*flags & flag_mask) (lars.py:161-163). */
+int gs_lars_pass2_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
+                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params, uint32_t hint,
+                        const double* partials, float* seg_scale, double* seg_out,
+                        double* grad_norm_out, uint32_t* counter, const uint32_t* flags,
+                        uint32_t flag_mask, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

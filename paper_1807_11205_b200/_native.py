@@ -80,6 +80,9 @@ SIGNATURES = {
     "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
                               c_void_p, c_void_p, c_uint32, c_void_p]),
     "gs_fill_zero": (c_int, [c_void_p, c_int64, c_void_p]),
+    "gs_lars_pass2_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, c_void_p,
+                                    c_uint32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_uint32, c_void_p]),
     "gs_ordered_allreduce_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64, c_int64,
                                          c_uint32, c_int, c_void_p, c_void_p]),
 }

@@ -183,6 +183,9 @@ class LarsPlan:
         # pass 1 through per-chunk arrival counters costs a release atomic
         # per chunk on the critical path (61 vs 43 us); see DESIGN.md §4
         self.fuse_trust = False
+        # the trust ratio folded into pass 2 (each CTA re-derives its
+        # segment's scale; removes the trust launch); see DESIGN.md §4
+        self.trust_in_pass2 = True
 
     def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
         """A segment table identical to the base one except for the gradient
@@ -252,15 +255,36 @@ class LarsPlan:
                      dev.ptr(self.grad_norm), dev.ptr(self.counters[self.nseg:]), stream_h)
 
     def pass2(self, stream_h: int, g_is_f16: bool, flag_mask: int, chunk0: int = 0,
-              nchunk: int | None = None):
+              nchunk: int | None = None, trust: bool = False):
+        """trust=True: gs_lars_pass2_trust (the trust ratio folded per CTA,
+        no separate trust launch; needs pass 1 without fusion)."""
         n = self.nchunk - chunk0 if nchunk is None else nchunk
+        if trust:
+            _native.call("gs_lars_pass2_trust", dev.ptr(self.d_segs), self.nseg, self.nseg_active,
+                         dev.ptr(self.d_chunks), chunk0, n, 1 if g_is_f16 else 0,
+                         dev.ptr(self.params), self.hint, dev.ptr(self.partials),
+                         dev.ptr(self.seg_scale), dev.ptr(self.seg_out), dev.ptr(self.grad_norm),
+                         dev.ptr(self.counters[self.nseg:]), dev.ptr(self.flags), flag_mask,
+                         stream_h)
+            return
         _native.call("gs_lars_pass2", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
                      1 if g_is_f16 else 0, dev.ptr(self.params), self.hint, dev.ptr(self.seg_scale),
                      dev.ptr(self.flags), flag_mask, stream_h)
 
-    def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
-        self.reset_flags(stream_h)
-        self.pass1(stream_h, g_is_f16)
+    @property
+    def trust_via_pass2(self) -> bool:
+        return not self.fused and self.trust_in_pass2 and self.nseg_active > 0
+
+    def finish(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
+        """trust (unless pass 1 fused it) + pass 2, in the configured form."""
+        if self.trust_via_pass2:
+            self.pass2(stream_h, g_is_f16, flag_mask, trust=True)
+            return
         if not self.fused:
             self.trust(stream_h)
         self.pass2(stream_h, g_is_f16, flag_mask)
+
+    def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
+        self.reset_flags(stream_h)
+        self.pass1(stream_h, g_is_f16)
+        self.finish(stream_h, g_is_f16, flag_mask)

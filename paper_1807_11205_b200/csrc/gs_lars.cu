@@ -846,11 +846,25 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
   }
 }
 
-template <bool F16, bool POW2>
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// TRUST: the CTA first derives its segment's trust ratio itself — the fold
+// of gs_lars_trust (256-strided + fixed block tree, so the same bits in every
+// CTA of the segment) — while its chunk streams into L2 behind
+// prefetch.global.L2; the first CTA of a segment publishes seg_scale/seg_out
+// and the last to do so (arrival counter) the empty segments and grad norm.
+// This removes the separate trust launch and its serial tail.
+template <bool F16, bool POW2, bool TRUST>
 __global__ void __launch_bounds__(kThreads)
-lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int chunk0,
-                  const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
-                  const uint32_t* __restrict__ flags, uint32_t flag_mask) {
+lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
+                  const gs_chunk* __restrict__ chunks,
+                  int chunk0, const gs_step_params* __restrict__ params,
+                  const double* __restrict__ partials, float* __restrict__ seg_scale,
+                  double* __restrict__ seg_out, double* __restrict__ grad_norm_out,
+                  uint32_t* __restrict__ counter, const uint32_t* __restrict__ flags,
+                  uint32_t flag_mask) {
   using T = typename G<F16>::T;
   // lars.py:161-163 — a non-finite step mutates nothing
   if (*flags & flag_mask) return;
@@ -867,7 +881,58 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
   cx.m = params->momentum;
-  const float s = seg_scale[ch.seg];
+  float s;
+  if (TRUST) {
+    __shared__ float s_scale;
+    __shared__ int s_last;
+    // stream the chunk towards L2 while the fold runs (one prefetch per line)
+    const int lg = (ch.len * (int)sizeof(T) + 127) / 128, lw = (ch.len * 4 + 127) / 128;
+    for (int i = threadIdx.x; i < lg + 2 * lw; i += kThreads) {
+      if (i < lg) prefetch_l2(reinterpret_cast<const char*>(g) + 128 * i);
+      else if (i < lg + lw) prefetch_l2(reinterpret_cast<const char*>(w) + 128 * (i - lg));
+      else prefetch_l2(reinterpret_cast<const char*>(v) + 128 * (i - lg - lw));
+    }
+    const int cb = sgp->chunk_begin, cn = sgp->chunk_count;
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (int i = threadIdx.x; i < cn; i += kThreads) {
+      const double* pp = partials + 3 * (int64_t)(cb + i);
+      x += pp[0];
+      y += pp[1];
+      z += pp[2];
+    }
+    gs::block_sum3<kThreads>(x, y, z);
+    if (threadIdx.x == 0) {
+      double o[4];
+      float sc;
+      trust_eval(sflags, x, y, z, params, &sc, o);
+      s_scale = sc;
+      s_last = 0;
+      if (c == cb) {  // the segment's first chunk publishes its statistics
+        seg_scale[ch.seg] = sc;
+        double* so = seg_out + 4 * (int64_t)ch.seg;
+        so[0] = o[0];
+        so[1] = o[1];
+        so[2] = o[2];
+        so[3] = o[3];
+        s_last = grad_norm_out != nullptr && counter != nullptr;
+      }
+    }
+    __syncthreads();
+    s = s_scale;
+    if (s_last) {  // one thread only (the fold above was block-wide)
+      if (threadIdx.x == 0) {
+        if (arrive_release(counter) + 1 == (uint32_t)nseg_active) {
+          __threadfence();
+          for (int q = 0; q < nseg; ++q)
+            if (segs[q].chunk_count == 0)
+              trust_eval(segs[q].flags, 0.0, 0.0, 0.0, params, seg_scale + q, seg_out + 4 * (int64_t)q);
+          *grad_norm_out = grad_norm_eval(seg_out, nseg);
+        }
+      }
+    }
+  } else {
+    s = seg_scale[ch.seg];
+  }
   const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
   if (decay)
     p2_chunk<F16, POW2, true>(g, w, v, w16, ch.len, cx, s);
@@ -1010,8 +1075,11 @@ int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   GS_REQUIRE(segs && chunks && params && seg_scale && flags, "gs_lars_pass2: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const bool pow2 = hint & GS_HINT_POW2;
-#define GS_P2(F, P) \
-  lars_pass2_kernel<F, P><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params, seg_scale, flags, flag_mask)
+  float* sc = const_cast<float*>(seg_scale);
+#define GS_P2(F, P)                                                                              \
+  lars_pass2_kernel<F, P, false><<<nchunk, kThreads, 0, s>>>(segs, 0, 0, chunks, chunk0, params, \
+                                                             nullptr, sc, nullptr, nullptr,      \
+                                                             nullptr, flags, flag_mask)
   if (g_is_f16) {
     if (pow2) GS_P2(true, true); else GS_P2(true, false);
   } else {
@@ -1019,6 +1087,35 @@ int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   }
 #undef GS_P2
   return gs_check_launch("gs_lars_pass2");
+}
+
+int gs_lars_pass2_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
+                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params, uint32_t hint,
+                        const double* partials, float* seg_scale, double* seg_out,
+                        double* grad_norm_out, uint32_t* counter, const uint32_t* flags,
+                        uint32_t flag_mask, void* stream) {
+  GS_REQUIRE(nchunk >= 0 && chunk0 >= 0 && nseg_active >= 1 && nseg_active <= nseg,
+             "gs_lars_pass2_trust: bad range (1 <= nseg_active <= nseg)");
+  if (nchunk == 0) return GS_OK;
+  GS_REQUIRE(segs && chunks && params && partials && seg_scale && seg_out && flags,
+             "gs_lars_pass2_trust: null pointer");
+  GS_REQUIRE(grad_norm_out == nullptr || counter != nullptr,
+             "gs_lars_pass2_trust: the grad norm needs a zeroed arrival counter");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool pow2 = hint & GS_HINT_POW2;
+#define GS_P2T(F, P)                                                                             \
+  lars_pass2_kernel<F, P, true><<<nchunk, kThreads, 0, s>>>(segs, nseg, nseg_active, chunks,     \
+                                                            chunk0, params,                      \
+                                                            partials, seg_scale, seg_out,        \
+                                                            grad_norm_out, counter, flags,       \
+                                                            flag_mask)
+  if (g_is_f16) {
+    if (pow2) GS_P2T(true, true); else GS_P2T(true, false);
+  } else {
+    if (pow2) GS_P2T(false, true); else GS_P2T(false, false);
+  }
+#undef GS_P2T
+  return gs_check_launch("gs_lars_pass2_trust");
 }
 
 }  // extern "C"

@@ -100,11 +100,18 @@ class Communicator:
                     self.cross = pg
 
     # -- the three algorithms; all in place, sum, on the caller's current stream
+    # (binary16 bit patterns travel as float16: NCCL has no uint16 type)
+    @staticmethod
+    def _wire(t: torch.Tensor) -> torch.Tensor:
+        return t.view(torch.float16) if t.dtype == torch.uint16 else t
+
     def allreduce_ring(self, t: torch.Tensor, async_op: bool = False):
-        return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.world, async_op=async_op)
+        return dist.all_reduce(self._wire(t), op=dist.ReduceOp.SUM, group=self.world,
+                               async_op=async_op)
 
     def allreduce_hierarchical(self, t: torch.Tensor):
         """Literal three-phase: reduce to master, masters all-reduce, broadcast."""
+        t = self._wire(t)
         topo = self.topo
         if topo.k > 1:
             dist.reduce(t, dst=self.master, op=dist.ReduceOp.SUM, group=self.intra)
@@ -116,6 +123,7 @@ class Communicator:
     def allreduce_sharded(self, t: torch.Tensor):
         """Reduce-scatter inside the group, all-reduce the shard across groups,
         all-gather inside the group.  t.numel() must be a multiple of k."""
+        t = self._wire(t)
         topo = self.topo
         k = topo.k
         if k == 1:

@@ -140,7 +140,8 @@ class GradientPipeline:
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
-                 bulk: bool = False, fuse_trust: bool = False, flat_variant: str = "ring"):
+                 bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = True,
+                 flat_variant: str = "ring"):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -203,6 +204,7 @@ class GradientPipeline:
         if bulk:
             self.plan.extra_hint &= ~_native.HINT_NO_BULK
         self.plan.fuse_trust = fuse_trust
+        self.plan.trust_in_pass2 = trust_in_pass2
         begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]
         c = 0
         for b in self.buckets:
@@ -475,14 +477,19 @@ class GradientPipeline:
             self._last_wire = wire
             if self.ordered is not None:
                 self._half ^= 1
-        if timer:
-            timer("trust")
-        if not plan.fused:
-            plan.trust(sh)
-        if timer:
-            timer("pass2")
-        plan.pass2(sh, g_is_f16=True,
-                   flag_mask=_native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE)
+        mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
+        if plan.trust_via_pass2:
+            if timer:
+                timer("pass2")
+            plan.pass2(sh, g_is_f16=True, flag_mask=mask, trust=True)
+        else:
+            if timer:
+                timer("trust")
+            if not plan.fused:
+                plan.trust(sh)
+            if timer:
+                timer("pass2")
+            plan.pass2(sh, g_is_f16=True, flag_mask=mask)
         plan.use_segments(None)
         if timer:
             timer("end")

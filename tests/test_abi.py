@@ -82,6 +82,6 @@ def test_no_packed_fp32_contraction_in_sass():
         assert op not in sass
     # pass-2 specialisation for power-of-two scaling: pure FMUL/FADD
     funcs = sass.split("Function : ")
-    p2 = [f for f in funcs if "lars_pass2_kernelILb1ELb1E" in f.split("\n", 1)[0]]
+    p2 = [f for f in funcs if "lars_pass2_kernelILb1ELb1ELb0E" in f.split("\n", 1)[0]]
     assert p2, "pow2 pass-2 kernel missing"
     assert "FFMA" not in p2[0]

@@ -119,9 +119,9 @@ def run_vs_oracle(model, p, theta, steps=2, loss_scale=1024.0, wd=5e-4, eta_byte
     return pipe
 
 
-@pytest.mark.parametrize("kw", [{}, {"bulk": True}, {"fuse_trust": True},
-                                {"bulk": True, "fuse_trust": True}, {"fused_pack": False},
-                                {"use_graph": False}])
+@pytest.mark.parametrize("kw", [{}, {"trust_in_pass2": False}, {"bulk": True},
+                                {"fuse_trust": True}, {"bulk": True, "fuse_trust": True},
+                                {"fused_pack": False}, {"use_graph": False}])
 def test_resnet50_single_gpu_matches_oracle(kw):
     pipe = run_vs_oracle("resnet50", 1, 4 << 20, steps=3, **kw)
     # the fused packer left the reference's bucket payloads in the wire

@@ -328,15 +328,14 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        arena = pipe.grad_arena()
         e2e_ms = []
         for i in range(max(2, min(args.steps, 10))):
             flush_l2()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            pipe.prepare(1000 + i)
             a.record(s0)
-            arena.copy_(grads_host, non_blocking=True)
-            pipe.enqueue(arena, 1000 + i)
+            pipe.enqueue_host(grads_host, 1000 + i)  # H2D per bucket, overlapped
             pipe.finish()
             b.record(s0)
             b.synchronize()
@@ -363,7 +362,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     tfile = ROOT / "profiles" / "pass2_traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.model)
-    update_bytes = 26 * n_params + 4 * n_params  # pass1+pass2 (26 B) + pack (4 B)
+    # algorithmic bytes of the update kernels per element: pass 1 reads g (2)
+    # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); packing adds
+    # 2 (fused into pass 1 at p = 1: the wire write) or 4 (separate packer)
+    update_bytes = (26 + (2 if world == 1 else 4)) * n_params
     line = {
         "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),

@@ -494,6 +494,65 @@ class GradientPipeline:
         if timer:
             timer("end")
 
+    def _bucket_host_ranges(self):
+        """Per bucket, the [lo, hi) element range of the registration-order
+        flat gradient that holds exactly its tensors, or None when a bucket's
+        tensors are not contiguous in registration order (custom orders)."""
+        if getattr(self, "_host_ranges", "unset") != "unset":
+            return self._host_ranges
+        offs = np.concatenate([[0], np.cumsum(self.sizes)])
+        ranges = []
+        for bk in self.buckets:
+            idx = sorted(bk.params)
+            if idx != list(range(idx[0], idx[-1] + 1)):
+                ranges = None
+                break
+            ranges.append((int(offs[idx[0]]), int(offs[idx[-1] + 1])))
+        self._host_ranges = ranges
+        return ranges
+
+    def enqueue_host(self, host_flat: torch.Tensor, step: int) -> None:
+        """One step from a pinned host fp16 gradient (registration order): the
+        host->device copy is split per bucket on a copy stream and pass 1 of
+        bucket b starts as soon as bucket b has landed, so the PCIe transfer
+        overlaps the update (p = 1, fused packer); otherwise one copy then
+        the regular step."""
+        arena = self.grad_arena()
+        s0 = torch.cuda.current_stream(self.device)
+        ranges = self._bucket_host_ranges() if self.fused_pack else None
+        if ranges is None:
+            arena.copy_(host_flat.reshape(-1), non_blocking=True)
+            self.enqueue(arena, step)
+            return
+        if self._prepared != step:
+            self.prepare(step)
+        self._prepared = None
+        tabs, _ = self._sources(arena)
+        plan = self.plan
+        sh = int(s0.cuda_stream)
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        cs = self._copy_stream
+        cs.wait_stream(s0)
+        src = host_flat.reshape(-1)
+        evs = []
+        with torch.cuda.stream(cs):
+            for lo, hi in ranges:
+                arena[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                evs.append(ev)
+        plan.upload_params(s0)
+        plan.use_segments(tabs[1])
+        plan.reset_flags(sh)
+        for bk, ev in zip(self.buckets, evs):
+            s0.wait_event(ev)
+            plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+        mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
+        plan.finish(sh, True, mask)
+        plan.use_segments(None)
+        self._last_wire = self.wire
+
     def finish(self) -> StepResult:
         """Read the step's flags (the one host sync) and advance LossScale
         exactly as experiment.py:403-413 does."""

@@ -207,3 +207,20 @@ def test_fp32_lars_step_api_matches_oracle(golden):
                 assert np.array_equal(grp.velocity.cpu().numpy().view(np.uint32),
                                       g[f"c{ci}_s{step}_v_{gi}"].view(np.uint32))
                 assert np.array_equal(grp.working_w16.cpu().numpy(), g[f"c{ci}_s{step}_h_{gi}"])
+
+
+def test_host_gradient_path_matches_device_path():
+    """enqueue_host (per-bucket H2D overlapped with pass 1) == device path."""
+    specs = sh.load_shapes("resnet50")
+    master = sh.synth_master(specs, seed=0)
+    cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
+    a = gs.GradientPipeline(specs, cfg, threshold_bytes=4 << 20, init_master=master)
+    b = gs.GradientPipeline(specs, cfg, threshold_bytes=4 << 20, init_master=master)
+    for step in range(2):
+        host = torch.from_numpy(sh.synth_wire_grads(specs, rank=0, seed=step)).pin_memory()
+        ra = a.step(host.cuda(), step)
+        b.enqueue_host(host, step)
+        rb = b.finish()
+        assert ra.applied == rb.applied and ra.grad_norm == rb.grad_norm
+        assert torch.equal(a.master, b.master) and torch.equal(a.working, b.working)
+        assert torch.equal(a.velocity, b.velocity)

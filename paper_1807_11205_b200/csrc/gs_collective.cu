@@ -103,24 +103,38 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
 #pragma unroll
   for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q] + lo);
   const int64_t nv = vec ? (hi - lo) / 8 : 0;
-  for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-    uint4 raw[P];
+  // kU vectors per thread in flight from every peer before any arithmetic
+  // (NVLink latency is ~2 us; a ring's worth of bandwidth needs MBs in flight)
+  constexpr int kU = P <= 4 ? 4 : 2;
+  for (int64_t base = threadIdx.x; base < nv; base += kU * kThreads) {
+    uint4 raw[kU][P];
 #pragma unroll
-    for (int q = 0; q < P; ++q) raw[q] = __ldcv(reinterpret_cast<const uint4*>(src[q] + lo) + i);
-    uint32_t o[4];
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * kThreads;
+      if (i < nv) {
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      float a[P], b[P];
-#pragma unroll
-      for (int q = 0; q < P; ++q) {
-        const float2 f = gs::widen2((&raw[q].x)[h]);
-        a[q] = f.x;
-        b[q] = f.y;
+        for (int q = 0; q < P; ++q) raw[u][q] = __ldcv(reinterpret_cast<const uint4*>(src[q] + lo) + i);
       }
-      o[h] = gs::narrow2(tree<P>(a), tree<P>(b));
-      bad |= ((o[h] & 0x7C00u) == 0x7C00u) | ((o[h] & 0x7C000000u) == 0x7C000000u);
     }
-    reinterpret_cast<uint4*>(mine + lo)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * kThreads;
+      if (i >= nv) break;
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float a[P], b[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const float2 f = gs::widen2((&raw[u][q].x)[h]);
+          a[q] = f.x;
+          b[q] = f.y;
+        }
+        o[h] = gs::narrow2(tree<P>(a), tree<P>(b));
+        bad |= ((o[h] & 0x7C00u) == 0x7C00u) | ((o[h] & 0x7C000000u) == 0x7C000000u);
+      }
+      reinterpret_cast<uint4*>(mine + lo)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
   for (int64_t i = lo + nv * 8 + threadIdx.x; i < hi; i += kThreads) {
     float v[P];
@@ -144,7 +158,15 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
     const int64_t m = v2 ? (hi - lo) / 8 : 0;
     const uint4* s4 = reinterpret_cast<const uint4*>(src[r] + lo);
     uint4* d4 = reinterpret_cast<uint4*>(mine + lo);
-    for (int64_t i = threadIdx.x; i < m; i += kThreads) d4[i] = __ldcv(s4 + i);
+    for (int64_t base = threadIdx.x; base < m; base += 8 * kThreads) {
+      uint4 t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (base + u * kThreads < m) t[u] = __ldcv(s4 + base + u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (base + u * kThreads < m) d4[base + u * kThreads] = t[u];
+    }
     for (int64_t i = lo + m * 8 + threadIdx.x; i < hi; i += kThreads) mine[i] = __ldcv(src[r] + i);
   }
 }
@@ -164,11 +186,20 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
   if (p == 1 || n == 0) return GS_OK;
   GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_f16: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
+  // every CTA waits for its counterparts on the peers, so the whole grid must
+  // be co-resident: clamp to what the occupancy calculator guarantees (the
+  // same on every rank of a homogeneous box, so the signal layout agrees)
 #define GS_OAR(P)                                                                                 \
-  case P:                                                                                         \
-    ordered_allreduce_kernel<P><<<nblocks, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,    \
-                                                             nonfinite);                          \
-    break;
+  case P: {                                                                                       \
+    int per_sm = 0, dev = 0, sms = 0;                                                             \
+    cudaGetDevice(&dev);                                                                          \
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_allreduce_kernel<P>, kThreads, 0); \
+    const int nb = per_sm > 0 ? min(nblocks, per_sm * sms) : 1;                                  \
+    ordered_allreduce_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,        \
+                                                        nonfinite);                               \
+    break;                                                                                        \
+  }
   switch (p) {
     GS_OAR(2)
     GS_OAR(3)

@@ -812,11 +812,14 @@ __device__ __forceinline__ F8 ld8(const float* p, int i) {
   return F8{q[0], q[1]};
 }
 
-template <bool F16, bool POW2, bool DECAY>
+// `scale_of()` yields the segment's fp32 trust scale; it is called by every
+// thread after the first batch's loads are in flight, so a scale that has to
+// be derived on the spot (TRUST) overlaps the loads' latency.
+template <bool F16, bool POW2, bool DECAY, typename ScaleFn>
 __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ g,
                                          float* __restrict__ w, float* __restrict__ v,
                                          uint16_t* __restrict__ w16, int len, const Ctx& cx,
-                                         float s) {
+                                         ScaleFn scale_of) {
   using Gt = G<F16>;
   const bool vec = gs::is_aligned16(g) && gs::is_aligned16(w) && gs::is_aligned16(v) &&
                    gs::is_aligned16(w16);
@@ -826,13 +829,20 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
   // the arithmetic and stores (stores cannot alias the next batch's loads,
   // but the compiler cannot prove it through the casts)
   int done = 0;
+  float s = 0.0f;
+  bool have_s = false;
   for (; done + 2 * kThreads <= nv; done += 2 * kThreads) {
     const int i0 = done + t, i1 = i0 + kThreads;
     const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
     const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
+    if (!have_s) {  // uniform: every thread runs the first batch
+      s = scale_of();
+      have_s = true;
+    }
     p2_vec<F16, POW2, DECAY>(g0, w0, v0, w, v, w16, i0, cx, s);
     p2_vec<F16, POW2, DECAY>(g1, w1, v1, w, v, w16, i1, cx, s);
   }
+  if (!have_s) s = scale_of();
   for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
     p2_vec<F16, POW2, DECAY>(gv, ld8(w, i), ld8(v, i), w, v, w16, i, cx, s);
@@ -850,12 +860,12 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// TRUST: the CTA first derives its segment's trust ratio itself — the fold
-// of gs_lars_trust (256-strided + fixed block tree, so the same bits in every
-// CTA of the segment) — while its chunk streams into L2 behind
-// prefetch.global.L2; the first CTA of a segment publishes seg_scale/seg_out
-// and the last to do so (arrival counter) the empty segments and grad norm.
-// This removes the separate trust launch and its serial tail.
+// TRUST: the CTA derives its segment's trust ratio itself — the fold of
+// gs_lars_trust (256-strided + fixed block tree, so the same bits in every
+// CTA of the segment) — while its first batch of loads is in flight; the
+// first CTA of a segment publishes seg_scale/seg_out and the last to do so
+// (arrival counter) the empty segments and grad norm.  This removes the
+// separate trust launch and its serial tail.
 template <bool F16, bool POW2, bool TRUST>
 __global__ void __launch_bounds__(kThreads)
 lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
@@ -881,17 +891,10 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
   cx.m = params->momentum;
-  float s;
-  if (TRUST) {
+  auto scale_of = [&]() -> float {
+    if (!TRUST) return seg_scale[ch.seg];
     __shared__ float s_scale;
     __shared__ int s_last;
-    // stream the chunk towards L2 while the fold runs (one prefetch per line)
-    const int lg = (ch.len * (int)sizeof(T) + 127) / 128, lw = (ch.len * 4 + 127) / 128;
-    for (int i = threadIdx.x; i < lg + 2 * lw; i += kThreads) {
-      if (i < lg) prefetch_l2(reinterpret_cast<const char*>(g) + 128 * i);
-      else if (i < lg + lw) prefetch_l2(reinterpret_cast<const char*>(w) + 128 * (i - lg));
-      else prefetch_l2(reinterpret_cast<const char*>(v) + 128 * (i - lg - lw));
-    }
     const int cb = sgp->chunk_begin, cn = sgp->chunk_count;
     double x = 0.0, y = 0.0, z = 0.0;
     for (int i = threadIdx.x; i < cn; i += kThreads) {
@@ -914,14 +917,8 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
         so[1] = o[1];
         so[2] = o[2];
         so[3] = o[3];
-        s_last = grad_norm_out != nullptr && counter != nullptr;
-      }
-    }
-    __syncthreads();
-    s = s_scale;
-    if (s_last) {  // one thread only (the fold above was block-wide)
-      if (threadIdx.x == 0) {
-        if (arrive_release(counter) + 1 == (uint32_t)nseg_active) {
+        if (grad_norm_out != nullptr && counter != nullptr &&
+            arrive_release(counter) + 1 == (uint32_t)nseg_active) {
           __threadfence();
           for (int q = 0; q < nseg; ++q)
             if (segs[q].chunk_count == 0)
@@ -930,14 +927,14 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
         }
       }
     }
-  } else {
-    s = seg_scale[ch.seg];
-  }
+    __syncthreads();
+    return s_scale;
+  };
   const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
   if (decay)
-    p2_chunk<F16, POW2, true>(g, w, v, w16, ch.len, cx, s);
+    p2_chunk<F16, POW2, true>(g, w, v, w16, ch.len, cx, scale_of);
   else
-    p2_chunk<F16, POW2, false>(g, w, v, w16, ch.len, cx, s);
+    p2_chunk<F16, POW2, false>(g, w, v, w16, ch.len, cx, scale_of);
 }
 
 // ------------------------------------------------------------ dispatch

@@ -174,7 +174,9 @@ class OrderedWire:
         self.p = comm.topo.p
         self.rank = comm.rank
         sms = torch.cuda.get_device_properties(device).multi_processor_count
-        self.nblocks = nblocks or max(1, min(sms, 128))
+        # all CTAs must be co-resident (they wait on their peers' CTAs): two
+        # 512-thread CTAs per SM fit next to anything else that is running
+        self.nblocks = nblocks or 2 * sms
         self.total = (total + 255) // 256 * 256
         sig_words = 2 * self.nblocks * self.p
         sig_elems = (4 * sig_words + 1) // 2 + 256

@@ -45,7 +45,7 @@ def main():
                     plan.extra_hint = 0 if bulk else _native.HINT_NO_BULK
                     plan.set_params(prm.copy(), g_is_f16=True)
                     sh_ = dev.stream_of()
-                    ts, t2, tt = [], [], []
+                    ts, t2, tt, t3 = [], [], [], []
                     for it in range(12):
                         _native.call("gs_fill_zero", flush.data_ptr(), flush.numel(), sh_)
                         plan.reset_flags(sh_)
@@ -63,16 +63,21 @@ def main():
                         plan.pass2(sh_, True, 3)
                         e2 = torch.cuda.Event(enable_timing=True)
                         e2.record()
-                        e2.synchronize()
+                        plan.pass2(sh_, True, 3, trust=True)
+                        e3 = torch.cuda.Event(enable_timing=True)
+                        e3.record()
+                        e3.synchronize()
                         if it >= 2:
                             ts.append(a.elapsed_time(b) * 1e3)
                             t2.append(c2.elapsed_time(e2) * 1e3)
                             tt.append(t0.elapsed_time(c2) * 1e3)
+                            t3.append(e2.elapsed_time(e3) * 1e3)
                     key = f"chunk={ce} gcopy={int(gcopy)} gnorm={int(gn)} bulk={int(bulk)} fuse={int(fuse)}"
                     results[key] = float(np.median(ts))
                     p2 = float(np.median(t2))
                     print(f"{key}: pass1 {results[key]:8.1f} us  ({(6 + 2 * gcopy) * n / results[key] / 1e3:7.0f} GB/s)"
-                          f"   trust {float(np.median(tt)):6.1f} us   pass2 {p2:7.1f} us ({20 * n / p2 / 1e3:7.0f} GB/s)",
+                          f"   trust {float(np.median(tt)):6.1f} us   pass2 {p2:7.1f} us ({20 * n / p2 / 1e3:7.0f} GB/s)"
+                          f"   pass2+trust {float(np.median(t3)):7.1f} us",
                           flush=True)
 
 

@@ -427,6 +427,7 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
 
             def run_ordered(_t=None):
                 ow.allreduce(half[0], 0, n, int(s0.cuda_stream))
+                ow.advance(1, int(s0.cuda_stream))
                 half[0] ^= 1
             comm_allreduce = run_ordered
         else:

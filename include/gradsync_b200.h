@@ -174,13 +174,20 @@ int gs_fold_f16_tree(const uint64_t* slots, int p, int64_t offset, uint16_t* out
  *   sig    device array of p peer-mapped pointers to zero-initialised uint32
  *          signal areas of >= 2 * nblocks * p words each;
  *   offset, n  the bucket (elements) inside every wire;
- *   epoch  nonzero, strictly increasing per call on a given sig area;
+ *   epoch  nonzero, strictly increasing per call on a given sig area; with
+ *          epoch_base != NULL the kernel uses epoch + *epoch_base instead, so
+ *          a captured CUDA graph stays valid when the caller advances the
+ *          device-resident base between replays (gs_counter_add);
  *   nblocks  grid size; all CTAs must be co-resident (<= SMs).
  * The wire must be double-buffered across consecutive calls on the same
  * range (the kernel has no exit barrier).  p <= 8. */
 int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                             int64_t offset, int64_t n, uint32_t epoch, int nblocks,
-                             uint32_t* nonfinite, void* stream);
+                             int64_t offset, int64_t n, uint32_t epoch,
+                             const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
+                             void* stream);
+
+/* *counter += inc on the device (stream-ordered; graph-capturable). */
+int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 
 /* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
 

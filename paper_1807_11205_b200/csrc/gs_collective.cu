@@ -87,7 +87,8 @@ template <int P>
 __global__ void __launch_bounds__(kThreads)
 ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
                          int rank, int64_t offset, int64_t n, uint32_t epoch,
-                         uint32_t* __restrict__ nonfinite) {
+                         const uint32_t* __restrict__ epoch_base, uint32_t* __restrict__ nonfinite) {
+  if (epoch_base != nullptr) epoch += *epoch_base;  // device-resident epochs: graph-replayable
   const uint16_t* src[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
@@ -171,18 +172,22 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
   }
 }
 
+__global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
+
 }  // namespace
 
 extern "C" {
 
 int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                             int64_t offset, int64_t n, uint32_t epoch, int nblocks,
-                             uint32_t* nonfinite, void* stream) {
+                             int64_t offset, int64_t n, uint32_t epoch,
+                             const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
+                             void* stream) {
   GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allreduce_f16: 1 <= p <= 8 (got %d)", p);
   GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allreduce_f16: bad rank %d", rank);
   GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_f16: negative size/offset");
   GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allreduce_f16: bad block count");
-  GS_REQUIRE(epoch != 0, "gs_ordered_allreduce_f16: epoch 0 is the reset value");
+  GS_REQUIRE(epoch != 0 || epoch_base != nullptr,
+             "gs_ordered_allreduce_f16: epoch 0 is the reset value");
   if (p == 1 || n == 0) return GS_OK;
   GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_f16: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -197,7 +202,7 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_allreduce_kernel<P>, kThreads, 0); \
     const int nb = per_sm > 0 ? min(nblocks, per_sm * sms) : 1;                                  \
     ordered_allreduce_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,        \
-                                                        nonfinite);                               \
+                                                        epoch_base, nonfinite);                   \
     break;                                                                                        \
   }
   switch (p) {
@@ -211,6 +216,12 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
   }
 #undef GS_OAR
   return gs_check_launch("gs_ordered_allreduce_f16");
+}
+
+int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream) {
+  GS_REQUIRE(counter != nullptr, "gs_counter_add: null pointer");
+  counter_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(counter, inc);
+  return gs_check_launch("gs_counter_add");
 }
 
 }  // extern "C"

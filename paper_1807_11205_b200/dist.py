@@ -193,14 +193,25 @@ class OrderedWire:
         self.bufs_dev = tabs
         self.sig_dev = dev.upload(np.array([b + 4 * self.total for b in bases], dtype=np.uint64),
                                   device)
-        self.epoch = 0
+        # device-resident epoch base: every call of a step uses base + slot,
+        # and advance() bumps the base once per step on the stream, so the
+        # kernels can be captured into a CUDA graph and replayed
+        self.epoch_base = torch.zeros(1, dtype=torch.int32, device=device)
+        self.slots = 0
         dist.barrier()
 
-    def allreduce(self, half: int, offset: int, n: int, stream_h: int) -> None:
+    def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
+        """Bucket all-reduce; `slot` (1-based within the step, < per_step)
+        makes the epoch unique among the step's calls."""
         from . import _device as dev
         from . import _native
 
-        self.epoch = (self.epoch + 1) & 0xFFFFFFFF or 1
         _native.call("gs_ordered_allreduce_f16", dev.ptr(self.bufs_dev[half]),
-                     dev.ptr(self.sig_dev), self.rank, self.p, offset, n, self.epoch,
-                     self.nblocks, None, stream_h)
+                     dev.ptr(self.sig_dev), self.rank, self.p, offset, n, slot + 1,
+                     dev.ptr(self.epoch_base), self.nblocks, None, stream_h)
+
+    def advance(self, per_step: int, stream_h: int) -> None:
+        from . import _device as dev
+        from . import _native
+
+        _native.call("gs_counter_add", dev.ptr(self.epoch_base), per_step, stream_h)

@@ -388,9 +388,13 @@ class GradientPipeline:
             self.prepare(step)
         self._prepared = None
         tabs, key = self._sources(grads)
-        key = (key, self.plan.hint)
+        key = (key, self.plan.hint, self._half)
         self.plan.upload_params(s0)
-        if timer is not None or not self.use_graph or self.comm is not None:
+        # graph replay needs every kernel of the step to be ours: comm = None,
+        # or only ordered (symmetric-memory) buckets, whose epochs live on
+        # the device (NCCL buckets run eagerly)
+        graphable = self.comm is None or all(b.algorithm == "ordered" for b in self.buckets)
+        if timer is not None or not self.use_graph or not graphable:
             self._launch(tabs, s0, timer)
             return
         entry = self._graphs.get(key)
@@ -403,14 +407,19 @@ class GradientPipeline:
         if entry == "warm":
             g = torch.cuda.CUDAGraph()
             n0 = _native.launch_count
+            half = self._half
             with torch.cuda.graph(g):
                 self._launch(tabs, torch.cuda.current_stream(self.device), None)
+            self._half = half  # capture executes nothing: the replay below does
             entry = (g, _native.launch_count - n0)
             _native.launch_count = n0
             self._graphs[key] = entry
         g, nk = entry
         g.replay()
         _native.launch_count += nk
+        if self.ordered is not None:
+            self._last_wire = self.ordered.halves[self._half]
+            self._half ^= 1
 
     def _launch(self, tabs, s0, timer) -> None:
         plan = self.plan
@@ -472,8 +481,11 @@ class GradientPipeline:
                 else:
                     w.wait()
                 if bk.algorithm == "ordered":
-                    self.ordered.allreduce(half, bk.start, bk.length, sh)
+                    self.ordered.allreduce(half, bk.start, bk.length, sh, slot=b)
                 plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+            s0.wait_stream(ps)
+            if self.ordered is not None:
+                self.ordered.advance(len(self.buckets) + 1, sh)
             self._last_wire = wire
             if self.ordered is not None:
                 self._half ^= 1

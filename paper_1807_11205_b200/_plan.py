@@ -184,8 +184,9 @@ class LarsPlan:
         # per chunk on the critical path (61 vs 43 us); see DESIGN.md §4
         self.fuse_trust = False
         # the trust ratio folded into pass 2 (each CTA re-derives its
-        # segment's scale; removes the trust launch); see DESIGN.md §4
-        self.trust_in_pass2 = True
+        # segment's scale) measured no faster than the separate trust kernel
+        # chained to pass 2 by programmatic dependent launch; DESIGN.md §4
+        self.trust_in_pass2 = False
 
     def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
         """A segment table identical to the base one except for the gradient

@@ -129,6 +129,35 @@ int gs_check_launch(const char* what);
     }                              \
   } while (0)
 
+// ---- programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor in the stream is still running; griddep_wait() blocks until
+// that predecessor grid completed and its memory is visible (a no-op when the
+// kernel was launched normally), griddep_launch_dependents() lets the next
+// PDL kernel in the stream start launching.
+namespace gs {
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+}  // namespace gs
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t gs_launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- Blackwell bulk-async copy (TMA engine, non-tensor 1-D form) + mbarrier
 namespace gs {
 

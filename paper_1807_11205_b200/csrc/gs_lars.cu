@@ -733,6 +733,8 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* _
                   const gs_step_params* __restrict__ params, float* __restrict__ seg_scale,
                   double* __restrict__ seg_out, double* __restrict__ grad_norm_out,
                   uint32_t* __restrict__ counter) {
+  gs::griddep_wait();                 // pass 1's partials are complete
+  gs::griddep_launch_dependents();    // let pass 2 start issuing its loads now
   const int s = blockIdx.x;
   const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
   double x = 0.0, y = 0.0, z = 0.0;
@@ -836,13 +838,13 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
     const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
     const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
     if (!have_s) {  // uniform: every thread runs the first batch
-      s = scale_of();
+      if (!scale_of(s)) return;
       have_s = true;
     }
     p2_vec<F16, POW2, DECAY>(g0, w0, v0, w, v, w16, i0, cx, s);
     p2_vec<F16, POW2, DECAY>(g1, w1, v1, w, v, w16, i1, cx, s);
   }
-  if (!have_s) s = scale_of();
+  if (!have_s && !scale_of(s)) return;
   for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
     p2_vec<F16, POW2, DECAY>(gv, ld8(w, i), ld8(v, i), w, v, w16, i, cx, s);
@@ -867,7 +869,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // (arrival counter) the empty segments and grad norm.  This removes the
 // separate trust launch and its serial tail.
 template <bool F16, bool POW2, bool TRUST>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active,
                   const gs_chunk* __restrict__ chunks,
                   int chunk0, const gs_step_params* __restrict__ params,
@@ -876,8 +878,9 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
                   uint32_t* __restrict__ counter, const uint32_t* __restrict__ flags,
                   uint32_t flag_mask) {
   using T = typename G<F16>::T;
-  // lars.py:161-163 — a non-finite step mutates nothing
-  if (*flags & flag_mask) return;
+  // lars.py:161-163 — a non-finite step mutates nothing (the non-TRUST form
+  // checks after griddep_wait: it may run ahead of the trust kernel)
+  if (TRUST && (*flags & flag_mask)) return;
   const int c = chunk0 + blockIdx.x;
   const gs_chunk ch = chunks[c];
   const gs_segment* sgp = segs + ch.seg;
@@ -891,8 +894,16 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
   cx.m = params->momentum;
-  auto scale_of = [&]() -> float {
-    if (!TRUST) return seg_scale[ch.seg];
+  // returns false when the step is rejected (nothing may be stored)
+  auto scale_of = [&](float& out) -> bool {
+    if (!TRUST) {
+      // launched with PDL behind the trust kernel: everything above and the
+      // first batch of loads overlapped it; scales and flags come after
+      gs::griddep_wait();
+      if (*flags & flag_mask) return false;
+      out = seg_scale[ch.seg];
+      return true;
+    }
     __shared__ float s_scale;
     __shared__ int s_last;
     const int cb = sgp->chunk_begin, cn = sgp->chunk_count;
@@ -928,7 +939,8 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, int nseg, int nseg_active
       }
     }
     __syncthreads();
-    return s_scale;
+    out = s_scale;
+    return true;
   };
   const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
   if (decay)
@@ -1058,8 +1070,13 @@ int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
       attr = true;
     }
   }
-  lars_trust_kernel<<<nseg, kThreads, dyn, (cudaStream_t)stream>>>(
-      segs, nseg, partials, params, seg_scale, seg_out, grad_norm_out, counter);
+  const cudaError_t e = gs_launch_pdl(lars_trust_kernel, dim3(nseg), dim3(kThreads), dyn,
+                                      (cudaStream_t)stream, segs, nseg, partials, params, seg_scale,
+                                      seg_out, grad_norm_out, counter);
+  if (e != cudaSuccess) {
+    gs_set_error("gs_lars_trust: %s", cudaGetErrorString(e));
+    return GS_ECUDA;
+  }
   return gs_check_launch("gs_lars_trust");
 }
 
@@ -1073,16 +1090,21 @@ int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   cudaStream_t s = (cudaStream_t)stream;
   const bool pow2 = hint & GS_HINT_POW2;
   float* sc = const_cast<float*>(seg_scale);
+  cudaError_t err = cudaSuccess;
 #define GS_P2(F, P)                                                                              \
-  lars_pass2_kernel<F, P, false><<<nchunk, kThreads, 0, s>>>(segs, 0, 0, chunks, chunk0, params, \
-                                                             nullptr, sc, nullptr, nullptr,      \
-                                                             nullptr, flags, flag_mask)
+  err = gs_launch_pdl(lars_pass2_kernel<F, P, false>, dim3(nchunk), dim3(kThreads), 0, s, segs, 0, \
+                      0, chunks, chunk0, params, (const double*)nullptr, sc, (double*)nullptr,     \
+                      (double*)nullptr, (uint32_t*)nullptr, flags, flag_mask)
   if (g_is_f16) {
     if (pow2) GS_P2(true, true); else GS_P2(true, false);
   } else {
     if (pow2) GS_P2(false, true); else GS_P2(false, false);
   }
 #undef GS_P2
+  if (err != cudaSuccess) {
+    gs_set_error("gs_lars_pass2: %s", cudaGetErrorString(err));
+    return GS_ECUDA;
+  }
   return gs_check_launch("gs_lars_pass2");
 }
 

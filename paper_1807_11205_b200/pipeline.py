@@ -140,7 +140,7 @@ class GradientPipeline:
                  eta_bytes: int = 0, hier_variant: str = "hierarchical",
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
-                 bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = True,
+                 bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = False,
                  flat_variant: str = "ring"):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]

@@ -119,7 +119,7 @@ def run_vs_oracle(model, p, theta, steps=2, loss_scale=1024.0, wd=5e-4, eta_byte
     return pipe
 
 
-@pytest.mark.parametrize("kw", [{}, {"trust_in_pass2": False}, {"bulk": True},
+@pytest.mark.parametrize("kw", [{}, {"trust_in_pass2": True}, {"bulk": True},
                                 {"fuse_trust": True}, {"bulk": True, "fuse_trust": True},
                                 {"fused_pack": False}, {"use_graph": False}])
 def test_resnet50_single_gpu_matches_oracle(kw):

@@ -58,9 +58,15 @@ def main():
                         t0 = torch.cuda.Event(enable_timing=True)
                         t0.record()
                         plan.trust(sh_)
+                        _native.call("gs_fill_zero", flush.data_ptr(), flush.numel(), sh_)
+                        torch.cuda._sleep(1_000_000)
                         c2 = torch.cuda.Event(enable_timing=True)
                         c2.record()
                         plan.pass2(sh_, True, 3)
+                        e2 = torch.cuda.Event(enable_timing=True)
+                        e2.record()
+                        _native.call("gs_fill_zero", flush.data_ptr(), flush.numel(), sh_)
+                        torch.cuda._sleep(1_000_000)
                         e2 = torch.cuda.Event(enable_timing=True)
                         e2.record()
                         plan.pass2(sh_, True, 3, trust=True)

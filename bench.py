@@ -259,6 +259,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
 
+    barrier()  # ranks start the first step together
     # ---- warmup (the first two calls also capture the CUDA graph at p = 1)
     for i in range(args.warmup):
         pipe.step(grads, i)

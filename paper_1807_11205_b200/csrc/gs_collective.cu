@@ -39,6 +39,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+constexpr uint64_t kPeerTimeoutNs = 120ull * 1000000000ull;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // block-level cross-rank barrier on signal slot `phase`
 __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, int rank, int p,
                                              int phase, uint32_t epoch) {
@@ -51,9 +59,12 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
     st_release_sys(remote, epoch);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig[rank]) +
                            ((size_t)phase * gridDim.x + blockIdx.x) * p + q;
-    uint32_t spins = 0;
+    // bounded by time, not spins: ranks can legitimately be seconds apart
+    // (first-use setup on one host thread); a peer that never arrives traps
+    // after kPeerTimeoutNs instead of hanging the GPU
+    const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys(mine) != epoch) {
-      if (++spins > (1u << 24)) __trap();
+      if (globaltimer_ns() - t0 > kPeerTimeoutNs) __trap();
     }
   }
   __syncthreads();

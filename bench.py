@@ -42,8 +42,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
-    ap.add_argument("--algorithm", default="ring",
-                    choices=["ring", "hierarchical", "sharded", "ordered"])
+    ap.add_argument("--algorithm", default="ordered",
+                    choices=["ring", "hierarchical", "sharded", "ordered"],
+                    help="bucket all-reduce at N > 1: ordered = own bit-exact NVLink kernel "
+                         "(default), ring/hierarchical/sharded = NCCL")
     ap.add_argument("--group-size", type=int, default=4, help="k of Topology(p, k)")
     ap.add_argument("--eta-bytes", type=int, default=None,
                     help="hybrid threshold; default: 0 for ring, inf otherwise")

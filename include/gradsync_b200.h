@@ -186,6 +186,23 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
                              const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
                              void* stream);
 
+/* Reduce-scatter half of the above with explicit slices: rank r folds
+ * elements [bounds[r], bounds[r+1]) (device int64 array of p + 1 offsets)
+ * of every peer's buffer into its own, in the reference's tree order.  Used
+ * by the sharded (ZeRO-1) update, whose slices follow chunk boundaries. */
+int gs_ordered_reduce_scatter_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                                  const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
+                                  int nblocks, uint32_t* nonfinite, void* stream);
+
+/* All-gather of byte ranges over peer memory: rank r owns bytes
+ * [bounds[r], bounds[r+1]) of its buffer; every rank copies the other ranks'
+ * ranges from their buffers (entry and exit barriers).  Used to gather the
+ * LARS chunk partials and the binary16 working weights of the sharded
+ * update. */
+int gs_ordered_allgather(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                         const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
+                         int nblocks, void* stream);
+
 /* *counter += inc on the device (stream-ordered; graph-capturable). */
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 
@@ -219,10 +236,14 @@ int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const
  * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (nseg x 4
  * doubles) receives {||w||, ||eff||, local, sum g^2}; grad_norm_out (optional)
  * receives sqrt of the sum of per-segment g^2 in segment order
- * (experiment.py:408-411) and then needs `counter`, one zeroed uint32. */
+ * (experiment.py:408-411) and then needs `counter`, one zeroed uint32.
+ * peer_flags (npeers device pointers, sharded update): OR every rank's step
+ * flags into *flags so a non-finite value anywhere rejects the step
+ * everywhere; npeers = 0 otherwise. */
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
                   const gs_step_params* params, float* seg_scale, double* seg_out,
-                  double* grad_norm_out, uint32_t* counter, void* stream);
+                  double* grad_norm_out, uint32_t* counter, const uint64_t* peer_flags,
+                  int npeers, uint32_t* flags, void* stream);
 
 /* Pass 2: if (*flags & flag_mask) do nothing (lars.py:161-163 — the step is
  * rejected with no mutation).  Otherwise per element

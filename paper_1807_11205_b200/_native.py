@@ -76,7 +76,7 @@ SIGNATURES = {
                                     c_void_p, c_uint32, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p]),
     "gs_lars_trust": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                              c_void_p, c_void_p, c_void_p]),
+                              c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
                               c_void_p, c_void_p, c_uint32, c_void_p]),
     "gs_fill_zero": (c_int, [c_void_p, c_int64, c_void_p]),
@@ -86,6 +86,10 @@ SIGNATURES = {
     "gs_ordered_allreduce_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64, c_int64,
                                          c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
     "gs_counter_add": (c_int, [c_void_p, c_uint32, c_void_p]),
+    "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p,
+                                              c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
+    "gs_ordered_allgather": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_uint32,
+                                     c_void_p, c_int, c_void_p]),
 }
 
 ABI_VERSION = 1

@@ -141,7 +141,8 @@ class LarsPlan:
     fixed set of segments."""
 
     def __init__(self, specs: list[SegmentSpec], device: torch.device, order=None,
-                 chunk_elems: int = CHUNK_ELEMS):
+                 chunk_elems: int = CHUNK_ELEMS, partials: torch.Tensor | None = None,
+                 flagbuf: torch.Tensor | None = None):
         self.device = device
         self.nseg = len(specs)
         chunks, begin, count = build_chunks([s.n for s in specs], order, chunk_elems)
@@ -159,14 +160,16 @@ class LarsPlan:
         self.base_segs = self.d_segs
         self._alt: dict = {}
         self.d_chunks = dev.upload(chunks, device)
-        self.partials = torch.zeros(max(1, 3 * self.nchunk), dtype=torch.float64, device=device)
+        self.partials = partials if partials is not None else \
+            torch.zeros(max(1, 3 * self.nchunk), dtype=torch.float64, device=device)
         self.seg_scale = torch.zeros(max(1, self.nseg), dtype=torch.float32, device=device)
         self.seg_out = torch.zeros(max(1, 4 * self.nseg), dtype=torch.float64, device=device)
         self.grad_norm = torch.zeros(1, dtype=torch.float64, device=device)
         # one int32 block, reset by one kernel per step: [0] = non-finite
         # flags, [4 : 4 + nseg + 1] = per-segment / global arrival counters
         # of the fused pass1 + trust kernel
-        self.flagbuf = torch.zeros(4 + self.nseg + 1, dtype=torch.int32, device=device)
+        self.flagbuf = flagbuf if flagbuf is not None else \
+            torch.zeros(4 + self.nseg + 1, dtype=torch.int32, device=device)
         self.flags = self.flagbuf[0:1]
         self.counters = self.flagbuf[4:]
         self.nseg_active = int((count > 0).sum())
@@ -250,10 +253,12 @@ class LarsPlan:
                          1 if g_is_f16 else 0, dev.ptr(self.params), self.hint,
                          dev.ptr(self.partials), dev.ptr(self.flags), stream_h)
 
-    def trust(self, stream_h: int):
+    def trust(self, stream_h: int, peer_flags: torch.Tensor | None = None, npeers: int = 0):
         _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
                      dev.ptr(self.params), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
-                     dev.ptr(self.grad_norm), dev.ptr(self.counters[self.nseg:]), stream_h)
+                     dev.ptr(self.grad_norm), dev.ptr(self.counters[self.nseg:]),
+                     dev.ptr(peer_flags) if peer_flags is not None else None, npeers,
+                     dev.ptr(self.flags), stream_h)
 
     def pass2(self, stream_h: int, g_is_f16: bool, flag_mask: int, chunk0: int = 0,
               nchunk: int | None = None, trust: bool = False):

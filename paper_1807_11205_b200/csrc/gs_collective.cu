@@ -62,8 +62,11 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
     // bounded by time, not spins: ranks can legitimately be seconds apart
     // (first-use setup on one host thread); a peer that never arrives traps
     // after kPeerTimeoutNs instead of hanging the GPU
+    // epochs only grow: a peer that already moved on to a later call has
+    // passed this barrier too (it only starts a call after finishing the
+    // previous one on its stream), so "at least epoch" is the condition
     const uint64_t t0 = globaltimer_ns();
-    while (ld_acquire_sys(mine) != epoch) {
+    while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
       if (globaltimer_ns() - t0 > kPeerTimeoutNs) __trap();
     }
   }
@@ -94,23 +97,10 @@ __device__ __forceinline__ void subrange(int64_t n, int p, int r, int nb, int b,
   hi = min(s1, lo + sub);
 }
 
+// fold [lo, hi) of every peer's buffer into mine (pairwise tree, P <= 8)
 template <int P>
-__global__ void __launch_bounds__(kThreads)
-ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
-                         int rank, int64_t offset, int64_t n, uint32_t epoch,
-                         const uint32_t* __restrict__ epoch_base, uint32_t* __restrict__ nonfinite) {
-  if (epoch_base != nullptr) epoch += *epoch_base;  // device-resident epochs: graph-replayable
-  const uint16_t* src[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
-  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
-
-  peer_barrier(sig, rank, P, 0, epoch);  // A: every bucket packed
-
-  // B: fold my slice, sub-range blockIdx.x
-  int64_t lo, hi;
-  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
-  uint32_t bad = 0;
+__device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint16_t* mine, int64_t lo,
+                                           int64_t hi, uint32_t& bad) {
   bool vec = gs::is_aligned16(mine + lo);
 #pragma unroll
   for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q] + lo);
@@ -156,6 +146,52 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
     bad |= (o & 0x7C00u) == 0x7C00u;
     mine[i] = o;
   }
+}
+
+// copy bytes [lo, hi) of a peer buffer into mine
+__device__ __forceinline__ void copy_range(const uint8_t* src, uint8_t* mine, int64_t lo, int64_t hi) {
+  const bool v2 = ((reinterpret_cast<uintptr_t>(src + lo) | reinterpret_cast<uintptr_t>(mine + lo)) & 15) == 0;
+  const int64_t m = v2 ? (hi - lo) / 16 : 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + lo);
+  uint4* d4 = reinterpret_cast<uint4*>(mine + lo);
+  for (int64_t base = threadIdx.x; base < m; base += 8 * kThreads) {
+    uint4 t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + u * kThreads < m) t[u] = __ldcv(s4 + base + u * kThreads);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (base + u * kThreads < m) d4[base + u * kThreads] = t[u];
+  }
+  for (int64_t i = lo + m * 16 + threadIdx.x; i < hi; i += kThreads) mine[i] = __ldcv(src + i);
+}
+
+// [lo, hi) of sub-range `b` of [s0, s1) split into nb pieces of whole 16 B
+__device__ __forceinline__ void split_range(int64_t s0, int64_t s1, int nb, int b, int64_t grain,
+                                            int64_t& lo, int64_t& hi) {
+  const int64_t sub = ((s1 - s0 + nb - 1) / nb + grain - 1) / grain * grain;
+  lo = min(s1, s0 + (int64_t)b * sub);
+  hi = min(s1, lo + sub);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                         int rank, int64_t offset, int64_t n, uint32_t epoch,
+                         const uint32_t* __restrict__ epoch_base, uint32_t* __restrict__ nonfinite) {
+  if (epoch_base != nullptr) epoch += *epoch_base;  // device-resident epochs: graph-replayable
+  const uint16_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+
+  peer_barrier(sig, rank, P, 0, epoch);  // A: every bucket packed
+
+  // B: fold my slice, sub-range blockIdx.x
+  int64_t lo, hi;
+  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
+  uint32_t bad = 0;
+  fold_range<P>(src, mine, lo, hi, bad);
   bad = __reduce_or_sync(0xFFFFFFFFu, bad);
   if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 
@@ -166,21 +202,53 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
   for (int d = 1; d < P; ++d) {
     const int r = (rank + d) % P;
     subrange(n, P, r, gridDim.x, blockIdx.x, lo, hi);
-    const bool v2 = gs::is_aligned16(mine + lo) && gs::is_aligned16(src[r] + lo);
-    const int64_t m = v2 ? (hi - lo) / 8 : 0;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src[r] + lo);
-    uint4* d4 = reinterpret_cast<uint4*>(mine + lo);
-    for (int64_t base = threadIdx.x; base < m; base += 8 * kThreads) {
-      uint4 t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (base + u * kThreads < m) t[u] = __ldcv(s4 + base + u * kThreads);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (base + u * kThreads < m) d4[base + u * kThreads] = t[u];
-    }
-    for (int64_t i = lo + m * 8 + threadIdx.x; i < hi; i += kThreads) mine[i] = __ldcv(src[r] + i);
+    copy_range(reinterpret_cast<const uint8_t*>(src[r]), reinterpret_cast<uint8_t*>(mine), 2 * lo, 2 * hi);
   }
+}
+
+// Reduce-scatter with explicit slice bounds (elements, p + 1 entries):
+// rank r folds [bounds[r], bounds[r+1]) of every peer's buffer into its own.
+// One barrier: the raw values it reads are never written by their owners in
+// this call, and the caller double-buffers the wire across steps.
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+ordered_reduce_scatter_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                              int rank, const int64_t* __restrict__ bounds, uint32_t epoch,
+                              const uint32_t* __restrict__ epoch_base,
+                              uint32_t* __restrict__ nonfinite) {
+  if (epoch_base != nullptr) epoch += *epoch_base;
+  const uint16_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]);
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]);
+  peer_barrier(sig, rank, P, 0, epoch);  // every rank's bucket is packed
+  int64_t lo, hi;
+  split_range(bounds[rank], bounds[rank + 1], gridDim.x, blockIdx.x, 8, lo, hi);
+  uint32_t bad = 0;
+  fold_range<P>(src, mine, lo, hi, bad);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+}
+
+// All-gather of byte ranges: rank r owns [bounds[r], bounds[r+1]) of the
+// buffer; every rank copies the others' ranges out of their buffers.  Entry
+// barrier (the owners' ranges are final) and exit barrier (nobody reads a
+// range its owner may overwrite next).
+__global__ void __launch_bounds__(kThreads)
+ordered_allgather_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                         int rank, int p, const int64_t* __restrict__ bounds, uint32_t epoch,
+                         const uint32_t* __restrict__ epoch_base) {
+  if (epoch_base != nullptr) epoch += *epoch_base;
+  uint8_t* mine = reinterpret_cast<uint8_t*>(bufs[rank]);
+  peer_barrier(sig, rank, p, 0, epoch);
+#pragma unroll 1
+  for (int d = 1; d < p; ++d) {
+    const int r = (rank + d) % p;
+    int64_t lo, hi;
+    split_range(bounds[r], bounds[r + 1], gridDim.x, blockIdx.x, 16, lo, hi);
+    copy_range(reinterpret_cast<const uint8_t*>(bufs[r]), mine, lo, hi);
+  }
+  peer_barrier(sig, rank, p, 1, epoch);
 }
 
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
@@ -227,6 +295,59 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
   }
 #undef GS_OAR
   return gs_check_launch("gs_ordered_allreduce_f16");
+}
+
+static int coresident_blocks(const void* kernel, int want) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  return per_sm > 0 ? min(want, per_sm * sms) : 1;
+}
+
+int gs_ordered_reduce_scatter_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                                  const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
+                                  int nblocks, uint32_t* nonfinite, void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_reduce_scatter_f16: 1 <= p <= 8 (got %d)", p);
+  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_reduce_scatter_f16: bad rank %d", rank);
+  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_reduce_scatter_f16: bad block count");
+  GS_REQUIRE(epoch != 0 || epoch_base != nullptr, "gs_ordered_reduce_scatter_f16: epoch 0");
+  if (p == 1) return GS_OK;
+  GS_REQUIRE(bufs && sig && bounds, "gs_ordered_reduce_scatter_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_ORS(P)                                                                                 \
+  case P: {                                                                                       \
+    const int nb = coresident_blocks((const void*)ordered_reduce_scatter_kernel<P>, nblocks);     \
+    ordered_reduce_scatter_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, bounds, epoch,      \
+                                                             epoch_base, nonfinite);              \
+    break;                                                                                        \
+  }
+  switch (p) {
+    GS_ORS(2)
+    GS_ORS(3)
+    GS_ORS(4)
+    GS_ORS(5)
+    GS_ORS(6)
+    GS_ORS(7)
+    GS_ORS(8)
+  }
+#undef GS_ORS
+  return gs_check_launch("gs_ordered_reduce_scatter_f16");
+}
+
+int gs_ordered_allgather(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                         const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
+                         int nblocks, void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allgather: 1 <= p <= 8 (got %d)", p);
+  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allgather: bad rank %d", rank);
+  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allgather: bad block count");
+  GS_REQUIRE(epoch != 0 || epoch_base != nullptr, "gs_ordered_allgather: epoch 0");
+  if (p == 1) return GS_OK;
+  GS_REQUIRE(bufs && sig && bounds, "gs_ordered_allgather: null pointer");
+  const int nb = coresident_blocks((const void*)ordered_allgather_kernel, nblocks);
+  ordered_allgather_kernel<<<nb, kThreads, 0, (cudaStream_t)stream>>>(bufs, sig, rank, p, bounds,
+                                                                      epoch, epoch_base);
+  return gs_check_launch("gs_ordered_allgather");
 }
 
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream) {

@@ -732,9 +732,16 @@ __global__ void __launch_bounds__(kThreads)
 lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, const double* __restrict__ partials,
                   const gs_step_params* __restrict__ params, float* __restrict__ seg_scale,
                   double* __restrict__ seg_out, double* __restrict__ grad_norm_out,
-                  uint32_t* __restrict__ counter) {
+                  uint32_t* __restrict__ counter, const uint64_t* __restrict__ peer_flags,
+                  int npeers, uint32_t* __restrict__ flags) {
   gs::griddep_wait();                 // pass 1's partials are complete
   gs::griddep_launch_dependents();    // let pass 2 start issuing its loads now
+  if (npeers > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    // sharded update: the step is rejected if any rank saw a non-finite value
+    uint32_t f = 0;
+    for (int q = 0; q < npeers; ++q) f |= *reinterpret_cast<const volatile uint32_t*>(peer_flags[q]);
+    if (f) atomicOr(flags, f);
+  }
   const int s = blockIdx.x;
   const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
   double x = 0.0, y = 0.0, z = 0.0;
@@ -1054,13 +1061,16 @@ int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const
 
 int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
                   const gs_step_params* params, float* seg_scale, double* seg_out,
-                  double* grad_norm_out, uint32_t* counter, void* stream) {
+                  double* grad_norm_out, uint32_t* counter, const uint64_t* peer_flags,
+                  int npeers, uint32_t* flags, void* stream) {
   GS_REQUIRE(nseg >= 0, "gs_lars_trust: negative segment count");
   if (nseg == 0) return GS_OK;
   GS_REQUIRE(segs && partials && params && seg_scale && seg_out, "gs_lars_trust: null pointer");
   GS_REQUIRE(grad_norm_out == nullptr || counter != nullptr,
              "gs_lars_trust: the grad norm needs a zeroed arrival counter");
   GS_REQUIRE(nseg <= 24 * 1024, "gs_lars_trust: at most 24576 segments");
+  GS_REQUIRE(npeers == 0 || (peer_flags != nullptr && flags != nullptr),
+             "gs_lars_trust: peer flags need both tables");
   const size_t dyn = grad_norm_out != nullptr ? sizeof(double) * (size_t)nseg : 0;
   if (dyn > 48 * 1024) {
     static bool attr = false;
@@ -1072,7 +1082,7 @@ int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
   }
   const cudaError_t e = gs_launch_pdl(lars_trust_kernel, dim3(nseg), dim3(kThreads), dyn,
                                       (cudaStream_t)stream, segs, nseg, partials, params, seg_scale,
-                                      seg_out, grad_norm_out, counter);
+                                      seg_out, grad_norm_out, counter, peer_flags, npeers, flags);
   if (e != cudaSuccess) {
     gs_set_error("gs_lars_trust: %s", cudaGetErrorString(e));
     return GS_ECUDA;

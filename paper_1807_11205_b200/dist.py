@@ -215,3 +215,45 @@ class OrderedWire:
         from . import _native
 
         _native.call("gs_counter_add", dev.ptr(self.epoch_base), per_step, stream_h)
+
+
+class SymmetricArena:
+    """One symmetric-memory allocation per rank carved into named regions
+    (byte sizes given up front), plus device tables of every peer's address
+    of each region — the building block of the sharded (ZeRO-1) update, in
+    which the wire, the binary16 working weights, the masters, the
+    velocities, the LARS chunk partials and the step flags are all reachable
+    by every peer over NVLink."""
+
+    ALIGN = 512
+
+    def __init__(self, comm: "Communicator", regions: dict, device, sig_words: int):
+        import numpy as np
+        import torch.distributed._symmetric_memory as symm
+
+        from . import _device as dev
+
+        self.p, self.rank = comm.topo.p, comm.rank
+        self.offsets, off = {}, 0
+        for name, nbytes in list(regions.items()) + [("sig", 4 * sig_words)]:
+            self.offsets[name] = off
+            off += (int(nbytes) + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        self.sizes = dict(regions, sig=4 * sig_words)
+        self.buf = symm.empty(off, dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        torch.cuda.synchronize(device)
+        self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
+        self.bases = [int(x) for x in self.hdl.buffer_ptrs]
+        self._tabs = {}
+        for name in self.offsets:
+            self._tabs[name] = dev.upload(
+                np.array([b + self.offsets[name] for b in self.bases], dtype=np.uint64), device)
+        dist.barrier()
+
+    def view(self, name: str, dtype: torch.dtype) -> torch.Tensor:
+        o, n = self.offsets[name], self.sizes[name]
+        return self.buf[o:o + n].view(dtype)
+
+    def peers(self, name: str) -> torch.Tensor:
+        """Device uint64[p]: every rank's address of region `name`."""
+        return self._tabs[name]

@@ -141,7 +141,7 @@ class GradientPipeline:
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
                  bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = False,
-                 flat_variant: str = "ring"):
+                 flat_variant: str = "ring", sharded_update: bool = False):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -167,15 +167,23 @@ class GradientPipeline:
                                                               threshold_bytes)
 
         d = self.device
+        self.sharded = bool(sharded_update)
+        if self.sharded and (comm is None or comm.topo.p < 2):
+            raise ValueError("sharded_update needs a Communicator with p >= 2")
         for b in self.buckets:
-            if comm is not None:
+            if self.sharded:
+                b.algorithm = "sharded-update"
+            elif comm is not None:
                 b.algorithm = comm.pick(b.nbytes, self.eta_bytes, hier_variant, flat_variant)
             else:
                 b.algorithm = "ordered" if self.local else "none"
         # the ordered (bit-exact) collective reads peers' wires over NVLink:
         # the wire then lives in a double-buffered symmetric-memory window
         self.ordered = None
-        if comm is not None and any(b.algorithm == "ordered" for b in self.buckets):
+        self.arena = None
+        if self.sharded:
+            self._init_sharded_arena(comm, d)
+        elif comm is not None and any(b.algorithm == "ordered" for b in self.buckets):
             from .dist import OrderedWire
             self.ordered = OrderedWire(comm, self.total, d)
             self.wire = self.ordered.halves[0]
@@ -183,9 +191,10 @@ class GradientPipeline:
             self.wire = torch.zeros(self.total, dtype=torch.uint16, device=d)
         self._last_wire = self.wire
         self._half = 0
-        self.master = torch.zeros(self.total, dtype=torch.float32, device=d)
-        self.velocity = torch.zeros(self.total, dtype=torch.float32, device=d)
-        self.working = torch.zeros(self.total, dtype=torch.uint16, device=d)
+        if not self.sharded:
+            self.master = torch.zeros(self.total, dtype=torch.float32, device=d)
+            self.velocity = torch.zeros(self.total, dtype=torch.float32, device=d)
+            self.working = torch.zeros(self.total, dtype=torch.uint16, device=d)
         self.grad32 = torch.zeros(self.total, dtype=torch.float32, device=d)
         if init_master is not None:
             self.load_master(init_master)
@@ -200,7 +209,12 @@ class GradientPipeline:
         segs = [SegmentSpec(wb + 2 * self.wire_off[i], mb + 4 * self.wire_off[i],
                             vb + 4 * self.wire_off[i], hb + 2 * self.wire_off[i], sizes[i],
                             segment_flags(self.groups[i])) for i in range(n)]
-        self.plan = LarsPlan(segs, d, order=self.order)
+        if self.sharded:
+            self.plan = LarsPlan(segs, d, order=self.order,
+                                 partials=self.arena.view("partials", torch.float64),
+                                 flagbuf=self.arena.view("flags", torch.int32))
+        else:
+            self.plan = LarsPlan(segs, d, order=self.order)
         if bulk:
             self.plan.extra_hint &= ~_native.HINT_NO_BULK
         self.plan.fuse_trust = fuse_trust
@@ -233,6 +247,125 @@ class GradientPipeline:
                                               dtype=np.uint64), d)
         self._result_host = torch.zeros(2, dtype=torch.float64).pin_memory()
         self._flags_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+
+    # ------------------------------------------------------------ sharded
+    def _init_sharded_arena(self, comm, d) -> None:
+        """ZeRO-1 layout: one symmetric window holding both wire halves, the
+        binary16 working weights, the masters, the velocities, the chunk
+        partials and the step flags, so every peer can reach them."""
+        from ._plan import build_chunks
+        from .dist import SymmetricArena
+
+        p = comm.topo.p
+        chunks, _, _ = build_chunks(self.sizes, self.order)
+        self._host_chunks = chunks
+        nchunk = len(chunks)
+        sms = torch.cuda.get_device_properties(d).multi_processor_count
+        self._nblocks = 2 * sms
+        regions = {
+            "wireA": 2 * self.total, "wireB": 2 * self.total, "working": 2 * self.total,
+            "master": 4 * self.total, "velocity": 4 * self.total,
+            "partials": 8 * max(1, 3 * nchunk), "flags": 4 * (4 + len(self.specs) + 1),
+        }
+        self.arena = SymmetricArena(comm, regions, d, sig_words=2 * self._nblocks * p)
+        a = self.arena
+        self.wire = a.view("wireA", torch.uint16)
+        self._halves = (a.view("wireA", torch.uint16), a.view("wireB", torch.uint16))
+        self.master = a.view("master", torch.float32)
+        self.velocity = a.view("velocity", torch.float32)
+        self.working = a.view("working", torch.uint16)
+        # ownership: rank r owns chunks [C_r, C_r+1) (balanced by elements, in
+        # wire order) = wire/arena elements [E_r, E_r+1)
+        abs_start = np.array([self.wire_off[int(c["seg"])] + int(c["start"]) for c in chunks],
+                             dtype=np.int64)
+        C = [0] + [int(np.searchsorted(abs_start, r * self.total // p)) for r in range(1, p)] \
+            + [nchunk]
+        E = [0] + [int(abs_start[c]) if c < nchunk else self.total for c in C[1:p]] + [self.total]
+        self._own_chunks, self._own_elems = C, E
+        r = comm.rank
+        self.owned = (E[r], E[r + 1])
+        self._rs_bounds = []
+        self._own_bucket_chunks = []
+        for bk in self.buckets:
+            bs, be = bk.start, bk.start + bk.padded
+            bounds = np.clip(np.array(E, dtype=np.int64), bs, be)
+            bounds[0], bounds[-1] = bs, be
+            self._rs_bounds.append(dev.upload(bounds, d))
+        self._part_bounds = dev.upload(np.array([24 * c for c in C], dtype=np.int64), d)
+        self._w16_bounds = dev.upload(np.array([2 * e for e in E], dtype=np.int64), d)
+        self._m_bounds = dev.upload(np.array([4 * e for e in E], dtype=np.int64), d)
+        self.epoch_base = torch.zeros(1, dtype=torch.int32, device=d)
+        self._ps_events = None
+
+    def gather_state(self) -> None:
+        """Make the sharded masters and velocities whole on every rank (for
+        inspection / checkpoints; the step itself only keeps the working
+        copy replicated, ZeRO-1)."""
+        if not self.sharded:
+            return
+        sh = int(torch.cuda.current_stream(self.device).cuda_stream)
+        p, r = self.comm.topo.p, self.comm.rank
+        for name in ("master", "velocity"):
+            _native.call("gs_ordered_allgather", dev.ptr(self.arena.peers(name)),
+                         dev.ptr(self.arena.peers("sig")), r, p, dev.ptr(self._m_bounds), 1,
+                         dev.ptr(self.epoch_base), self._nblocks, sh)
+            _native.call("gs_counter_add", dev.ptr(self.epoch_base), 1, sh)
+
+    def _launch_sharded(self, tabs, s0, timer) -> None:
+        """reduce-scatter (own slice, reference tree order) -> pass 1 on own
+        chunks -> all-gather of the chunk partials -> trust (flags OR-ed over
+        ranks) -> pass 2 on own chunks -> all-gather of the working weights."""
+        plan, a = self.plan, self.arena
+        sh = int(s0.cuda_stream)
+        p, r = self.comm.topo.p, self.comm.rank
+        half = self._half
+        wire = self._halves[half]
+        ptabs = tabs[half]
+        wb = wire.data_ptr()
+        plan.use_segments(plan.alt_segments([wb + 2 * o for o in self.wire_off]))
+        plan.reset_flags(sh)
+        C = self._own_chunks
+        sig, ebase = dev.ptr(a.peers("sig")), dev.ptr(self.epoch_base)
+        wires = a.peers("wireA" if half == 0 else "wireB")
+        ps = self._pack_stream
+        ps.wait_stream(s0)
+        evs = []
+        for b in range(len(self.buckets)):
+            with torch.cuda.stream(ps):
+                self._pack(ptabs, b, int(ps.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(ps)
+                evs.append(ev)
+        if timer:
+            timer("pass1")
+        nb = len(self.buckets)
+        for b, bk in enumerate(self.buckets):
+            s0.wait_event(evs[b])
+            _native.call("gs_ordered_reduce_scatter_f16", dev.ptr(wires), sig, r, p,
+                         dev.ptr(self._rs_bounds[b]), b + 1, ebase, self._nblocks, None, sh)
+            c0 = max(bk.chunk0, C[r])
+            c1 = min(bk.chunk0 + bk.nchunk, C[r + 1])
+            if c1 > c0:
+                plan.pass1(sh, g_is_f16=True, chunk0=c0, nchunk=c1 - c0)
+        s0.wait_stream(ps)
+        _native.call("gs_ordered_allgather", dev.ptr(a.peers("partials")), sig, r, p,
+                     dev.ptr(self._part_bounds), nb + 1, ebase, self._nblocks, sh)
+        if timer:
+            timer("trust")
+        plan.trust(sh, peer_flags=a.peers("flags"), npeers=p)
+        if timer:
+            timer("pass2")
+        mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
+        if C[r + 1] > C[r]:
+            plan.pass2(sh, g_is_f16=True, flag_mask=mask, chunk0=C[r], nchunk=C[r + 1] - C[r])
+        _native.call("gs_ordered_allgather", dev.ptr(a.peers("working")), sig, r, p,
+                     dev.ptr(self._w16_bounds), nb + 2, ebase, self._nblocks, sh)
+        _native.call("gs_counter_add", ebase, nb + 3, sh)
+        plan.use_segments(None)
+        self._last_wire = wire
+        self._half ^= 1
+        if timer:
+            timer("end")
 
     # ------------------------------------------------------------ layout
     def _group_view(self, i: int) -> ParamGroup:
@@ -365,6 +498,9 @@ class GradientPipeline:
         if self.ordered is not None:
             tabs = tuple(self._tables_for(views, h) for h in self.ordered.halves)
             return tabs, tuple(id(t) for t in tabs)
+        if self.sharded:
+            tabs = tuple(self._tables_for(views, h) for h in self._halves)
+            return tabs, tuple(id(t) for t in tabs)
         tabs = self._tables_for(views, self.wire)
         return tabs, id(tabs)
 
@@ -393,7 +529,8 @@ class GradientPipeline:
         # graph replay needs every kernel of the step to be ours: comm = None,
         # or only ordered (symmetric-memory) buckets, whose epochs live on
         # the device (NCCL buckets run eagerly)
-        graphable = self.comm is None or all(b.algorithm == "ordered" for b in self.buckets)
+        graphable = self.comm is None or self.sharded or \
+            all(b.algorithm == "ordered" for b in self.buckets)
         if timer is not None or not self.use_graph or not graphable:
             self._launch(tabs, s0, timer)
             return
@@ -420,8 +557,14 @@ class GradientPipeline:
         if self.ordered is not None:
             self._last_wire = self.ordered.halves[self._half]
             self._half ^= 1
+        elif self.sharded:
+            self._last_wire = self._halves[self._half]
+            self._half ^= 1
 
     def _launch(self, tabs, s0, timer) -> None:
+        if self.sharded:
+            self._launch_sharded(tabs, s0, timer)
+            return
         plan = self.plan
         sh = int(s0.cuda_stream)
         fused = isinstance(tabs, tuple) and tabs[0] == "fused"

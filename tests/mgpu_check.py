@@ -49,8 +49,9 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    algos = os.environ.get("MGPU_ALGOS", "ordered,ring,hierarchical,sharded").split(",")
-    for algo, k in (("ordered", 1), ("ring", 1), ("hierarchical", 2), ("sharded", 2)):
+    algos = os.environ.get("MGPU_ALGOS", "zero,ordered,ring,hierarchical,sharded").split(",")
+    for algo, k in (("zero", 1), ("ordered", 1), ("ring", 1), ("hierarchical", 2),
+                    ("sharded", 2)):
         if algo not in algos:
             continue
         if world % k or (algo != "ring" and world == 1):
@@ -61,6 +62,7 @@ def main():
                                    eta_bytes=0 if algo in ("ring", "ordered") else 1 << 62,
                                    hier_variant=algo if algo not in ("ring", "ordered") else "hierarchical",
                                    flat_variant="ordered" if algo == "ordered" else "ring",
+                                   sharded_update=algo == "zero",
                                    init_master=master, loss_scale=gs.LossScale(1024.0), device=dev)
         groups = [rp.Group(s.name, s.kind, w.copy(), np.zeros(s.numel, np.float32),
                            np.zeros(s.numel, np.float32), rp.narrow(w))
@@ -75,14 +77,17 @@ def main():
                 wires[world - 1][4321] = 0x7C00
             res = pipe.step(torch.from_numpy(wires[rank]).to(dev), step)
             reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]
+            if algo == "zero":
+                pipe.gather_state()  # masters/velocities are sharded (ZeRO-1)
+                torch.cuda.synchronize(dev)
             if rank == 0:
                 parts = [split(w, specs) for w in wires]
-                exact = world == 2 or algo == "ordered"
+                exact = world == 2 or algo in ("ordered", "zero")
                 out = rp.compose_step_fp16(parts, [s.name for s in specs], [s.numel for s in specs],
                                            order, groups, rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1,
                                            oloss, theta, 0,
                                            reduced_override=None if exact else reduced)
-                if not exact:
+                if not exact and algo != "zero":
                     # reduced buckets within the reference's fp16 bound
                     tree = rp.compose_step_fp16  # noqa: F841 (documentation)
                     for b, bk in enumerate(pipe.buckets):
@@ -108,6 +113,11 @@ def main():
                 if not np.array_equal(gotv.view(np.uint32), wantv.view(np.uint32)):
                     ok = False
                     notes.append(f"step {step}: velocity differs")
+                goth = pipe.registration_view(pipe.working).cpu().numpy()
+                wanth = np.concatenate([g.working for g in groups])
+                if not np.array_equal(goth, wanth):
+                    ok = False
+                    notes.append(f"step {step}: working copy differs")
                 if out.applied and not np.array_equal(pipe.seg_scales(), out.scales):
                     ok = False
                     notes.append(f"step {step}: trust scales differ")

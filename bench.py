@@ -43,9 +43,10 @@ def parse():
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
     ap.add_argument("--algorithm", default="ordered",
-                    choices=["ring", "hierarchical", "sharded", "ordered"],
-                    help="bucket all-reduce at N > 1: ordered = own bit-exact NVLink kernel "
-                         "(default), ring/hierarchical/sharded = NCCL")
+                    choices=["ring", "hierarchical", "sharded", "ordered", "zero"],
+                    help="gradient exchange at N > 1: ordered = own bit-exact NVLink all-reduce "
+                         "(default), zero = own reduce-scatter + sharded LARS update + all-gather "
+                         "of the working weights, ring/hierarchical/sharded = NCCL all-reduce")
     ap.add_argument("--group-size", type=int, default=4, help="k of Topology(p, k)")
     ap.add_argument("--eta-bytes", type=int, default=None,
                     help="hybrid threshold; default: 0 for ring, inf otherwise")
@@ -201,7 +202,7 @@ def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, wa
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    flat = args.algorithm in ("ring", "ordered")
+    flat = args.algorithm in ("ring", "ordered", "zero")
     eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     r = cpu_reference(args.model, world, args.theta, eta, args.steps, args.warmup)
     line = {
@@ -239,13 +240,14 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if world > 1:
         k = args.group_size if args.algorithm in ("hierarchical", "sharded") else 1
         comm = Communicator(gs.Topology(world, k if world % k == 0 else 1))
-    flat = args.algorithm in ("ring", "ordered")
+    flat = args.algorithm in ("ring", "ordered", "zero")
     eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0, weight_decay=5e-4,
                         momentum=0.9)
     pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=args.theta, comm=comm, eta_bytes=eta,
                                hier_variant=args.algorithm if not flat else "hierarchical",
                                flat_variant="ordered" if args.algorithm == "ordered" else "ring",
+                               sharded_update=args.algorithm == "zero" and world > 1,
                                init_master=sh.synth_master(specs, seed=0),
                                loss_scale=gs.LossScale(1024.0), device=dev)
     grads_host = torch.from_numpy(sh.synth_wire_grads(specs, rank=rank, seed=0)).pin_memory()
@@ -374,8 +376,11 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "wire_dtype": "f16", "data": "synthetic",
-        "config": {"workload": f"{args.model} fused MP-LARS step (pack -> "
-                               f"{'allreduce -> ' if world > 1 else ''}pass1 -> trust -> pass2)",
+        "config": {"workload": f"{args.model} fused MP-LARS step (" + (
+                       "pack -> pass1 -> trust -> pass2" if world == 1 else
+                       "pack -> reduce-scatter -> pass1(shard) -> gather partials -> trust -> "
+                       "pass2(shard) -> all-gather w16" if args.algorithm == "zero" else
+                       "pack -> allreduce -> pass1 -> trust -> pass2") + ")",
                    "model": args.model, "params": n_params, "tensors": len(specs),
                    "theta": args.theta, "buckets": len(pipe.buckets),
                    "algorithm": args.algorithm if world > 1 else "none",

@@ -301,7 +301,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # device-side sleep, so every kernel runs back to back and the events
     # between launches time kernels, not host launch gaps
     phase_ms = {}
-    wanted = ("pack", "fold", "pass1", "trust", "pass2") if world == 1 else ("trust", "pass2")
+    wanted = None  # every phase the step reports
     for i in range(max(3, min(args.steps, 10))):
         flush_l2()
         torch.cuda._sleep(4_000_000)
@@ -311,12 +311,12 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             e = torch.cuda.Event(enable_timing=True)
             e.record(s0)
             ev[name] = e
+        mark("begin")
         pipe.enqueue(grads, args.warmup + i, timer=mark)
         pipe.finish()
-        names = [n for n in ("pack", "fold", "pass1", "trust", "pass2", "end") if n in ev]
+        names = list(ev)  # insertion order = launch order
         for x, y in zip(names, names[1:]):
-            if x in wanted:
-                phase_ms.setdefault(x, []).append(ev[x].elapsed_time(ev[y]))
+            phase_ms.setdefault(x, []).append(ev[x].elapsed_time(ev[y]))
 
     mean_ms = statistics.mean(step_ms)
     t = torch.tensor([mean_ms, statistics.median(phase_ms["pass2"])], dtype=torch.float64,

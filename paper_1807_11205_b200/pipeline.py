@@ -336,18 +336,22 @@ class GradientPipeline:
                 ev = torch.cuda.Event()
                 ev.record(ps)
                 evs.append(ev)
-        if timer:
-            timer("pass1")
         nb = len(self.buckets)
         for b, bk in enumerate(self.buckets):
             s0.wait_event(evs[b])
+            if timer:
+                timer(f"rs{b}")
             _native.call("gs_ordered_reduce_scatter_f16", dev.ptr(wires), sig, r, p,
                          dev.ptr(self._rs_bounds[b]), b + 1, ebase, self._nblocks, None, sh)
             c0 = max(bk.chunk0, C[r])
             c1 = min(bk.chunk0 + bk.nchunk, C[r + 1])
+            if timer:
+                timer(f"pass1_{b}")
             if c1 > c0:
                 plan.pass1(sh, g_is_f16=True, chunk0=c0, nchunk=c1 - c0)
         s0.wait_stream(ps)
+        if timer:
+            timer("gather_partials")
         _native.call("gs_ordered_allgather", dev.ptr(a.peers("partials")), sig, r, p,
                      dev.ptr(self._part_bounds), nb + 1, ebase, self._nblocks, sh)
         if timer:
@@ -358,6 +362,8 @@ class GradientPipeline:
         mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
         if C[r + 1] > C[r]:
             plan.pass2(sh, g_is_f16=True, flag_mask=mask, chunk0=C[r], nchunk=C[r + 1] - C[r])
+        if timer:
+            timer("gather_w16")
         _native.call("gs_ordered_allgather", dev.ptr(a.peers("working")), sig, r, p,
                      dev.ptr(self._w16_bounds), nb + 2, ebase, self._nblocks, sh)
         _native.call("gs_counter_add", ebase, nb + 3, sh)

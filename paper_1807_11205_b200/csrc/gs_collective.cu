@@ -38,6 +38,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 constexpr uint64_t kPeerTimeoutNs = 120ull * 1000000000ull;
 
@@ -55,7 +60,8 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
     const int q = threadIdx.x;
     uint32_t* remote = reinterpret_cast<uint32_t*>(sig[q]) +
                        ((size_t)phase * gridDim.x + blockIdx.x) * p + rank;
-    __threadfence_system();
+    // the release store is cumulative over the block's writes ordered before
+    // it by the bar.sync above, so no separate system-scope fence is needed
     st_release_sys(remote, epoch);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig[rank]) +
                            ((size_t)phase * gridDim.x + blockIdx.x) * p + q;
@@ -65,9 +71,13 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
     // epochs only grow: a peer that already moved on to a later call has
     // passed this barrier too (it only starts a call after finishing the
     // previous one on its stream), so "at least epoch" is the condition
-    const uint64_t t0 = globaltimer_ns();
-    while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
-      if (globaltimer_ns() - t0 > kPeerTimeoutNs) __trap();
+    if ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+      // poll with relaxed loads, then one acquire load once the value is in
+      const uint64_t t0 = globaltimer_ns();
+      while ((int32_t)(ld_relaxed_sys(mine) - epoch) < 0) {
+        if (globaltimer_ns() - t0 > kPeerTimeoutNs) __trap();
+      }
+      (void)ld_acquire_sys(mine);
     }
   }
   __syncthreads();

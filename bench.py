@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
     ap.add_argument("--algorithm", default="ordered",
-                    choices=["ring", "hierarchical", "sharded", "ordered", "zero"],
+                    choices=["ring", "hierarchical", "sharded", "ordered", "zero", "zero_unfused"],
                     help="gradient exchange at N > 1: ordered = own bit-exact NVLink all-reduce "
                          "(default), zero = own reduce-scatter + sharded LARS update + all-gather "
                          "of the working weights, ring/hierarchical/sharded = NCCL all-reduce")
@@ -202,7 +202,7 @@ def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, wa
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    flat = args.algorithm in ("ring", "ordered", "zero")
+    flat = args.algorithm in ("ring", "ordered", "zero", "zero_unfused")
     eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     r = cpu_reference(args.model, world, args.theta, eta, args.steps, args.warmup)
     line = {
@@ -240,14 +240,15 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if world > 1:
         k = args.group_size if args.algorithm in ("hierarchical", "sharded") else 1
         comm = Communicator(gs.Topology(world, k if world % k == 0 else 1))
-    flat = args.algorithm in ("ring", "ordered", "zero")
+    flat = args.algorithm in ("ring", "ordered", "zero", "zero_unfused")
     eta = args.eta_bytes if args.eta_bytes is not None else (0 if flat else 1 << 62)
     cfg = gs.LarsConfig(gs.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0, weight_decay=5e-4,
                         momentum=0.9)
     pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=args.theta, comm=comm, eta_bytes=eta,
                                hier_variant=args.algorithm if not flat else "hierarchical",
                                flat_variant="ordered" if args.algorithm == "ordered" else "ring",
-                               sharded_update=args.algorithm == "zero" and world > 1,
+                               sharded_update=args.algorithm.startswith("zero") and world > 1,
+                               fused_collective=args.algorithm == "zero",
                                init_master=sh.synth_master(specs, seed=0),
                                loss_scale=gs.LossScale(1024.0), device=dev)
     grads_host = torch.from_numpy(sh.synth_wire_grads(specs, rank=rank, seed=0)).pin_memory()
@@ -319,11 +320,19 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             phase_ms.setdefault(x, []).append(ev[x].elapsed_time(ev[y]))
 
     mean_ms = statistics.mean(step_ms)
-    t = torch.tensor([mean_ms, statistics.median(phase_ms["pass2"])], dtype=torch.float64,
-                     device=dev)
+    # the dominant kernel: pass 2 (gs_pass2_push in the fused sharded step,
+    # over this rank's owned elements only); its achieved bandwidth is taken
+    # per rank and the slowest rank reported
+    p2_name = "pass2_push" if "pass2_push" in phase_ms else "pass2"
+    p2_elems = (pipe.owned[1] - pipe.owned[0]) if pipe.sharded else n_params
+    p2_ms_local = statistics.median(phase_ms[p2_name])
+    t = torch.tensor([mean_ms, -20.0 * p2_elems / (p2_ms_local * 1e-3) / 1e9],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    mean_ms, pass2_ms = float(t[0]), float(t[1])
+    mean_ms, achieved = float(t[0]), -float(t[1])
+    pass2_bytes = 20 * p2_elems
+    pass2_ms = p2_ms_local
 
     # ---- all-reduce bus bandwidth on the whole fp16 gradient (S = 2N bytes)
     allreduce = None
@@ -361,8 +370,6 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if rank != 0:
         return
     peak, peak_kind = load_peaks()
-    pass2_bytes = 20 * n_params
-    achieved = pass2_bytes / (pass2_ms * 1e-3) / 1e9
     traffic = None
     tfile = ROOT / "profiles" / "pass2_traffic.json"
     if tfile.exists():
@@ -378,8 +385,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "dtype": "f32", "wire_dtype": "f16", "data": "synthetic",
         "config": {"workload": f"{args.model} fused MP-LARS step (" + (
                        "pack -> pass1 -> trust -> pass2" if world == 1 else
+                       "pack -> [reduce-scatter+pass1, partials pushed] -> fence -> trust -> "
+                       "[pass2+w16 push] -> fence" if args.algorithm == "zero" else
                        "pack -> reduce-scatter -> pass1(shard) -> gather partials -> trust -> "
-                       "pass2(shard) -> all-gather w16" if args.algorithm == "zero" else
+                       "pass2(shard) -> all-gather w16" if args.algorithm == "zero_unfused" else
                        "pack -> allreduce -> pass1 -> trust -> pass2") + ")",
                    "model": args.model, "params": n_params, "tensors": len(specs),
                    "theta": args.theta, "buckets": len(pipe.buckets),
@@ -388,7 +397,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                    "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every step"},
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
-        "roofline": {"bound": "hbm", "kernel": "gs_lars_pass2", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm",
+                     "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2", "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": pass2_bytes},

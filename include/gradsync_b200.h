@@ -206,6 +206,41 @@ int gs_ordered_allgather(const uint64_t* bufs, const uint64_t* sig, int rank, in
 /* *counter += inc on the device (stream-ordered; graph-capturable). */
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 
+/* ---- collective + LARS fused (sharded update, gs_fused.cu) ------------- */
+
+/* Reduce-scatter fused with LARS pass 1 (replaces gs_ordered_reduce_scatter_f16
+ * + gs_lars_pass1 + the all-gather of the chunk partials; reference:
+ * collectives.py:273-283 fold_f16_tree then lars.py:142-177 norms).  After an
+ * entry barrier, chunks [c0, c1) of the local chunk table — this rank's
+ * chunks of one bucket — are folded from every peer's wire (wires[q] = peer
+ * q's base, the segment's g pointers lie in wires[rank]) in the reference's
+ * tree order, stored into the local wire, and reduced to fp64 partials that
+ * are STORED into every peer's partials array (peer_partials[q], 3 doubles
+ * per chunk at the chunk's global index); the step flags are OR-ed into every
+ * peer's flag word (peer_flags[q]).  Every rank must call it (also with
+ * c0 == c1) with the same epoch; p in {2, 4, 8}. */
+int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
+                const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
+                const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
+                const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
+                int nblocks, void* stream);
+
+/* LARS pass 2 over chunks [c0, c1) (binary16 gradients) that also stores each
+ * updated binary16 working weight into every peer's working arena
+ * (peer_working[q] = peer q's base; the segments' w16 lie in
+ * peer_working[rank]).  Replaces gs_lars_pass2 + the all-gather of the
+ * working weights (lars.py:178-181).  Launched as a programmatic dependent of
+ * gs_lars_trust. */
+int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
+                  const gs_step_params* params, uint32_t hint, const float* seg_scale,
+                  const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
+                  int rank, void* stream);
+
+/* One-CTA barrier: this GPU's remote stores from earlier kernels on the
+ * stream are visible to every peer, and every peer's to this GPU. */
+int gs_peer_fence(const uint64_t* sig, int rank, int p, uint32_t epoch, const uint32_t* epoch_base,
+                  void* stream);
+
 /* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
 
 /* Pass 1 over `nchunk` chunks starting at chunk index `chunk0`: widen (fp16

@@ -1,0 +1,340 @@
+// gs_lars_device.cuh — device-side building blocks of the LARS passes
+// (element arithmetic, chunk reductions, trust evaluation), shared by the
+// LARS kernels (gs_lars.cu) and the fused collective + LARS kernels
+// (gs_fused.cu).  See gs_lars.cu for the semantics and reference lines.
+#pragma once
+
+#include "gs_common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRounds = 4;                      // 8-element vectors per thread
+#ifndef GS_P1_ROUNDS
+#define GS_P1_ROUNDS 4   // pass-1 load batch (vectors per thread)
+#endif
+#ifndef GS_P1_MINB
+#define GS_P1_MINB 4     // pass-1 __launch_bounds__ min blocks per SM
+#endif
+constexpr int kP1Rounds = GS_P1_ROUNDS;
+constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
+constexpr int kTrustThreads = 1024;
+constexpr uint32_t kBoth = GS_FLAG_SCALED_NONFINITE | GS_FLAG_GRAD_NONFINITE;
+
+// Pairwise fp32 ops, each lane rounded separately.  NOT the packed
+// __fmul2_rn/__fadd2_rn intrinsics: ptxas 12.9 contracts mul.rn.f32x2 feeding
+// add.rn.f32x2 into FFMA2 even under -fmad=false (seen in SASS), which would
+// break the separate roundings numpy performs; scalar mul.rn/add.rn are kept.
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+}
+
+__device__ __forceinline__ void sq_acc(double& acc, float x) {
+  const double d = (double)x;
+  acc = fma(d, d, acc);
+}
+
+// |x| widened to fp64 with integer ops (exact for normal floats and +-0;
+// NOT for subnormals; Inf/NaN map to garbage finite values, which only occurs
+// on steps the flags reject).  F2F.F64.F32 issues on the XU pipe at a quarter
+// of the ALU rate and was pass 1's co-limiter (ncu: XU 43 % busy), so the
+// squares of normal values are widened on the ALU instead.
+__device__ __forceinline__ double f2d_normal_abs(float x) {
+  const uint32_t a = __float_as_uint(x) & 0x7FFFFFFFu;
+  const uint32_t hi = a ? (a >> 3) + 0x38000000u : 0u;
+  return __hiloint2double((int)hi, (int)(a << 29));
+}
+
+__device__ __forceinline__ void sq_acc_int(double& acc, float x) {
+  const double d = f2d_normal_abs(x);
+  acc = fma(d, d, acc);
+}
+
+__device__ __forceinline__ bool is_subnormal_nonzero(float x) {
+  return (__float_as_uint(x) & 0x7FFFFFFFu) - 1u < 0x007FFFFFu;
+}
+
+// release-ordered arrival: the partials this thread stored become visible no
+// later than the counter increment (no full fence / L1 invalidate on the
+// common path; the rare last arriver fences before reading everyone's data)
+__device__ __forceinline__ uint32_t arrive_release(uint32_t* p) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
+// raw binary16 non-finite detector for two halves in one word: adding 0x0400
+// to an all-ones exponent field carries into the (masked-off) sign position
+__device__ __forceinline__ uint32_t raw_nonfinite_bits(uint32_t w) {
+  return (w & 0x7C007C00u) + 0x04000400u;
+}
+
+struct Ctx {
+  gs::Unscale u;
+  float mul, wd, m;
+};
+
+struct Acc {
+  double sw = 0.0, se = 0.0, sg = 0.0;
+  uint32_t fl = 0u, raw = 0u;
+};
+
+// ------------------------------------------------------------ pass 1 body
+// One element pair (x = widened gradient, w = master).
+// GINT: gradients are widened for the squares with integer ops (fp16 input
+// with exact power-of-two scaling: every value is 0, normal, or non-finite).
+// WINT: the same for the masters (the caller checked for subnormals).
+template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool GINT = false,
+          bool WINT = false>
+__device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& a) {
+  float2 gu;
+  if (POW2) {
+    gu = mul2(x, make_float2(cx.mul, cx.mul));
+    if (!RAWFLAG) {
+      // the mean x/p (p >= 1) is non-finite iff x is; the unscaled value
+      // can additionally overflow when mul > 1
+      a.fl |= (gs::is_finite_f32(x.x) && gs::is_finite_f32(x.y)) ? 0u : kBoth;
+      a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
+    }
+  } else {
+    const float mx = cx.u.mean(x.x), my = cx.u.mean(x.y);
+    a.fl |= (gs::is_finite_f32(mx) && gs::is_finite_f32(my)) ? 0u : GS_FLAG_SCALED_NONFINITE;
+    gu = make_float2(cx.u.unscale(mx), cx.u.unscale(my));
+    a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
+  }
+  if (LARS) {
+    if (WINT) {
+      sq_acc_int(a.sw, w.x);
+      sq_acc_int(a.sw, w.y);
+    } else {
+      sq_acc(a.sw, w.x);
+      sq_acc(a.sw, w.y);
+    }
+    if (DECAY) {
+      // eff = g + float32(wd) * w, two roundings (lars.py:172)
+      const float2 eff = add2(gu, mul2(make_float2(cx.wd, cx.wd), w));
+      sq_acc(a.se, eff.x);
+      sq_acc(a.se, eff.y);
+    }
+  }
+  if (GNORM || (LARS && !DECAY)) {
+    if (GINT) {
+      sq_acc_int(a.sg, gu.x);
+      sq_acc_int(a.sg, gu.y);
+    } else {
+      sq_acc(a.sg, gu.x);
+      sq_acc(a.sg, gu.y);
+    }
+  }
+}
+
+template <bool F16>
+struct G;
+template <>
+struct G<true> {
+  using T = uint16_t;
+  using V = uint4;  // 8 halves
+  static __device__ __forceinline__ V ld(const T* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+  static __device__ __forceinline__ float2 pair(const V& v, int q) {
+    return gs::widen2((&v.x)[q]);
+  }
+  static __device__ __forceinline__ float one(const T* p) { return gs::widen(*p); }
+};
+struct F8 {
+  float4 a, b;
+};
+template <>
+struct G<false> {
+  using T = float;
+  using V = F8;
+  static __device__ __forceinline__ V ld(const T* p) {
+    return F8{__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
+  }
+  static __device__ __forceinline__ float2 pair(const V& v, int q) {
+    return q == 0 ? make_float2(v.a.x, v.a.y) : q == 1 ? make_float2(v.a.z, v.a.w)
+         : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);
+  }
+  static __device__ __forceinline__ float one(const T* p) { return *p; }
+};
+
+__device__ __forceinline__ F8 ldw(const float* p) {
+  return F8{__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
+}
+__device__ __forceinline__ float2 wpair(const F8& v, int q) {
+  return q == 0 ? make_float2(v.a.x, v.a.y) : q == 1 ? make_float2(v.a.z, v.a.w)
+       : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& wv, const Ctx& cx,
+                                       Acc& a) {
+  if (RAWFLAG) {
+    const uint4& r = reinterpret_cast<const uint4&>(gv);
+    a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
+             raw_nonfinite_bits(r.w);
+  }
+  constexpr bool GINT = F16 && POW2;
+  bool wsub = false;
+  if (LARS) {
+    wsub = is_subnormal_nonzero(wv.a.x) | is_subnormal_nonzero(wv.a.y) |
+           is_subnormal_nonzero(wv.a.z) | is_subnormal_nonzero(wv.a.w) |
+           is_subnormal_nonzero(wv.b.x) | is_subnormal_nonzero(wv.b.y) |
+           is_subnormal_nonzero(wv.b.z) | is_subnormal_nonzero(wv.b.w);
+    wsub = __any_sync(__activemask(), wsub);  // warp-uniform: a subnormal master is rare
+  }
+  if (!wsub) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, true>(
+          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, false>(
+          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
+  }
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ g,
+                                         const float* __restrict__ w, uint16_t* __restrict__ gcopy,
+                                         int len, const Ctx& cx, Acc& a) {
+  using Gt = G<F16>;
+  const bool vec = gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w)) &&
+                   (gcopy == nullptr || gs::is_aligned16(gcopy));
+  const int nv = vec ? len / 8 : 0;
+  const int t = threadIdx.x;
+  // full batches of kRounds vectors per thread: issue every load of the
+  // batch (4 x 16 B of g, 4 x 32 B of w) before any arithmetic; each thread
+  // still visits its vectors t, t+256, t+512, ... in increasing order, so
+  // the batching never changes the summation order
+  constexpr int kBatch = kP1Rounds * kThreads;
+  int done = 0;
+  for (; done + kBatch <= nv; done += kBatch) {
+    typename Gt::V gv[kP1Rounds];
+    F8 wv[kP1Rounds];
+#pragma unroll
+    for (int k = 0; k < kP1Rounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
+    if (LARS) {
+#pragma unroll
+      for (int k = 0; k < kP1Rounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
+    }
+    if (F16 && gcopy != nullptr) {
+#pragma unroll
+      for (int k = 0; k < kP1Rounds; ++k)
+        reinterpret_cast<uint4*>(gcopy)[done + t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kP1Rounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
+  }
+  for (int i = done + t; i < nv; i += kThreads) {
+    const typename Gt::V gv = Gt::ld(g + 8 * i);
+    F8 wv{};
+    if (LARS) wv = ldw(w + 8 * i);
+    if (F16 && gcopy != nullptr) reinterpret_cast<uint4*>(gcopy)[i] = reinterpret_cast<const uint4&>(gv);
+    p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv, wv, cx, a);
+  }
+  // scalar tail (and misaligned segments): pair the element with a zero
+  // partner that contributes nothing
+  for (int i = nv * 8 + t; i < len; i += kThreads) {
+    if (F16) {
+      const uint16_t h = reinterpret_cast<const uint16_t*>(g)[i];
+      if (gcopy != nullptr) gcopy[i] = h;
+      if (RAWFLAG) a.raw |= raw_nonfinite_bits(h);
+    }
+    const float x = Gt::one(g + i);
+    const float wx = LARS ? w[i] : 0.0f;
+    Acc b;
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(make_float2(x, 0.0f), make_float2(wx, 0.0f), cx, b);
+    a.sw += b.sw;
+    a.se += b.se;
+    a.sg += b.sg;
+    a.fl |= b.fl;
+  }
+}
+
+// lars_local_lr (lars.py:142-150) + lars.py:177 for one segment: norms are
+// sqrt of the fp64 dots, local = (eta * w_norm) / (g_norm + eps) or 1.0 when
+// degenerate / LARS disabled, scale = float32(local * gamma).
+__device__ __forceinline__ void trust_eval(uint32_t sflags, double sw, double se, double sg,
+                                           const gs_step_params* __restrict__ params,
+                                           float* scale_out, double* o) {
+  const double w_norm = __dsqrt_rn(sw);
+  const double g_norm = __dsqrt_rn(se);
+  double local = 1.0;
+  if (sflags & GS_SEG_LARS_ENABLED) {
+    const double denom = __dadd_rn(g_norm, params->epsilon);
+    if (!(w_norm == 0.0 || denom == 0.0)) local = __ddiv_rn(__dmul_rn(params->eta, w_norm), denom);
+  }
+  *scale_out = __double2float_rn(__dmul_rn(local, params->gamma));
+  o[0] = w_norm;
+  o[1] = g_norm;
+  o[2] = local;
+  o[3] = sg;
+}
+
+// experiment.py:408-411: sqrt(sum over groups of float(dot(g, g))), summed in
+// group order starting from 0.
+__device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg) {
+  double acc = 0.0;
+  for (int s = 0; s < nseg; ++s) acc = __dadd_rn(acc, __ldcg(seg_out + 4 * (int64_t)s + 3));
+  return __dsqrt_rn(acc);
+}
+
+// ----------------------------------------------------------------- pass 2
+// v = m*v + s*eff (lars.py:178), w -= v (:179), w16 = f32_to_f16(w) (:180),
+// eff = g or g + wd*w (:169-172); every product and sum rounded separately.
+template <bool POW2, bool DECAY>
+__device__ __forceinline__ void p2_pair(float2 x, float2& w, float2& v, const Ctx& cx, float s) {
+  float2 gu;
+  if (POW2) {
+    gu = mul2(x, make_float2(cx.mul, cx.mul));
+  } else {
+    gu = make_float2(cx.u.unscale(cx.u.mean(x.x)), cx.u.unscale(cx.u.mean(x.y)));
+  }
+  const float2 eff = DECAY ? add2(gu, mul2(make_float2(cx.wd, cx.wd), w)) : gu;
+  v = add2(mul2(make_float2(cx.m, cx.m), v), mul2(make_float2(s, s), eff));
+  w = sub2(w, v);
+}
+
+// binary16 pack with NaN canonicalisation for two lanes
+__device__ __forceinline__ uint32_t pack_w16(float2 w) {
+  __half2 h = __floats2half2_rn(w.x, w.y);
+  uint32_t bits = *reinterpret_cast<uint32_t*>(&h);
+  // any half with |h| > 0x7C00 is a NaN: force 0x7E00 (halfprec.py:76-77)
+  const uint32_t nan = __vcmpgtu2(bits & 0x7FFF7FFFu, 0x7C007C00u);
+  return (bits & ~nan) | (0x7E007E00u & nan);
+}
+
+template <bool F16, bool POW2, bool DECAY>
+__device__ __forceinline__ void p2_vec(const typename G<F16>::V& gv, const F8& wv, const F8& vv,
+                                       float* __restrict__ w, float* __restrict__ v,
+                                       uint16_t* __restrict__ w16, int i, const Ctx& cx, float s) {
+  float2 ww[4] = {make_float2(wv.a.x, wv.a.y), make_float2(wv.a.z, wv.a.w),
+                  make_float2(wv.b.x, wv.b.y), make_float2(wv.b.z, wv.b.w)};
+  float2 xv[4] = {make_float2(vv.a.x, vv.a.y), make_float2(vv.a.z, vv.a.w),
+                  make_float2(vv.b.x, vv.b.y), make_float2(vv.b.z, vv.b.w)};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) p2_pair<POW2, DECAY>(G<F16>::pair(gv, q), ww[q], xv[q], cx, s);
+  float4* vp = reinterpret_cast<float4*>(v) + 2 * i;
+  float4* wp = reinterpret_cast<float4*>(w) + 2 * i;
+  __stcs(vp, make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y));
+  __stcs(vp + 1, make_float4(xv[2].x, xv[2].y, xv[3].x, xv[3].y));
+  __stcs(wp, make_float4(ww[0].x, ww[0].y, ww[1].x, ww[1].y));
+  __stcs(wp + 1, make_float4(ww[2].x, ww[2].y, ww[3].x, ww[3].y));
+  __stcs(reinterpret_cast<uint4*>(w16) + i,
+         make_uint4(pack_w16(ww[0]), pack_w16(ww[1]), pack_w16(ww[2]), pack_w16(ww[3])));
+}
+
+__device__ __forceinline__ F8 ld8(const float* p, int i) {
+  const float4* q = reinterpret_cast<const float4*>(p) + 2 * i;
+  return F8{q[0], q[1]};
+}
+
+}  // namespace

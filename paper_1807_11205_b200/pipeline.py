@@ -141,7 +141,8 @@ class GradientPipeline:
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
                  bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = False,
-                 flat_variant: str = "ring", sharded_update: bool = False):
+                 flat_variant: str = "ring", sharded_update: bool = False,
+                 fused_collective: bool = True):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -168,6 +169,11 @@ class GradientPipeline:
 
         d = self.device
         self.sharded = bool(sharded_update)
+        # sharded update: reduce-scatter fused with pass 1 and pass 2 fused
+        # with the working-weight push (gs_fused.cu) instead of separate
+        # collective kernels
+        self.fused_collective = bool(fused_collective) and self.sharded and \
+            comm is not None and comm.topo.p in (2, 4, 8)
         if self.sharded and (comm is None or comm.topo.p < 2):
             raise ValueError("sharded_update needs a Communicator with p >= 2")
         for b in self.buckets:
@@ -337,6 +343,12 @@ class GradientPipeline:
                 ev.record(ps)
                 evs.append(ev)
         nb = len(self.buckets)
+        if self.fused_collective:
+            self._launch_sharded_fused(s0, sh, evs, sig, ebase, wires, timer)
+            self._last_wire = wire
+            self._half ^= 1
+            plan.use_segments(None)
+            return
         for b, bk in enumerate(self.buckets):
             s0.wait_event(evs[b])
             if timer:
@@ -370,6 +382,45 @@ class GradientPipeline:
         plan.use_segments(None)
         self._last_wire = wire
         self._half ^= 1
+        if timer:
+            timer("end")
+
+    def _launch_sharded_fused(self, s0, sh, evs, sig, ebase, wires, timer) -> None:
+        """The sharded step in fused kernels: per bucket one gs_rs_pass1
+        (reduce-scatter + pass 1, partials and flags pushed to every peer),
+        a one-CTA peer fence, trust, gs_pass2_push (pass 2 + working-weight
+        push to every peer), and a closing fence."""
+        plan, a = self.plan, self.arena
+        p, r = self.comm.topo.p, self.comm.rank
+        C = self._own_chunks
+        nb = len(self.buckets)
+        parts, flags = dev.ptr(a.peers("partials")), dev.ptr(a.peers("flags"))
+        for b, bk in enumerate(self.buckets):
+            s0.wait_event(evs[b])
+            if timer:
+                timer(f"rs_pass1_{b}")
+            c0 = max(bk.chunk0, C[r])
+            c1 = max(c0, min(bk.chunk0 + bk.nchunk, C[r + 1]))
+            _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
+                         dev.ptr(plan.d_chunks), c0, c1, dev.ptr(plan.params), plan.hint,
+                         parts, flags, b + 1, ebase, self._nblocks, sh)
+        s0.wait_stream(self._pack_stream)
+        if timer:
+            timer("fence")
+        _native.call("gs_peer_fence", sig, r, p, nb + 1, ebase, sh)
+        if timer:
+            timer("trust")
+        plan.trust(sh)
+        if timer:
+            timer("pass2_push")
+        mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
+        _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), C[r],
+                     C[r + 1], dev.ptr(plan.params), plan.hint, dev.ptr(plan.seg_scale),
+                     dev.ptr(plan.flags), mask, dev.ptr(a.peers("working")), p, r, sh)
+        if timer:
+            timer("fence_end")
+        _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
+        _native.call("gs_counter_add", ebase, nb + 3, sh)
         if timer:
             timer("end")
 

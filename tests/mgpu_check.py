@@ -49,8 +49,8 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    algos = os.environ.get("MGPU_ALGOS", "zero,ordered,ring,hierarchical,sharded").split(",")
-    for algo, k in (("zero", 1), ("ordered", 1), ("ring", 1), ("hierarchical", 2),
+    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded").split(",")
+    for algo, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ring", 1), ("hierarchical", 2),
                     ("sharded", 2)):
         if algo not in algos:
             continue
@@ -62,7 +62,8 @@ def main():
                                    eta_bytes=0 if algo in ("ring", "ordered") else 1 << 62,
                                    hier_variant=algo if algo not in ("ring", "ordered") else "hierarchical",
                                    flat_variant="ordered" if algo == "ordered" else "ring",
-                                   sharded_update=algo == "zero",
+                                   sharded_update=algo.startswith("zero"),
+                                   fused_collective=algo == "zero",
                                    init_master=master, loss_scale=gs.LossScale(1024.0), device=dev)
         groups = [rp.Group(s.name, s.kind, w.copy(), np.zeros(s.numel, np.float32),
                            np.zeros(s.numel, np.float32), rp.narrow(w))
@@ -77,17 +78,17 @@ def main():
                 wires[world - 1][4321] = 0x7C00
             res = pipe.step(torch.from_numpy(wires[rank]).to(dev), step)
             reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]
-            if algo == "zero":
+            if algo.startswith("zero"):
                 pipe.gather_state()  # masters/velocities are sharded (ZeRO-1)
                 torch.cuda.synchronize(dev)
             if rank == 0:
                 parts = [split(w, specs) for w in wires]
-                exact = world == 2 or algo in ("ordered", "zero")
+                exact = world == 2 or algo in ("ordered", "zero", "zero_unfused")
                 out = rp.compose_step_fp16(parts, [s.name for s in specs], [s.numel for s in specs],
                                            order, groups, rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1,
                                            oloss, theta, 0,
                                            reduced_override=None if exact else reduced)
-                if not exact and algo != "zero":
+                if not exact and not algo.startswith("zero"):
                     # reduced buckets within the reference's fp16 bound
                     tree = rp.compose_step_fp16  # noqa: F841 (documentation)
                     for b, bk in enumerate(pipe.buckets):

@@ -10,8 +10,8 @@ One step = pack the rank's 161 fp16 gradient tensors into theta-buckets ->
 all-reduce every bucket over NCCL (N > 1) -> pass 1 (mean, overflow flags,
 unscale, fp64 segment norms) -> trust ratios -> pass 2 (momentum / master /
 working-copy update) -> read the flags (the one host sync).  Inputs are
-resident in HBM; L2 is flushed (256 MiB written) before every timed step and
-each step is timed alone with CUDA events on the launching stream; the value
+resident in HBM; L2 is flushed (256 MiB written, then read back so it is
+left clean) before every timed step and each step is timed alone with CUDA events on the launching stream; the value
 is the mean step time, max over ranks.
 """
 
@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-allreduce-sweep", action="store_true")
+    ap.add_argument("--overflow", action="store_true",
+                    help="forced overflow: rank 0's gradient carries +Inf, every step takes "
+                         "the skip path (fixed loss-scale policy so the scale stays put)")
     ap.add_argument("--no-soak", action="store_true", help="skip the clock soak (profiling runs)")
     return ap.parse_args()
 
@@ -250,14 +253,24 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                                sharded_update=args.algorithm.startswith("zero") and world > 1,
                                fused_collective=args.algorithm == "zero",
                                init_master=sh.synth_master(specs, seed=0),
-                               loss_scale=gs.LossScale(1024.0), device=dev)
-    grads_host = torch.from_numpy(sh.synth_wire_grads(specs, rank=rank, seed=0)).pin_memory()
+                               loss_scale=gs.LossScale(1024.0, policy="fixed" if args.overflow
+                                                       else "dynamic"), device=dev)
+    wire_np = sh.synth_wire_grads(specs, rank=rank, seed=0)
+    if args.overflow and rank == 0:
+        wire_np[len(wire_np) // 2] = 0x7C00  # +Inf: every step is skipped
+    grads_host = torch.from_numpy(wire_np).pin_memory()
     grads = grads_host.to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     s0 = torch.cuda.current_stream(dev)
 
+    flush_sink = torch.zeros(1, dtype=torch.int64, device=dev)
+
     def flush_l2():
+        # write 256 MiB (> 126 MB L2), then read it back: every line of the
+        # step's data is evicted AND the L2 is left clean, so the write-back of
+        # the flush buffer's dirty lines is not charged to the timed step
         _native.call("gs_fill_zero", flush.data_ptr(), flush.numel(), int(s0.cuda_stream))
+        flush_sink.add_(flush.view(torch.int64).sum())
 
     def barrier():
         if world > 1:
@@ -394,7 +407,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                    "theta": args.theta, "buckets": len(pipe.buckets),
                    "algorithm": args.algorithm if world > 1 else "none",
                    "topology": (f"Topology({world},{comm.topo.k})" if comm else "1 GPU"),
-                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every step"},
+                   "forced_overflow": bool(args.overflow),
+                   "parallelism": f"dp{world}", "l2": "flushed before every step (256 MiB write, then read: no step data resident, L2 clean)"},
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
         "roofline": {"bound": "hbm",

@@ -1,0 +1,184 @@
+#!/usr/bin/env python
+"""All-reduce message-size sweep (BASELINE.json config 5).
+
+fp16 sum all-reduce of 2^10 ... 2^30 bytes at p = WORLD_SIZE GPUs, for every
+variant the pipeline can pick per bucket (collectives.py:238-340):
+
+  ring                 flat 1xp ncclAllReduce (fp16 wire)
+  hierarchical_GxK     the paper's literal reduce -> masters all-reduce ->
+                       broadcast on Topology(p, K) sub-communicators
+  sharded_GxK          intra-group reduce-scatter -> same-offset all-reduce ->
+                       intra-group all-gather
+  ordered              our symmetric-memory NVLink kernel, reference fold order
+
+with FORCED OVERFLOW: rank 0's buffer carries 0x7C00 (+Inf) at element 0 and
+every other element is a finite binary16, so every result must carry Inf
+there — the overflow flag the loss scale's skip decision reads
+(halfprec.py:209-216).  The ordered kernel reports it through its own
+non-finite flag; NCCL results are checked directly.  busBW = S/t * 2(p-1)/p
+(nccl-tests convention) for every variant; max over ranks of the per-rank
+CUDA-event time on the launching stream.
+
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+      --master-addr 127.0.0.1 --master-port P tools/allreduce_sweep.py [--max-log2 30]
+
+Rank 0 prints one JSON line per (size, variant) and a final summary line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--min-log2", type=int, default=10)
+    ap.add_argument("--max-log2", type=int, default=30)
+    ap.add_argument("--variants", default="ring,hierarchical,sharded,ordered")
+    ap.add_argument("--out", default=None, help="also write the lines to this file (rank 0)")
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_11205_b200 as gs
+    from paper_1807_11205_b200 import _device as dv
+    from paper_1807_11205_b200 import _native
+    from paper_1807_11205_b200.dist import Communicator, OrderedWire, init_from_env
+
+    rank, world, local = init_from_env("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    s0 = torch.cuda.current_stream(dev)
+    want = set(args.variants.split(","))
+    max_elems = (1 << args.max_log2) // 2
+
+    variants = []
+    if "ring" in want:
+        variants.append(("ring", 1))
+    for k in (4, 2):
+        if 1 < k < world and world % k == 0:
+            if "hierarchical" in want:
+                variants.append((f"hierarchical_{world // k}x{k}", k))
+            if "sharded" in want:
+                variants.append((f"sharded_{world // k}x{k}", k))
+    if "ordered" in want:
+        variants.append(("ordered", 1))
+    comms = {k: Communicator(gs.Topology(world, k)) for k in sorted({k for _, k in variants})}
+
+    # finite binary16 payload (small values: no finite sum overflows), Inf at 0 on rank 0
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    base = (torch.rand(max_elems, generator=g) * 2e-3 - 1e-3).to(torch.float16).to(dev)
+    buf = torch.empty_like(base)
+    ow = OrderedWire(comms[1], max_elems, dev) if ("ordered", 1) in variants else None
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    half = [0]
+    lines = []
+    for lg in range(args.min_log2, args.max_log2 + 1):
+        S = 1 << lg
+        n = S // 2
+        for name, k in variants:
+            comm = comms[k]
+            algo = name.split("_")[0]
+            nn = n - n % k if algo == "sharded" else n
+            if nn == 0:
+                continue
+            if algo == "ordered":
+                def refill():
+                    h = ow.halves[half[0]]
+                    h[:nn].view(torch.float16).copy_(base[:nn])
+                    if rank == 0:
+                        h[:1].view(torch.int16).fill_(0x7C00)
+
+                def run():
+                    _native.call("gs_ordered_allreduce_f16", dv.ptr(ow.bufs_dev[half[0]]),
+                                 dv.ptr(ow.sig_dev), ow.rank, ow.p, 0, nn, 1,
+                                 dv.ptr(ow.epoch_base), ow.nblocks, dv.ptr(flag),
+                                 int(s0.cuda_stream))
+                    ow.advance(1, int(s0.cuda_stream))
+                    half[0] ^= 1
+
+                def result():
+                    return ow.halves[half[0] ^ 1][:nn].view(torch.float16)
+            else:
+                t = buf[:nn]
+
+                def refill(_t=t):
+                    _t.copy_(base[:nn])
+                    if rank == 0:
+                        _t[:1].view(torch.int16).fill_(0x7C00)
+
+                def run(_t=t, _c=comm, _a=algo):
+                    _c.allreduce(_t, _a)
+
+                def result(_t=t):
+                    return _t
+            # correctness of the forced-overflow path (one untimed call)
+            flag.zero_()
+            refill()
+            if algo == "ordered":
+                refill()  # both halves hold the payload
+                half[0] ^= 1
+                refill()
+                half[0] ^= 1
+            torch.cuda.synchronize(dev)
+            dist.barrier(device_ids=[local])
+            run()
+            torch.cuda.synchronize(dev)
+            r = result()
+            inf_ok = bool(torch.isinf(r[0]).item())
+            finite_rest = bool(torch.isfinite(r[1:]).all().item()) if nn > 1 else True
+            flag_ok = bool(flag.item() != 0) if algo == "ordered" else None
+            # timing: in-place repeats grow the values by ~p per call until they
+            # saturate to Inf; binary16 adds cost the same on any value
+            iters = 50 if S <= (1 << 20) else (20 if S <= (1 << 26) else 5)
+            for _ in range(3):
+                run()
+            torch.cuda.synchronize(dev)
+            dist.barrier(device_ids=[local])
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s0)
+            for _ in range(iters):
+                run()
+            b.record(s0)
+            b.synchronize()
+            ms = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=dev)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            ok = torch.tensor([int(inf_ok and finite_rest and flag_ok is not False)],
+                              dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            sec = float(ms) * 1e-3
+            Sb = 2 * nn
+            line = {"bytes": Sb, "variant": name, "p": world, "us": round(sec * 1e6, 2),
+                    "algbw_gbs": round(Sb / sec / 1e9, 2),
+                    "busbw_gbs": round(Sb / sec * 2 * (world - 1) / world / 1e9, 2),
+                    "overflow_propagated": bool(ok.item()), "iters": iters}
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            lines.append(line)
+    if rank == 0:
+        best = {}
+        for ln in lines:
+            v = ln["variant"]
+            best[v] = max(best.get(v, 0.0), ln["busbw_gbs"])
+        summary = {"summary": "allreduce_sweep", "p": world,
+                   "nccl_algo_env": os.environ.get("NCCL_ALGO"),
+                   "peak_busbw_gbs": best,
+                   "all_overflow_propagated": all(ln["overflow_propagated"] for ln in lines)}
+        print(json.dumps(summary), flush=True)
+        if args.out:
+            Path(args.out).write_text("\n".join(json.dumps(x) for x in lines + [summary]) + "\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -277,6 +277,15 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
 
+    tok = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def device_barrier():
+        """Untimed, on the launching stream: a 4-byte all-reduce that every
+        rank's stream leaves at (nearly) the same moment, so a timed step
+        starts together on all ranks instead of absorbing host launch skew."""
+        if world > 1:
+            dist.all_reduce(tok)
+
     barrier()  # ranks start the first step together
     # ---- warmup (the first two calls also capture the CUDA graph at p = 1)
     for i in range(args.warmup):
@@ -300,6 +309,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     for i in range(args.steps):
         flush_l2()
         pipe.prepare(args.warmup + i)  # host-only: schedule, loss scale, hint
+        device_barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s0)
@@ -319,6 +329,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     for i in range(max(3, min(args.steps, 10))):
         flush_l2()
         torch.cuda._sleep(4_000_000)
+        device_barrier()
         ev = {}
 
         def mark(name):
@@ -361,6 +372,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             pipe.prepare(1000 + i)
+            device_barrier()
             a.record(s0)
             pipe.enqueue_host(grads_host, 1000 + i)  # H2D per bucket, overlapped
             pipe.finish()

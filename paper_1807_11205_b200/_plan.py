@@ -168,15 +168,24 @@ class LarsPlan:
         # one int32 block, reset by one kernel per step: [0] = non-finite
         # flags, [4 : 4 + nseg + 1] = per-segment / global arrival counters
         # of the fused pass1 + trust kernel
-        self.flagbuf = flagbuf if flagbuf is not None else \
-            torch.zeros(4 + self.nseg + 1, dtype=torch.int32, device=device)
+        # the step scalars and (when the plan owns it) the flag block share one
+        # device allocation, [params | pad | flags], uploaded by ONE copy per
+        # step whose zero tail resets the flags — no separate reset launch
+        psz = _native.STEP_PARAMS_DTYPE.itemsize
+        pad = (psz + 15) // 16 * 16
+        nflag = 4 + self.nseg + 1
+        own_flags = flagbuf is None
+        ctl_bytes = pad + 4 * nflag if own_flags else psz
+        self._ctl = torch.zeros(ctl_bytes, dtype=torch.uint8, device=device)
+        self._pinned_ctl = torch.zeros(ctl_bytes, dtype=torch.uint8).pin_memory()
+        self.params = self._ctl[:psz]
+        self._pinned_params = self._pinned_ctl[:psz]
+        self.flagbuf = self._ctl[pad:].view(torch.int32) if own_flags else flagbuf
+        self._flags_in_ctl = own_flags
+        self._ctl_fresh = False
         self.flags = self.flagbuf[0:1]
         self.counters = self.flagbuf[4:]
         self.nseg_active = int((count > 0).sum())
-        self.params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize, dtype=torch.uint8,
-                                  device=device)
-        self._pinned_params = torch.zeros(_native.STEP_PARAMS_DTYPE.itemsize,
-                                          dtype=torch.uint8).pin_memory()
         self.hint = 0
         # pass 1 runs the register-staged kernel by default: on B200 it beats
         # the TMA-pipelined persistent kernel (43 vs 47 us on ResNet-50,
@@ -226,12 +235,18 @@ class LarsPlan:
         return self.hint
 
     def upload_params(self, stream=None) -> None:
-        """Device half of set_params: one 56-byte async copy."""
+        """Device half of set_params: one async copy of the step scalars and,
+        when the plan owns the flag block, of its zeros (the flag reset)."""
         s = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
-            self.params.copy_(self._pinned_params, non_blocking=True)
+            self._ctl.copy_(self._pinned_ctl, non_blocking=True)
+        self._ctl_fresh = self._flags_in_ctl
 
     def reset_flags(self, stream_h: int) -> None:
+        """Zero the flag block, unless the step's parameter upload just did."""
+        if self._ctl_fresh:
+            self._ctl_fresh = False
+            return
         _native.call("gs_fill_zero", dev.ptr(self.flagbuf), 4 * self.flagbuf.numel(), stream_h)
 
     @property

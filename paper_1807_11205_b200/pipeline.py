@@ -765,6 +765,150 @@ class GradientPipeline:
         plan.use_segments(None)
         self._last_wire = self.wire
 
+    # ------------------------------------------------------------ incremental
+    # The step split at bucket granularity, for a backward pass that hands
+    # gradients over as they are produced (overlap.py): bucket b
+    # is packed, reduced and run through pass 1 on a side stream as soon as
+    # its last gradient exists, while the backward pass keeps computing.
+    def begin(self, step: int) -> None:
+        """Open a step: stage the scalars, reset the flags (current stream)."""
+        if self.local:
+            raise ValueError("incremental steps need one gradient set per rank "
+                             "(local_workers > 1 takes whole gradient sets)")
+        if self.sharded and not self.fused_collective:
+            raise ValueError("incremental sharded steps use the fused kernels (p in 2, 4, 8)")
+        s0 = torch.cuda.current_stream(self.device)
+        if self._prepared != step:
+            self.prepare(step)
+        self._prepared = None
+        plan = self.plan
+        plan.upload_params(s0)
+        sh = int(s0.cuda_stream)
+        half = self._half
+        if self.sharded:
+            wire = self._halves[half]
+            plan.use_segments(plan.alt_segments([wire.data_ptr() + 2 * o for o in self.wire_off]))
+        elif self.ordered is not None:
+            wire = self.ordered.halves[half]
+            plan.use_segments(self._half_segments(half))
+        else:
+            wire = self.wire
+            plan.use_segments(None)
+        plan.reset_flags(sh)
+        if getattr(self, "_side_stream", None) is None:
+            self._side_stream = torch.cuda.Stream(device=self.device)
+        ss = self._side_stream
+        ss.wait_stream(s0)
+        self._inc = {"step": step, "half": half, "wire": wire, "next": 0,
+                     "ready": [None] * len(self.buckets)}
+
+    def submit(self, b: int, grads) -> None:
+        """Bucket b's gradients (tensors of its parameters, in `buckets[b].params`
+        order, fp16/uint16, on this device) are complete on the current stream.
+        Buckets launch strictly in bucket order (every rank issues the same
+        collective sequence), each as soon as it and all earlier ones are in."""
+        inc = getattr(self, "_inc", None)
+        if inc is None:
+            raise RuntimeError("submit() outside begin()/end()")
+        if inc["ready"][b] is not None:
+            raise ValueError(f"bucket {b} submitted twice in one step")
+        bk = self.buckets[b]
+        grads = list(grads)
+        if len(grads) != len(bk.params):
+            raise ValueError(f"bucket {b} holds {len(bk.params)} tensors, got {len(grads)}")
+        wb = inc["wire"].data_ptr()
+        pairs = []
+        for i, t in zip(bk.params, grads):
+            if t.numel() != self.sizes[i] or t.dtype not in (torch.uint16, torch.float16) \
+                    or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"gradient of {self.specs[i].name!r} must be a contiguous CUDA "
+                                 f"fp16 tensor of {self.sizes[i]} elements")
+            if self.sizes[i]:
+                pairs.append((t.data_ptr(), wb + 2 * self.wire_off[i], 2 * self.sizes[i]))
+        key = ("inc", b, wb) + tuple(p[0] for p in pairs)
+        tab = self._pack_cache.get(key)
+        if tab is None:
+            t = copy_table(pairs)
+            if len(self._pack_cache) > 64:
+                self._pack_cache.clear()
+                self._graphs.clear()
+            tab = self._pack_cache[key] = (dev.upload(t, self.device), len(t))
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        for t in grads:
+            t.record_stream(self._side_stream)  # read there; keep the allocator off it
+        inc["ready"][b] = (tab, ev, grads)
+        while inc["next"] < len(self.buckets) and inc["ready"][inc["next"]] is not None:
+            self._launch_bucket(inc["next"])
+            inc["next"] += 1
+
+    def _launch_bucket(self, b: int) -> None:
+        inc = self._inc
+        tab, ev, _ = inc["ready"][b]
+        bk, plan, ss = self.buckets[b], self.plan, self._side_stream
+        ss.wait_event(ev)
+        sh = int(ss.cuda_stream)
+        with torch.cuda.stream(ss):
+            if tab[1]:
+                _native.call("gs_batched_copy", dev.ptr(tab[0]), tab[1], sh)
+            if self.sharded:
+                p, r = self.comm.topo.p, self.comm.rank
+                C = self._own_chunks
+                c0 = max(bk.chunk0, C[r])
+                c1 = max(c0, min(bk.chunk0 + bk.nchunk, C[r + 1]))
+                wires = self.arena.peers("wireA" if inc["half"] == 0 else "wireB")
+                _native.call("gs_rs_pass1", dev.ptr(wires), dev.ptr(self.arena.peers("sig")), r,
+                             p, dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), c0, c1,
+                             dev.ptr(plan.params), plan.hint, dev.ptr(self.arena.peers("partials")),
+                             dev.ptr(self.arena.peers("flags")), b + 1, dev.ptr(self.epoch_base),
+                             self._nblocks, sh)
+                return
+            if bk.algorithm == "ordered":
+                self.ordered.allreduce(inc["half"], bk.start, bk.length, sh, slot=b)
+            elif bk.algorithm != "none":
+                self.comm.allreduce(inc["wire"][bk.start:bk.start + bk.padded], bk.algorithm)
+            if bk.nchunk:
+                plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+
+    def end(self) -> None:
+        """Close the step: every bucket must have been submitted; trust and
+        pass 2 run on the current stream after the side stream's work."""
+        inc = getattr(self, "_inc", None)
+        if inc is None:
+            raise RuntimeError("end() without begin()")
+        missing = [b for b, r in enumerate(inc["ready"]) if r is None]
+        if missing:
+            names = [self.specs[i].name for i in self.buckets[missing[0]].params]
+            raise RuntimeError(f"step ended with {len(missing)} bucket(s) never submitted "
+                               f"(first: bucket {missing[0]}, tensors {names[:4]}...)")
+        s0 = torch.cuda.current_stream(self.device)
+        s0.wait_stream(self._side_stream)
+        sh = int(s0.cuda_stream)
+        plan = self.plan
+        mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
+        nb = len(self.buckets)
+        if self.sharded:
+            p, r = self.comm.topo.p, self.comm.rank
+            C = self._own_chunks
+            sig, ebase = dev.ptr(self.arena.peers("sig")), dev.ptr(self.epoch_base)
+            _native.call("gs_peer_fence", sig, r, p, nb + 1, ebase, sh)
+            plan.trust(sh)
+            _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), C[r],
+                         C[r + 1], dev.ptr(plan.params), plan.hint, dev.ptr(plan.seg_scale),
+                         dev.ptr(plan.flags), mask, dev.ptr(self.arena.peers("working")), p, r,
+                         sh)
+            _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
+            _native.call("gs_counter_add", ebase, nb + 3, sh)
+            self._half ^= 1
+        else:
+            plan.finish(sh, True, mask)
+            if self.ordered is not None:
+                self.ordered.advance(nb + 1, sh)
+                self._half ^= 1
+        plan.use_segments(None)
+        self._last_wire = inc["wire"]
+        self._inc = None
+
     def finish(self) -> StepResult:
         """Read the step's flags (the one host sync) and advance LossScale
         exactly as experiment.py:403-413 does."""

@@ -49,11 +49,17 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded").split(",")
-    for algo, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ring", 1), ("hierarchical", 2),
-                    ("sharded", 2)):
-        if algo not in algos:
+    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded,zero_inc,ordered_inc,ring_inc").split(",")
+    for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ring", 1),
+                         ("hierarchical", 2), ("sharded", 2), ("zero_inc", 1), ("ordered_inc", 1),
+                         ("ring_inc", 1)):
+        if algo_name not in algos:
             continue
+        # *_inc: the same step driven through the incremental API the
+        # backward-overlap driver uses (begin / submit per bucket / end),
+        # buckets submitted in REVERSE order to exercise the in-order gating
+        inc = algo_name.endswith("_inc")
+        algo = algo_name[:-4] if inc else algo_name
         if world % k or (algo != "ring" and world == 1):
             continue
         comm = Communicator(gs.Topology(world, k))
@@ -76,7 +82,16 @@ def main():
                      for r in range(world)]
             if step == 2:
                 wires[world - 1][4321] = 0x7C00
-            res = pipe.step(torch.from_numpy(wires[rank]).to(dev), step)
+            flat = torch.from_numpy(wires[rank]).to(dev)
+            if inc:
+                views = split(flat, specs)
+                pipe.begin(step)
+                for b in reversed(range(len(pipe.buckets))):
+                    pipe.submit(b, [views[i] for i in pipe.buckets[b].params])
+                pipe.end()
+                res = pipe.finish()
+            else:
+                res = pipe.step(flat, step)
             reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]
             if algo.startswith("zero"):
                 pipe.gather_state()  # masters/velocities are sharded (ZeRO-1)
@@ -127,7 +142,7 @@ def main():
             if step == 2 and int(flag) != world:
                 ok = False
                 notes.append("injected Inf did not skip on every rank")
-        results[algo] = {"ok": ok, "notes": notes[:5], "k": k}
+        results[algo_name] = {"ok": ok, "notes": notes[:5], "k": k}
     if rank == 0:
         print(json.dumps({"world": world, "model": model, "theta": theta, "results": results}))
     dist.barrier()

@@ -198,3 +198,21 @@ def test_shapes_frozen():
     assert sh.total_params(sh.load_shapes("shufflenet_v2_x0_5")) == 1_366_792
     kinds = [s.kind for s in sh.load_shapes("resnet50")]
     assert kinds.count("weight") == 54 and kinds.count("bias") == 1
+
+
+def test_specs_from_module_kind_map():
+    """overlap.specs_from_module follows the shapes.json kind map:
+    BN weight/bias -> bn_gamma/bn_beta, dim > 1 -> weight, other 1-D -> bias."""
+    import torch
+    from paper_1807_11205_b200.overlap import specs_from_module
+
+    net = torch.nn.Sequential(torch.nn.Conv2d(3, 4, 3), torch.nn.BatchNorm2d(4),
+                              torch.nn.Flatten(), torch.nn.Linear(4, 2))
+    specs = specs_from_module(net)
+    assert [(s.name, s.kind) for s in specs] == [
+        ("0.weight", "weight"), ("0.bias", "bias"), ("1.weight", "bn_gamma"),
+        ("1.bias", "bn_beta"), ("3.weight", "weight"), ("3.bias", "bias")]
+    assert [s.shape for s in specs][0] == (4, 3, 3, 3)
+    # same map as the frozen torchvision shape lists
+    r50 = sh.load_shapes("resnet50")
+    assert sum(s.kind == "bn_gamma" for s in r50) == 53

@@ -72,6 +72,8 @@ def main() -> None:
     if "ordered" in want:
         variants.append(("ordered", 1))
     comms = {k: Communicator(gs.Topology(world, k)) for k in sorted({k for _, k in variants})}
+    # bookkeeping reductions on CPU (gloo): NCCL_ALGO=NVLS runs have no fp64/int path
+    host = dist.new_group(backend="gloo")
 
     # finite binary16 payload (small values: no finite sum overflows), Inf at 0 on rank 0
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
@@ -129,20 +131,23 @@ def main() -> None:
                 refill()
                 half[0] ^= 1
             torch.cuda.synchronize(dev)
-            dist.barrier(device_ids=[local])
+            dist.barrier(group=host)
             run()
             torch.cuda.synchronize(dev)
             r = result()
             inf_ok = bool(torch.isinf(r[0]).item())
             finite_rest = bool(torch.isfinite(r[1:]).all().item()) if nn > 1 else True
-            flag_ok = bool(flag.item() != 0) if algo == "ordered" else None
+            # the ordered kernel flags the slice its rank folded: OR over ranks
+            flag_any = torch.tensor([int(flag.item())], dtype=torch.int64)
+            dist.all_reduce(flag_any, op=dist.ReduceOp.MAX, group=host)
+            flag_ok = bool(flag_any.item() != 0) if algo == "ordered" else None
             # timing: in-place repeats grow the values by ~p per call until they
             # saturate to Inf; binary16 adds cost the same on any value
             iters = 50 if S <= (1 << 20) else (20 if S <= (1 << 26) else 5)
             for _ in range(3):
                 run()
             torch.cuda.synchronize(dev)
-            dist.barrier(device_ids=[local])
+            dist.barrier(group=host)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(s0)
@@ -150,11 +155,11 @@ def main() -> None:
                 run()
             b.record(s0)
             b.synchronize()
-            ms = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64, device=dev)
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            ms = torch.tensor([a.elapsed_time(b) / iters], dtype=torch.float64)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=host)
             ok = torch.tensor([int(inf_ok and finite_rest and flag_ok is not False)],
-                              dtype=torch.int32, device=dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                              dtype=torch.int64)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=host)
             sec = float(ms) * 1e-3
             Sb = 2 * nn
             line = {"bytes": Sb, "variant": name, "p": world, "us": round(sec * 1e6, 2),
@@ -176,7 +181,7 @@ def main() -> None:
         print(json.dumps(summary), flush=True)
         if args.out:
             Path(args.out).write_text("\n".join(json.dumps(x) for x in lines + [summary]) + "\n")
-    dist.barrier()
+    dist.barrier(group=host)
     dist.destroy_process_group()
 
 

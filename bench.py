@@ -403,6 +403,16 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); packing adds
     # 2 (fused into pass 1 at p = 1: the wire write) or 4 (separate packer)
     update_bytes = (26 + (2 if world == 1 else 4)) * n_params
+    roofline = {"bound": "hbm",
+                "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2",
+                "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": pass2_bytes}
+    if args.overflow:
+        # every step is skipped: pass 2 only reads the flag and exits, so its
+        # bandwidth is not a roofline figure
+        roofline["frac"] = None
+        roofline["note"] = "forced-overflow run: pass 2 takes the skip exit"
     line = {
         "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
@@ -423,11 +433,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                    "parallelism": f"dp{world}", "l2": "flushed before every step (256 MiB write, then read: no step data resident, L2 clean)"},
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
-        "roofline": {"bound": "hbm",
-                     "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2", "achieved": round(achieved, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_launch": pass2_bytes},
+        "roofline": roofline,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -455,13 +461,13 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k)]
     comms = {}
     s0 = torch.cuda.current_stream(dev)
-    variants.append(("ordered", 1))
+    variants += [("ordered", 1), ("ordered_push", 1)]
     ow = None
     for name, k in variants:
         if k not in comms:
             comms[k] = Communicator(gs.Topology(world, k))
         comm = comms[k]
-        algo = name.split("_")[0]
+        algo = "ordered" if name.startswith("ordered") else name.split("_")[0]
         n = buf.numel() - buf.numel() % (k * 8)
         t = buf[:n]
         if algo == "ordered":
@@ -469,7 +475,8 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             ow = ow or OrderedWire(comm, pipe.total, dev)
             half = [0]
 
-            def run_ordered(_t=None):
+            def run_ordered(_t=None, _push=name == "ordered_push"):
+                ow.push = _push
                 ow.allreduce(half[0], 0, n, int(s0.cuda_stream))
                 ow.advance(1, int(s0.cuda_stream))
                 half[0] ^= 1

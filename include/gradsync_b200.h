@@ -186,6 +186,15 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
                              const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
                              void* stream);
 
+/* Same contract and result as gs_ordered_allreduce_f16, push form: the
+ * owner of a slice stores the folded slice into every peer's buffer as it
+ * folds (remote stores), then one exit barrier; no gather phase.  The wire
+ * must still be double-buffered across calls. */
+int gs_ordered_allreduce_push_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                                  int64_t offset, int64_t n, uint32_t epoch,
+                                  const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
+                                  void* stream);
+
 /* Reduce-scatter half of the above with explicit slices: rank r folds
  * elements [bounds[r], bounds[r+1]) (device int64 array of p + 1 offsets)
  * of every peer's buffer into its own, in the reference's tree order.  Used

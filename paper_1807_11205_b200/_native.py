@@ -85,6 +85,9 @@ SIGNATURES = {
                                     c_void_p, c_uint32, c_void_p]),
     "gs_ordered_allreduce_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64, c_int64,
                                          c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
+    "gs_ordered_allreduce_push_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64,
+                                              c_int64, c_uint32, c_void_p, c_int, c_void_p,
+                                              c_void_p]),
     "gs_counter_add": (c_int, [c_void_p, c_uint32, c_void_p]),
     "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p,
                                               c_uint32, c_void_p, c_int, c_void_p, c_void_p]),

@@ -40,8 +40,11 @@ __device__ __forceinline__ void subrange(int64_t n, int p, int r, int nb, int b,
   hi = min(s1, lo + sub);
 }
 
-// fold [lo, hi) of every peer's buffer into mine (pairwise tree, P <= 8)
-template <int P>
+// fold [lo, hi) of every peer's buffer into mine (pairwise tree, P <= 8);
+// PUSH: also store every folded vector into every peer's buffer at the same
+// offset (only the slice's owner ever reads or writes those positions, and
+// each thread reads its element from all peers before it overwrites it)
+template <int P, bool PUSH = false>
 __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint16_t* mine, int64_t lo,
                                            int64_t hi, uint32_t& bad) {
   bool vec = gs::is_aligned16(mine + lo);
@@ -78,7 +81,14 @@ __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint
         o[h] = gs::narrow2(tree<P>(a), tree<P>(b));
         bad |= ((o[h] & 0x7C00u) == 0x7C00u) | ((o[h] & 0x7C000000u) == 0x7C000000u);
       }
-      reinterpret_cast<uint4*>(mine + lo)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+      const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+      if (PUSH) {
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+          reinterpret_cast<uint4*>(const_cast<uint16_t*>(src[q]) + lo)[i] = ov;
+      } else {
+        reinterpret_cast<uint4*>(mine + lo)[i] = ov;
+      }
     }
   }
   for (int64_t i = lo + nv * 8 + threadIdx.x; i < hi; i += kThreads) {
@@ -87,7 +97,12 @@ __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint
     for (int q = 0; q < P; ++q) v[q] = gs::widen(__ldcv(src[q] + i));
     const uint16_t o = gs::narrow(tree<P>(v));
     bad |= (o & 0x7C00u) == 0x7C00u;
-    mine[i] = o;
+    if (PUSH) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) const_cast<uint16_t*>(src[q])[i] = o;
+    } else {
+      mine[i] = o;
+    }
   }
 }
 
@@ -147,6 +162,33 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
     subrange(n, P, r, gridDim.x, blockIdx.x, lo, hi);
     copy_range(reinterpret_cast<const uint8_t*>(src[r]), reinterpret_cast<uint8_t*>(mine), 2 * lo, 2 * hi);
   }
+}
+
+// Push form: A entry barrier -> fold my slice and store it into EVERY rank's
+// buffer (remote stores over NVLink, overlapping the next loads) -> exit
+// barrier per block (block b of every peer has pushed its sub-range b; the
+// kernel ends only when all blocks passed, i.e. the whole bucket arrived).
+// Same bytes as the pull form; one barrier and no separate gather phase.
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+ordered_allreduce_push_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                              int rank, int64_t offset, int64_t n, uint32_t epoch,
+                              const uint32_t* __restrict__ epoch_base,
+                              uint32_t* __restrict__ nonfinite) {
+  if (epoch_base != nullptr) epoch += *epoch_base;
+  const uint16_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+  peer_barrier(sig, rank, P, 0, epoch);
+  int64_t lo, hi;
+  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
+  uint32_t bad = 0;
+  fold_range<P, true>(src, mine, lo, hi, bad);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+  __threadfence_system();  // this thread's remote stores, before the release below
+  peer_barrier(sig, rank, P, 1, epoch);
 }
 
 // Reduce-scatter with explicit slice bounds (elements, p + 1 entries):
@@ -238,6 +280,44 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
   }
 #undef GS_OAR
   return gs_check_launch("gs_ordered_allreduce_f16");
+}
+
+int gs_ordered_allreduce_push_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
+                                  int64_t offset, int64_t n, uint32_t epoch,
+                                  const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
+                                  void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allreduce_push_f16: 1 <= p <= 8 (got %d)", p);
+  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allreduce_push_f16: bad rank %d", rank);
+  GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_push_f16: negative size/offset");
+  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allreduce_push_f16: bad block count");
+  GS_REQUIRE(epoch != 0 || epoch_base != nullptr,
+             "gs_ordered_allreduce_push_f16: epoch 0 is the reset value");
+  if (p == 1 || n == 0) return GS_OK;
+  GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_push_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_OARP(P)                                                                                \
+  case P: {                                                                                       \
+    int per_sm = 0, dev = 0, sms = 0;                                                             \
+    cudaGetDevice(&dev);                                                                          \
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_allreduce_push_kernel<P>,      \
+                                                  kThreads, 0);                                   \
+    const int nb = per_sm > 0 ? min(nblocks, per_sm * sms) : 1;                                  \
+    ordered_allreduce_push_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,   \
+                                                             epoch_base, nonfinite);              \
+    break;                                                                                        \
+  }
+  switch (p) {
+    GS_OARP(2)
+    GS_OARP(3)
+    GS_OARP(4)
+    GS_OARP(5)
+    GS_OARP(6)
+    GS_OARP(7)
+    GS_OARP(8)
+  }
+#undef GS_OARP
+  return gs_check_launch("gs_ordered_allreduce_push_f16");
 }
 
 static int coresident_blocks(const void* kernel, int want) {

@@ -198,6 +198,9 @@ class OrderedWire:
         # kernels can be captured into a CUDA graph and replayed
         self.epoch_base = torch.zeros(1, dtype=torch.int32, device=device)
         self.slots = 0
+        # push form (fold + remote stores, one exit barrier) vs pull form
+        # (fold, barrier, gather by remote loads); same result bit for bit
+        self.push = os.environ.get("GS_ORDERED_PUSH", "0") == "1"
         dist.barrier()
 
     def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
@@ -206,7 +209,8 @@ class OrderedWire:
         from . import _device as dev
         from . import _native
 
-        _native.call("gs_ordered_allreduce_f16", dev.ptr(self.bufs_dev[half]),
+        _native.call("gs_ordered_allreduce_push_f16" if self.push else "gs_ordered_allreduce_f16",
+                     dev.ptr(self.bufs_dev[half]),
                      dev.ptr(self.sig_dev), self.rank, self.p, offset, n, slot + 1,
                      dev.ptr(self.epoch_base), self.nblocks, None, stream_h)
 

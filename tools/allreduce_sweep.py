@@ -41,7 +41,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--min-log2", type=int, default=10)
     ap.add_argument("--max-log2", type=int, default=30)
-    ap.add_argument("--variants", default="ring,hierarchical,sharded,ordered")
+    ap.add_argument("--variants", default="ring,hierarchical,sharded,ordered,ordered_push")
     ap.add_argument("--out", default=None, help="also write the lines to this file (rank 0)")
     args = ap.parse_args()
 
@@ -71,6 +71,8 @@ def main() -> None:
                 variants.append((f"sharded_{world // k}x{k}", k))
     if "ordered" in want:
         variants.append(("ordered", 1))
+    if "ordered_push" in want:
+        variants.append(("ordered_push", 1))
     comms = {k: Communicator(gs.Topology(world, k)) for k in sorted({k for _, k in variants})}
     # bookkeeping reductions on CPU (gloo): NCCL_ALGO=NVLS runs have no fp64/int path
     host = dist.new_group(backend="gloo")
@@ -79,7 +81,8 @@ def main() -> None:
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     base = (torch.rand(max_elems, generator=g) * 2e-3 - 1e-3).to(torch.float16).to(dev)
     buf = torch.empty_like(base)
-    ow = OrderedWire(comms[1], max_elems, dev) if ("ordered", 1) in variants else None
+    ow = OrderedWire(comms[1], max_elems, dev) if any(v[0].startswith("ordered") for v in variants) \
+        else None
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     half = [0]
     lines = []
@@ -88,7 +91,9 @@ def main() -> None:
         n = S // 2
         for name, k in variants:
             comm = comms[k]
-            algo = name.split("_")[0]
+            algo = "ordered" if name.startswith("ordered") else name.split("_")[0]
+            fn = "gs_ordered_allreduce_push_f16" if name == "ordered_push" else \
+                "gs_ordered_allreduce_f16"
             nn = n - n % k if algo == "sharded" else n
             if nn == 0:
                 continue
@@ -99,8 +104,8 @@ def main() -> None:
                     if rank == 0:
                         h[:1].view(torch.int16).fill_(0x7C00)
 
-                def run():
-                    _native.call("gs_ordered_allreduce_f16", dv.ptr(ow.bufs_dev[half[0]]),
+                def run(_fn=fn):
+                    _native.call(_fn, dv.ptr(ow.bufs_dev[half[0]]),
                                  dv.ptr(ow.sig_dev), ow.rank, ow.p, 0, nn, 1,
                                  dv.ptr(ow.epoch_base), ow.nblocks, dv.ptr(flag),
                                  int(s0.cuda_stream))

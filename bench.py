@@ -348,7 +348,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # over this rank's owned elements only); its achieved bandwidth is taken
     # per rank and the slowest rank reported
     p2_name = "pass2_push" if "pass2_push" in phase_ms else "pass2"
-    p2_elems = (pipe.owned[1] - pipe.owned[0]) if pipe.sharded else n_params
+    p2_elems = pipe.owned_elems if pipe.sharded else n_params
     p2_ms_local = statistics.median(phase_ms[p2_name])
     t = torch.tensor([mean_ms, -20.0 * p2_elems / (p2_ms_local * 1e-3) / 1e9],
                      dtype=torch.float64, device=dev)

@@ -234,14 +234,15 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
                 const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
                 int nblocks, void* stream);
 
-/* LARS pass 2 over chunks [c0, c1) (binary16 gradients) that also stores each
+/* LARS pass 2 over chunks [c0, c1) (binary16 gradients; with a non-null
+ * chunk_list, over chunks chunk_list[c0 .. c1-1]) that also stores each
  * updated binary16 working weight into every peer's working arena
  * (peer_working[q] = peer q's base; the segments' w16 lie in
  * peer_working[rank]).  Replaces gs_lars_pass2 + the all-gather of the
  * working weights (lars.py:178-181).  Launched as a programmatic dependent of
  * gs_lars_trust. */
 int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                  const gs_step_params* params, uint32_t hint, const float* seg_scale,
+                  const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const float* seg_scale,
                   const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
                   int rank, void* stream);
 

@@ -96,7 +96,8 @@ SIGNATURES = {
     "gs_rs_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                             c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
                             c_void_p]),
-    "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_uint32, c_void_p,
+    "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32,
+                              c_void_p,
                               c_void_p, c_uint32, c_void_p, c_int, c_int, c_void_p]),
     "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_uint32, c_void_p, c_void_p]),
 }

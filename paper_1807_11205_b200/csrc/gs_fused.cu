@@ -161,9 +161,9 @@ __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, fl
                    gs::is_aligned16(w16);
   const int nv = vec ? len / 8 : 0;
   const int t = threadIdx.x;
-  for (int i = t; i < nv; i += kThreads) {
-    const uint4 gv = Gt::ld(g + 8 * i);
-    const F8 wv = ld8(w, i), vv = ld8(v, i);
+  // one 8-element vector: update in registers, local v/w streaming stores,
+  // binary16 result stored into every rank's working arena (own included)
+  auto one = [&](const uint4& gv, const F8& wv, const F8& vv, int i) {
     float2 ww[4] = {make_float2(wv.a.x, wv.a.y), make_float2(wv.a.z, wv.a.w),
                     make_float2(wv.b.x, wv.b.y), make_float2(wv.b.z, wv.b.w)};
     float2 xv[4] = {make_float2(vv.a.x, vv.a.y), make_float2(vv.a.z, vv.a.w),
@@ -179,7 +179,19 @@ __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, fl
     const uint4 h = make_uint4(pack_w16(ww[0]), pack_w16(ww[1]), pack_w16(ww[2]), pack_w16(ww[3]));
     for (int q = 0; q < p; ++q)
       reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(peer_working[q]) + woff)[i] = h;
+  };
+  // batches of two vectors per thread with every load issued first (the
+  // stores cannot alias the next batch's loads, which the compiler cannot
+  // prove through the casts) -- the same batching as lars_pass2
+  int done = 0;
+  for (; done + 2 * kThreads <= nv; done += 2 * kThreads) {
+    const int i0 = done + t, i1 = i0 + kThreads;
+    const uint4 g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
+    const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
+    one(g0, w0, v0, i0);
+    one(g1, w1, v1, i1);
   }
+  for (int i = done + t; i < nv; i += kThreads) one(Gt::ld(g + 8 * i), ld8(w, i), ld8(v, i), i);
   for (int i = nv * 8 + t; i < len; i += kThreads) {
     float2 ww = make_float2(w[i], 0.0f), vv = make_float2(v[i], 0.0f);
     p2_pair<POW2, DECAY>(make_float2(Gt::one(g + i), 0.0f), ww, vv, cx, s);
@@ -194,12 +206,12 @@ __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, fl
 template <bool POW2>
 __global__ void __launch_bounds__(kThreads, 4)
 pass2_push_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
-                  const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
+                  const int32_t* __restrict__ chunk_list, const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
                   const uint32_t* __restrict__ flags, uint32_t flag_mask,
                   const uint64_t* __restrict__ peer_working, int p, int rank) {
   gs::griddep_wait();  // the trust kernel's scales (PDL launch)
   if (*flags & flag_mask) return;  // lars.py:161-163
-  const int c = c0 + blockIdx.x;
+  const int c = chunk_list != nullptr ? chunk_list[c0 + blockIdx.x] : c0 + blockIdx.x;
   const gs_chunk ch = chunks[c];
   const gs_segment* sp = segs + ch.seg;
   const uint32_t sflags = sp->flags;
@@ -280,7 +292,7 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
 }
 
 int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                  const gs_step_params* params, uint32_t hint, const float* seg_scale,
+                  const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const float* seg_scale,
                   const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
                   int rank, void* stream) {
   GS_REQUIRE(c0 >= 0 && c1 >= c0 && p >= 1 && rank >= 0 && rank < p, "gs_pass2_push: bad arguments");
@@ -291,10 +303,10 @@ int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1
   cudaError_t e;
   if (hint & GS_HINT_POW2)
     e = gs_launch_pdl(pass2_push_kernel<true>, dim3(c1 - c0), dim3(kThreads), 0, s, segs, chunks, c0,
-                      params, seg_scale, flags, flag_mask, peer_working, p, rank);
+                      chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank);
   else
     e = gs_launch_pdl(pass2_push_kernel<false>, dim3(c1 - c0), dim3(kThreads), 0, s, segs, chunks,
-                      c0, params, seg_scale, flags, flag_mask, peer_working, p, rank);
+                      c0, chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank);
   if (e != cudaSuccess) {
     gs_set_error("gs_pass2_push: %s", cudaGetErrorString(e));
     return GS_ECUDA;

@@ -280,26 +280,39 @@ class GradientPipeline:
         self.master = a.view("master", torch.float32)
         self.velocity = a.view("velocity", torch.float32)
         self.working = a.view("working", torch.uint16)
-        # ownership: rank r owns chunks [C_r, C_r+1) (balanced by elements, in
-        # wire order) = wire/arena elements [E_r, E_r+1)
+        # ownership, PER BUCKET: rank r owns chunks [C_b[r], C_b[r+1]) of bucket
+        # b (balanced by elements, in wire order) = wire elements [E_b[r],
+        # E_b[r+1]); every bucket's fold is spread over all ranks, so the
+        # bucket pipeline never waits on one rank's share
         abs_start = np.array([self.wire_off[int(c["seg"])] + int(c["start"]) for c in chunks],
                              dtype=np.int64)
-        C = [0] + [int(np.searchsorted(abs_start, r * self.total // p)) for r in range(1, p)] \
-            + [nchunk]
-        E = [0] + [int(abs_start[c]) if c < nchunk else self.total for c in C[1:p]] + [self.total]
-        self._own_chunks, self._own_elems = C, E
+        clen = np.array([int(c["len"]) for c in chunks], dtype=np.int64)
         r = comm.rank
-        self.owned = (E[r], E[r + 1])
-        self._rs_bounds = []
-        self._own_bucket_chunks = []
+        self._own_bucket = []       # (c0, c1) of this rank per bucket
+        self._bucket_C, self._bucket_E = [], []
+        self._rs_bounds, self._part_bounds, self._w16_bounds, self._m_bounds = [], [], [], []
+        own_list = []
         for bk in self.buckets:
-            bs, be = bk.start, bk.start + bk.padded
-            bounds = np.clip(np.array(E, dtype=np.int64), bs, be)
-            bounds[0], bounds[-1] = bs, be
-            self._rs_bounds.append(dev.upload(bounds, d))
-        self._part_bounds = dev.upload(np.array([24 * c for c in C], dtype=np.int64), d)
-        self._w16_bounds = dev.upload(np.array([2 * e for e in E], dtype=np.int64), d)
-        self._m_bounds = dev.upload(np.array([4 * e for e in E], dtype=np.int64), d)
+            cb0, cb1 = bk.chunk0, bk.chunk0 + bk.nchunk
+            C = [cb0]
+            for q in range(1, p):
+                target = bk.start + q * bk.length // p
+                C.append(cb0 + int(np.searchsorted(abs_start[cb0:cb1], target)))
+            C.append(cb1)
+            E = [bk.start] + [int(abs_start[c]) if c < cb1 else bk.start + bk.padded
+                              for c in C[1:p]] + [bk.start + bk.padded]
+            self._bucket_C.append(C)
+            self._bucket_E.append(E)
+            self._own_bucket.append((C[r], C[r + 1]))
+            own_list.extend(range(C[r], C[r + 1]))
+            self._rs_bounds.append(dev.upload(np.array(E, dtype=np.int64), d))
+            self._part_bounds.append(dev.upload(np.array([24 * c for c in C], dtype=np.int64), d))
+            self._w16_bounds.append(dev.upload(np.array([2 * e for e in E], dtype=np.int64), d))
+            self._m_bounds.append(dev.upload(np.array([4 * e for e in E], dtype=np.int64), d))
+        self._own_list = dev.upload(np.array(own_list or [0], dtype=np.int32), d)
+        self._n_own = len(own_list)
+        #: elements this rank updates (pass 2) per step
+        self.owned_elems = int(clen[own_list].sum()) if own_list else 0
         self.epoch_base = torch.zeros(1, dtype=torch.int32, device=d)
         self._ps_events = None
 
@@ -311,11 +324,13 @@ class GradientPipeline:
             return
         sh = int(torch.cuda.current_stream(self.device).cuda_stream)
         p, r = self.comm.topo.p, self.comm.rank
+        nb = len(self.buckets)
         for name in ("master", "velocity"):
-            _native.call("gs_ordered_allgather", dev.ptr(self.arena.peers(name)),
-                         dev.ptr(self.arena.peers("sig")), r, p, dev.ptr(self._m_bounds), 1,
-                         dev.ptr(self.epoch_base), self._nblocks, sh)
-            _native.call("gs_counter_add", dev.ptr(self.epoch_base), 1, sh)
+            for b in range(nb):
+                _native.call("gs_ordered_allgather", dev.ptr(self.arena.peers(name)),
+                             dev.ptr(self.arena.peers("sig")), r, p, dev.ptr(self._m_bounds[b]),
+                             b + 1, dev.ptr(self.epoch_base), self._nblocks, sh)
+            _native.call("gs_counter_add", dev.ptr(self.epoch_base), nb, sh)
 
     def _launch_sharded(self, tabs, s0, timer) -> None:
         """reduce-scatter (own slice, reference tree order) -> pass 1 on own
@@ -330,7 +345,6 @@ class GradientPipeline:
         wb = wire.data_ptr()
         plan.use_segments(plan.alt_segments([wb + 2 * o for o in self.wire_off]))
         plan.reset_flags(sh)
-        C = self._own_chunks
         sig, ebase = dev.ptr(a.peers("sig")), dev.ptr(self.epoch_base)
         wires = a.peers("wireA" if half == 0 else "wireB")
         ps = self._pack_stream
@@ -355,8 +369,7 @@ class GradientPipeline:
                 timer(f"rs{b}")
             _native.call("gs_ordered_reduce_scatter_f16", dev.ptr(wires), sig, r, p,
                          dev.ptr(self._rs_bounds[b]), b + 1, ebase, self._nblocks, None, sh)
-            c0 = max(bk.chunk0, C[r])
-            c1 = min(bk.chunk0 + bk.nchunk, C[r + 1])
+            c0, c1 = self._own_bucket[b]
             if timer:
                 timer(f"pass1_{b}")
             if c1 > c0:
@@ -364,21 +377,25 @@ class GradientPipeline:
         s0.wait_stream(ps)
         if timer:
             timer("gather_partials")
-        _native.call("gs_ordered_allgather", dev.ptr(a.peers("partials")), sig, r, p,
-                     dev.ptr(self._part_bounds), nb + 1, ebase, self._nblocks, sh)
+        for b in range(nb):
+            _native.call("gs_ordered_allgather", dev.ptr(a.peers("partials")), sig, r, p,
+                         dev.ptr(self._part_bounds[b]), nb + 1 + b, ebase, self._nblocks, sh)
         if timer:
             timer("trust")
         plan.trust(sh, peer_flags=a.peers("flags"), npeers=p)
         if timer:
             timer("pass2")
         mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
-        if C[r + 1] > C[r]:
-            plan.pass2(sh, g_is_f16=True, flag_mask=mask, chunk0=C[r], nchunk=C[r + 1] - C[r])
+        for b in range(nb):
+            c0, c1 = self._own_bucket[b]
+            if c1 > c0:
+                plan.pass2(sh, g_is_f16=True, flag_mask=mask, chunk0=c0, nchunk=c1 - c0)
         if timer:
             timer("gather_w16")
-        _native.call("gs_ordered_allgather", dev.ptr(a.peers("working")), sig, r, p,
-                     dev.ptr(self._w16_bounds), nb + 2, ebase, self._nblocks, sh)
-        _native.call("gs_counter_add", ebase, nb + 3, sh)
+        for b in range(nb):
+            _native.call("gs_ordered_allgather", dev.ptr(a.peers("working")), sig, r, p,
+                         dev.ptr(self._w16_bounds[b]), 2 * nb + 1 + b, ebase, self._nblocks, sh)
+        _native.call("gs_counter_add", ebase, 3 * nb + 1, sh)
         plan.use_segments(None)
         self._last_wire = wire
         self._half ^= 1
@@ -392,15 +409,13 @@ class GradientPipeline:
         push to every peer), and a closing fence."""
         plan, a = self.plan, self.arena
         p, r = self.comm.topo.p, self.comm.rank
-        C = self._own_chunks
         nb = len(self.buckets)
         parts, flags = dev.ptr(a.peers("partials")), dev.ptr(a.peers("flags"))
         for b, bk in enumerate(self.buckets):
             s0.wait_event(evs[b])
             if timer:
                 timer(f"rs_pass1_{b}")
-            c0 = max(bk.chunk0, C[r])
-            c1 = max(c0, min(bk.chunk0 + bk.nchunk, C[r + 1]))
+            c0, c1 = self._own_bucket[b]
             _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
                          dev.ptr(plan.d_chunks), c0, c1, dev.ptr(plan.params), plan.hint,
                          parts, flags, b + 1, ebase, self._nblocks, sh)
@@ -414,9 +429,10 @@ class GradientPipeline:
         if timer:
             timer("pass2_push")
         mask = _native.FLAG_SCALED_NONFINITE | _native.FLAG_GRAD_NONFINITE
-        _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), C[r],
-                     C[r + 1], dev.ptr(plan.params), plan.hint, dev.ptr(plan.seg_scale),
-                     dev.ptr(plan.flags), mask, dev.ptr(a.peers("working")), p, r, sh)
+        _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), 0,
+                     self._n_own, dev.ptr(self._own_list), dev.ptr(plan.params), plan.hint,
+                     dev.ptr(plan.seg_scale), dev.ptr(plan.flags), mask,
+                     dev.ptr(a.peers("working")), p, r, sh)
         if timer:
             timer("fence_end")
         _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
@@ -853,9 +869,7 @@ class GradientPipeline:
                 _native.call("gs_batched_copy", dev.ptr(tab[0]), tab[1], sh)
             if self.sharded:
                 p, r = self.comm.topo.p, self.comm.rank
-                C = self._own_chunks
-                c0 = max(bk.chunk0, C[r])
-                c1 = max(c0, min(bk.chunk0 + bk.nchunk, C[r + 1]))
+                c0, c1 = self._own_bucket[b]
                 wires = self.arena.peers("wireA" if inc["half"] == 0 else "wireB")
                 _native.call("gs_rs_pass1", dev.ptr(wires), dev.ptr(self.arena.peers("sig")), r,
                              p, dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), c0, c1,
@@ -889,14 +903,13 @@ class GradientPipeline:
         nb = len(self.buckets)
         if self.sharded:
             p, r = self.comm.topo.p, self.comm.rank
-            C = self._own_chunks
             sig, ebase = dev.ptr(self.arena.peers("sig")), dev.ptr(self.epoch_base)
             _native.call("gs_peer_fence", sig, r, p, nb + 1, ebase, sh)
             plan.trust(sh)
-            _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), C[r],
-                         C[r + 1], dev.ptr(plan.params), plan.hint, dev.ptr(plan.seg_scale),
-                         dev.ptr(plan.flags), mask, dev.ptr(self.arena.peers("working")), p, r,
-                         sh)
+            _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), 0,
+                         self._n_own, dev.ptr(self._own_list), dev.ptr(plan.params), plan.hint,
+                         dev.ptr(plan.seg_scale), dev.ptr(plan.flags), mask,
+                         dev.ptr(self.arena.peers("working")), p, r, sh)
             _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
             _native.call("gs_counter_add", ebase, nb + 3, sh)
             self._half ^= 1

@@ -40,7 +40,7 @@ from .halfprec import LossScale
 from .lars import LarsConfig, ParamGroup, segment_flags
 
 __all__ = ["ParamSpec", "Bucket", "GradientPipeline", "StepResult", "BUCKET_ALIGN",
-           "plan_layout"]
+           "plan_layout", "shard_buckets"]
 
 #: wire-buffer granularity (elements): bucket starts are 512-byte aligned and
 #: padded lengths are multiples of 256 so any k <= 8 shards 16-byte aligned
@@ -109,6 +109,26 @@ def plan_layout(specs, order, threshold_bytes: int):
         off = start + max(BUCKET_ALIGN, _roundup(length, BUCKET_ALIGN))
         buckets.append(Bucket(start, length, off - start, idxs, tuple(umap)))
     return wire_off, buckets, max(off, BUCKET_ALIGN)
+
+
+def shard_buckets(buckets, chunk_abs_start, p: int):
+    """Per-bucket ownership of the sharded update: for bucket b, rank r owns
+    chunks [C_b[r], C_b[r+1]) = wire elements [E_b[r], E_b[r+1]), split at
+    chunk starts so each rank gets ~length/p elements; E_b spans the padded
+    bucket (the zero slack goes to the last owner).  Returns (C, E) lists."""
+    Cs, Es = [], []
+    for bk in buckets:
+        cb0, cb1 = bk.chunk0, bk.chunk0 + bk.nchunk
+        C = [cb0]
+        for q in range(1, p):
+            target = bk.start + q * bk.length // p
+            C.append(cb0 + int(np.searchsorted(chunk_abs_start[cb0:cb1], target)))
+        C.append(cb1)
+        E = [bk.start] + [int(chunk_abs_start[c]) if c < cb1 else bk.start + bk.padded
+                          for c in C[1:p]] + [bk.start + bk.padded]
+        Cs.append(C)
+        Es.append(E)
+    return Cs, Es
 
 
 class GradientPipeline:
@@ -234,6 +254,8 @@ class GradientPipeline:
                 assert int(begin[b.params[0]]) == c or sizes[b.params[0]] == 0
             c += b.nchunk
         assert c == self.plan.nchunk
+        if self.sharded:
+            self._init_ownership(d)
 
         self._pack_cache: dict = {}
         self.use_graph = use_graph
@@ -280,6 +302,14 @@ class GradientPipeline:
         self.master = a.view("master", torch.float32)
         self.velocity = a.view("velocity", torch.float32)
         self.working = a.view("working", torch.uint16)
+        self.epoch_base = torch.zeros(1, dtype=torch.int32, device=d)
+        self._ps_events = None
+
+    def _init_ownership(self, d) -> None:
+        """Sharded update: which chunks this rank folds and updates (needs
+        the buckets' chunk ranges, i.e. runs after the LARS plan is built)."""
+        p = self.comm.topo.p
+        chunks = self._host_chunks
         # ownership, PER BUCKET: rank r owns chunks [C_b[r], C_b[r+1]) of bucket
         # b (balanced by elements, in wire order) = wire elements [E_b[r],
         # E_b[r+1]); every bucket's fold is spread over all ranks, so the
@@ -287,23 +317,12 @@ class GradientPipeline:
         abs_start = np.array([self.wire_off[int(c["seg"])] + int(c["start"]) for c in chunks],
                              dtype=np.int64)
         clen = np.array([int(c["len"]) for c in chunks], dtype=np.int64)
-        r = comm.rank
-        self._own_bucket = []       # (c0, c1) of this rank per bucket
-        self._bucket_C, self._bucket_E = [], []
+        r = self.comm.rank
+        self._bucket_C, self._bucket_E = shard_buckets(self.buckets, abs_start, p)
+        self._own_bucket = [(C[r], C[r + 1]) for C in self._bucket_C]
         self._rs_bounds, self._part_bounds, self._w16_bounds, self._m_bounds = [], [], [], []
         own_list = []
-        for bk in self.buckets:
-            cb0, cb1 = bk.chunk0, bk.chunk0 + bk.nchunk
-            C = [cb0]
-            for q in range(1, p):
-                target = bk.start + q * bk.length // p
-                C.append(cb0 + int(np.searchsorted(abs_start[cb0:cb1], target)))
-            C.append(cb1)
-            E = [bk.start] + [int(abs_start[c]) if c < cb1 else bk.start + bk.padded
-                              for c in C[1:p]] + [bk.start + bk.padded]
-            self._bucket_C.append(C)
-            self._bucket_E.append(E)
-            self._own_bucket.append((C[r], C[r + 1]))
+        for C, E in zip(self._bucket_C, self._bucket_E):
             own_list.extend(range(C[r], C[r + 1]))
             self._rs_bounds.append(dev.upload(np.array(E, dtype=np.int64), d))
             self._part_bounds.append(dev.upload(np.array([24 * c for c in C], dtype=np.int64), d))
@@ -313,8 +332,6 @@ class GradientPipeline:
         self._n_own = len(own_list)
         #: elements this rank updates (pass 2) per step
         self.owned_elems = int(clen[own_list].sum()) if own_list else 0
-        self.epoch_base = torch.zeros(1, dtype=torch.int32, device=d)
-        self._ps_events = None
 
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank (for

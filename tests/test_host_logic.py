@@ -216,3 +216,37 @@ def test_specs_from_module_kind_map():
     # same map as the frozen torchvision shape lists
     r50 = sh.load_shapes("resnet50")
     assert sum(s.kind == "bn_gamma" for s in r50) == 53
+
+
+@pytest.mark.parametrize("model,theta,p", [("resnet50", 16 << 20, 2), ("resnet50", 256 << 10, 4),
+                                           ("alexnet", 4 << 20, 8),
+                                           ("shufflenet_v2_x0_5", 256 << 10, 8)])
+def test_shard_buckets_cover_every_chunk_once(model, theta, p):
+    """Sharded-update ownership (pipeline.shard_buckets): per bucket the p
+    chunk ranges tile the bucket's chunks, the element bounds tile the padded
+    bucket and agree with the chunk starts, and the split is balanced to
+    within one chunk."""
+    from paper_1807_11205_b200.pipeline import shard_buckets
+    specs = sh.load_shapes(model)
+    order = list(reversed(range(len(specs))))
+    wire_off, buckets, _ = plan_layout(specs, order, theta)
+    chunks, begin, count = build_chunks([s.numel for s in specs], order)
+    c = 0
+    for bk in buckets:
+        bk.chunk0, bk.nchunk = c, int(sum(int(count[i]) for i in bk.params))
+        c += bk.nchunk
+    abs_start = np.array([wire_off[int(x["seg"])] + int(x["start"]) for x in chunks])
+    Cs, Es = shard_buckets(buckets, abs_start, p)
+    owned = np.zeros(len(chunks), dtype=int)
+    for bk, C, E in zip(buckets, Cs, Es):
+        assert C[0] == bk.chunk0 and C[-1] == bk.chunk0 + bk.nchunk and C == sorted(C)
+        assert E[0] == bk.start and E[-1] == bk.start + bk.padded and E == sorted(E)
+        for q in range(p):
+            owned[C[q]:C[q + 1]] += 1
+            if C[q] < C[q + 1]:
+                assert E[q] == abs_start[C[q]]
+                last = C[q + 1] - 1
+                assert abs_start[last] + int(chunks[last]["len"]) <= E[q + 1]
+            share = sum(int(chunks[k]["len"]) for k in range(C[q], C[q + 1]))
+            assert share <= bk.length // p + 8192 + 1
+    assert (owned == 1).all()

@@ -22,9 +22,11 @@
 
 namespace {
 
-// vectors per thread in flight per batch (P raw loads each)
+// vectors per thread in flight per batch (P raw loads each); one vector
+// keeps P = 2 / 4 / 8 at 75 / 92 / 118 registers, i.e. 3 / 2 / 2 co-resident
+// CTAs per SM (two vectors: 124-206 registers, 1-2 CTAs per SM)
 template <int P>
-constexpr int kU = P >= 8 ? 1 : 2;
+constexpr int kU = 1;
 
 template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
 __device__ __forceinline__ void rs_p1_chunk(const uint16_t* const (&src)[P], uint16_t* mine,
@@ -85,8 +87,14 @@ __device__ __forceinline__ void rs_p1_chunk(const uint16_t* const (&src)[P], uin
   }
 }
 
+// residency: every CTA waits for its peers at entry, so the whole grid must
+// fit at once; more CTAs per SM hide NVLink load latency behind other CTAs'
+// fp64 work (unbounded, P = 4 took 206 registers = 1 CTA per SM)
+template <int P>
+constexpr int kRsMinBlocks = P <= 2 ? 3 : 2;
+
 template <int P, bool POW2, bool RAWFLAG, bool GNORM>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kRsMinBlocks<P>)
 rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__ sig, int rank,
                 const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
                 int c1, const gs_step_params* __restrict__ params,

@@ -110,6 +110,9 @@ typedef struct gs_step_params {
 #define GS_HINT_RAWFLAG 2u    /* fp16 input, GS_HINT_POW2 and mul <= 1: a value is
                                  non-finite iff its binary16 exponent is all ones */
 #define GS_HINT_GRADNORM 4u   /* must equal (params->mode & GS_MODE_GRADNORM) != 0 */
+#define GS_HINT_RS_DIRECT 16u /* gs_rs_pass1: register loads per vector instead of
+                                 staging a chunk's peer vectors in shared memory
+                                 with cp.async (all of them in flight at once) */
 #define GS_HINT_NO_BULK 8u    /* fp16 pass 1: use the register-staged kernel instead of
                                  the TMA (cp.async.bulk) pipelined persistent kernel */
 

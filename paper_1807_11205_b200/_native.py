@@ -35,6 +35,7 @@ HINT_POW2 = 1
 HINT_RAWFLAG = 2
 HINT_GRADNORM = 4
 HINT_NO_BULK = 8
+HINT_RS_DIRECT = 16
 
 # numpy mirrors of the device structs (layout asserted against the header)
 SEGMENT_DTYPE = np.dtype([

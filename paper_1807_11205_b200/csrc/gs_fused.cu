@@ -87,13 +87,109 @@ __device__ __forceinline__ void rs_p1_chunk(const uint16_t* const (&src)[P], uin
   }
 }
 
+// cp.async (LDGSTS) 16-byte copy global -> shared, L2 only (peer addresses are
+// plain global addresses mapped over NVLink)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// vectors of a full chunk per thread (8192 / 256 / 8)
+constexpr int kChunkIters = kFullChunk / (kThreads * 8);
+
+// shared-memory staging of one chunk: [iter][source q = 0..P-1, w lo, w hi][thread]
+template <int P>
+constexpr int kStageBytes = kChunkIters * (P + 2) * kThreads * 16;
+
+// The staged form of rs_p1_chunk: every thread issues ALL its vectors' peer
+// loads (and master loads) for the chunk as cp.async copies into its own
+// shared-memory slots at once, waits for its own copies only (no CTA
+// barrier: a thread reads back nothing but what it staged), then folds and
+// runs pass 1 in the same per-thread vector order as rs_p1_chunk — so the
+// results are bit-identical; only the memory-level parallelism changes
+// (P x 4 x 16 B per thread in flight instead of P x 16 B).
+template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+__device__ __forceinline__ void rs_p1_chunk_staged(const uint16_t* const (&src)[P], uint16_t* mine,
+                                                   const float* __restrict__ w, int len,
+                                                   const Ctx& cx, Acc& a, uint4* stage) {
+  bool vec = gs::is_aligned16(mine) && (!LARS || gs::is_aligned16(w)) && len <= kFullChunk;
+#pragma unroll
+  for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q]);
+  if (!vec) {
+    rs_p1_chunk<P, POW2, RAWFLAG, GNORM, LARS, DECAY>(src, mine, w, len, cx, a);
+    return;
+  }
+  const int nv = len / 8;
+  const int t = threadIdx.x;
+  auto slot = [&](int it, int q) -> uint4* { return stage + (it * (P + 2) + q) * kThreads + t; };
+#pragma unroll
+  for (int it = 0; it < kChunkIters; ++it) {
+    const int i = t + it * kThreads;
+    if (i < nv) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) cp_async16(slot(it, q), reinterpret_cast<const uint4*>(src[q]) + i);
+      if (LARS) {
+        cp_async16(slot(it, P), reinterpret_cast<const uint4*>(w + 8 * i));
+        cp_async16(slot(it, P + 1), reinterpret_cast<const uint4*>(w + 8 * i) + 1);
+      }
+    }
+  }
+  cp_async_wait_all();
+#pragma unroll 1
+  for (int it = 0; it < kChunkIters; ++it) {
+    const int i = t + it * kThreads;
+    if (i >= nv) break;
+    uint4 o;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      float x[P], y[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const float2 f = gs::widen2((&slot(it, q)->x)[h]);
+        x[q] = f.x;
+        y[q] = f.y;
+      }
+      (&o.x)[h] = gs::narrow2(tree<P>(x), tree<P>(y));
+    }
+    reinterpret_cast<uint4*>(mine)[i] = o;
+    F8 wv{};
+    if (LARS) {
+      const uint4 lo = *slot(it, P), hi = *slot(it, P + 1);
+      wv.a = make_float4(__uint_as_float(lo.x), __uint_as_float(lo.y), __uint_as_float(lo.z),
+                         __uint_as_float(lo.w));
+      wv.b = make_float4(__uint_as_float(hi.x), __uint_as_float(hi.y), __uint_as_float(hi.z),
+                         __uint_as_float(hi.w));
+    }
+    p1_vec<true, POW2, RAWFLAG, GNORM, LARS, DECAY>(o, wv, cx, a);
+  }
+  // scalar tail (len not a multiple of 8): the direct path's loop
+  for (int i = nv * 8 + t; i < len; i += kThreads) {
+    float v[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = gs::widen(__ldcv(src[q] + i));
+    const uint16_t h = gs::narrow(tree<P>(v));
+    mine[i] = h;
+    if (RAWFLAG) a.raw |= raw_nonfinite_bits(h);
+    Acc b;
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(make_float2(gs::widen(h), 0.0f),
+                                               make_float2(LARS ? w[i] : 0.0f, 0.0f), cx, b);
+    a.sw += b.sw;
+    a.se += b.se;
+    a.sg += b.sg;
+    a.fl |= b.fl;
+  }
+}
+
 // residency: every CTA waits for its peers at entry, so the whole grid must
 // fit at once; more CTAs per SM hide NVLink load latency behind other CTAs'
 // fp64 work (unbounded, P = 4 took 206 registers = 1 CTA per SM)
 template <int P>
 constexpr int kRsMinBlocks = P <= 2 ? 3 : 2;
 
-template <int P, bool POW2, bool RAWFLAG, bool GNORM>
+template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool STAGE>
 __global__ void __launch_bounds__(kThreads, kRsMinBlocks<P>)
 rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__ sig, int rank,
                 const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
@@ -121,12 +217,21 @@ rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__
     const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
     const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
     Acc a;
-    if (lars && decay)
+    if (STAGE) {
+      extern __shared__ uint4 stage[];
+      if (lars && decay)
+        rs_p1_chunk_staged<P, POW2, RAWFLAG, GNORM, true, true>(src, mine, w, ch.len, cx, a, stage);
+      else if (lars)
+        rs_p1_chunk_staged<P, POW2, RAWFLAG, GNORM, true, false>(src, mine, w, ch.len, cx, a, stage);
+      else
+        rs_p1_chunk_staged<P, POW2, RAWFLAG, GNORM, false, false>(src, mine, w, ch.len, cx, a, stage);
+    } else if (lars && decay) {
       rs_p1_chunk<P, POW2, RAWFLAG, GNORM, true, true>(src, mine, w, ch.len, cx, a);
-    else if (lars)
+    } else if (lars) {
       rs_p1_chunk<P, POW2, RAWFLAG, GNORM, true, false>(src, mine, w, ch.len, cx, a);
-    else
+    } else {
       rs_p1_chunk<P, POW2, RAWFLAG, GNORM, false, false>(src, mine, w, ch.len, cx, a);
+    }
     if (lars && !decay) {
       a.se = a.sg;
       if (!GNORM) a.sg = 0.0;
@@ -265,7 +370,7 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
              "gs_rs_pass1: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const bool pow2 = hint & GS_HINT_POW2, raw = pow2 && (hint & GS_HINT_RAWFLAG),
-             gnorm = hint & GS_HINT_GRADNORM;
+             gnorm = hint & GS_HINT_GRADNORM, stage = !(hint & GS_HINT_RS_DIRECT);
   // every CTA waits for its peers at entry: the grid must be co-resident
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -273,12 +378,20 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
   int nb = nblocks;
 #define GS_RSP(P, PW, RW, GN)                                                                     \
   {                                                                                               \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rs_pass1_kernel<P, PW, RW, GN>,        \
-                                                  kThreads, 0);                                   \
-    nb = min(nblocks, max(1, per_sm * sms));                                                      \
-    rs_pass1_kernel<P, PW, RW, GN><<<nb, kThreads, 0, s>>>(wires, sig, rank, segs, chunks, c0, c1, \
-                                                          params, peer_partials, peer_flags,      \
-                                                          epoch, epoch_base);                     \
+    if (stage) {                                                                                  \
+      auto k = rs_pass1_kernel<P, PW, RW, GN, true>;                                              \
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes<P>);       \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kStageBytes<P>);        \
+      nb = min(nblocks, max(1, per_sm * sms));                                                    \
+      k<<<nb, kThreads, kStageBytes<P>, s>>>(wires, sig, rank, segs, chunks, c0, c1, params,      \
+                                             peer_partials, peer_flags, epoch, epoch_base);       \
+    } else {                                                                                      \
+      auto k = rs_pass1_kernel<P, PW, RW, GN, false>;                                             \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);                     \
+      nb = min(nblocks, max(1, per_sm * sms));                                                    \
+      k<<<nb, kThreads, 0, s>>>(wires, sig, rank, segs, chunks, c0, c1, params, peer_partials,    \
+                                peer_flags, epoch, epoch_base);                                   \
+    }                                                                                             \
   }
 #define GS_RSP_P(P)                                      \
   if (raw) {                                             \

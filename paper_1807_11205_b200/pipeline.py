@@ -27,6 +27,7 @@ arrays with one index.  ParamGroup objects are views into the arenas.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -243,6 +244,10 @@ class GradientPipeline:
             self.plan = LarsPlan(segs, d, order=self.order)
         if bulk:
             self.plan.extra_hint &= ~_native.HINT_NO_BULK
+        if self.sharded and os.environ.get("GS_RS_DIRECT", "0") == "1":
+            # A/B switch: gs_rs_pass1 with per-vector register loads instead of
+            # the cp.async-staged chunk (same results)
+            self.plan.extra_hint |= _native.HINT_RS_DIRECT
         self.plan.fuse_trust = fuse_trust
         self.plan.trust_in_pass2 = trust_in_pass2
         begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]

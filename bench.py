@@ -392,6 +392,20 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         cpu = {"value": round(r["ms"], 2), "unit": "ms", "cores": r["threads"], "kind": "port",
                "sample": r["sample"]}
 
+    nvlink = None
+    if pipe.sharded and pipe.fused_collective and world > 1:
+        # the sharded kernels also move (p-1)/p of their slice over NVLink:
+        # rs_pass1 pulls p-1 peer copies of the rank's slice (2 B/elem each),
+        # pass2_push stores the updated binary16 slice into p-1 peers (a
+        # collective: every rank takes part before rank 0 alone reports)
+        nv_bytes = (world - 1) * 2 * pipe.owned_elems
+        rs_ms = sum(statistics.median(v) for k, v in phase_ms.items() if k.startswith("rs_pass1"))
+        t_nv = torch.tensor([rs_ms, p2_ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_nv, op=dist.ReduceOp.MAX)
+        nvlink = {"peak_gbs": 900.0, "peak_kind": "NVLink 5 per direction (nominal)",
+                  "rs_pass1_in_gbs": round(nv_bytes / (float(t_nv[0]) * 1e-3) / 1e9, 1),
+                  "pass2_push_out_gbs": round(nv_bytes / (float(t_nv[1]) * 1e-3) / 1e9, 1),
+                  "bytes_per_rank": nv_bytes}
     if rank != 0:
         return
     peak, peak_kind = load_peaks()
@@ -408,6 +422,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                 "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": pass2_bytes}
+    if nvlink is not None:
+        roofline["nvlink"] = nvlink
     if args.overflow:
         # every step is skipped: pass 2 only reads the flag and exits, so its
         # bandwidth is not a roofline figure

@@ -17,7 +17,8 @@ there — the overflow flag the loss scale's skip decision reads
 (halfprec.py:209-216).  The ordered kernel reports it through its own
 non-finite flag; NCCL results are checked directly.  busBW = S/t * 2(p-1)/p
 (nccl-tests convention) for every variant; max over ranks of the per-rank
-CUDA-event time on the launching stream.
+CUDA-event time on the launching stream, with the calls queued behind a
+device sleep so the events time the GPU, not the host launch rate.
 
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
       --master-addr 127.0.0.1 --master-port P tools/allreduce_sweep.py [--max-log2 30]
@@ -84,6 +85,8 @@ def main() -> None:
     ow = OrderedWire(comms[1], max_elems, dev) if any(v[0].startswith("ordered") for v in variants) \
         else None
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    tok = torch.zeros(1, dtype=torch.float32, device=dev)
+    sleep_cycles = 1.0e7  # ~5 ms at 2 GHz, longer than queueing 50 eager calls
     half = [0]
     lines = []
     for lg in range(args.min_log2, args.max_log2 + 1):
@@ -153,6 +156,11 @@ def main() -> None:
                 run()
             torch.cuda.synchronize(dev)
             dist.barrier(group=host)
+            # line the ranks' streams up, then let the host queue every call
+            # while the GPU sleeps, so the events time device work and not the
+            # host's launch rate (which bounds eager small-message calls)
+            comms[1].allreduce_ring(tok)
+            torch.cuda._sleep(int(sleep_cycles))
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(s0)

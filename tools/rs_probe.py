@@ -81,6 +81,9 @@ def main():
             times = []
             for rep in range(5):
                 dist.all_reduce(tok)
+                # the host queues every call while the GPU sleeps: the events
+                # then time device work, not the host's launch rate
+                torch.cuda._sleep(8_000_000)
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev0.record(s0)

@@ -110,9 +110,9 @@ typedef struct gs_step_params {
 #define GS_HINT_RAWFLAG 2u    /* fp16 input, GS_HINT_POW2 and mul <= 1: a value is
                                  non-finite iff its binary16 exponent is all ones */
 #define GS_HINT_GRADNORM 4u   /* must equal (params->mode & GS_MODE_GRADNORM) != 0 */
-#define GS_HINT_RS_DIRECT 16u /* gs_rs_pass1: register loads per vector instead of
-                                 staging a chunk's peer vectors in shared memory
-                                 with cp.async (all of them in flight at once) */
+#define GS_HINT_RS_STAGE 16u  /* gs_rs_pass1: stage a chunk's peer vectors in shared
+                                 memory with cp.async (all in flight at once) instead
+                                 of register loads per vector (measured slower) */
 #define GS_HINT_NO_BULK 8u    /* fp16 pass 1: use the register-staged kernel instead of
                                  the TMA (cp.async.bulk) pipelined persistent kernel */
 
@@ -230,10 +230,12 @@ int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
  * are STORED into every peer's partials array (peer_partials[q], 3 doubles
  * per chunk at the chunk's global index); the step flags are OR-ed into every
  * peer's flag word (peer_flags[q]).  Every rank must call it (also with
- * c0 == c1) with the same epoch; p in {2, 4, 8}. */
+ * c0 == c1) with the same epoch; p in {2, 4, 8}.  A non-null chunk_list
+ * (device int32) makes the chunks chunk_list[c0 .. c1-1] (the rank's owned
+ * chunks of several buckets: one launch, one entry barrier). */
 int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
                 const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
+                const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
                 const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
                 int nblocks, void* stream);
 

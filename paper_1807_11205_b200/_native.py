@@ -35,7 +35,7 @@ HINT_POW2 = 1
 HINT_RAWFLAG = 2
 HINT_GRADNORM = 4
 HINT_NO_BULK = 8
-HINT_RS_DIRECT = 16
+HINT_RS_STAGE = 16
 
 # numpy mirrors of the device structs (layout asserted against the header)
 SEGMENT_DTYPE = np.dtype([
@@ -95,7 +95,7 @@ SIGNATURES = {
     "gs_ordered_allgather": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_uint32,
                                      c_void_p, c_int, c_void_p]),
     "gs_rs_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
-                            c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
+                            c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
                             c_void_p]),
     "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32,
                               c_void_p,

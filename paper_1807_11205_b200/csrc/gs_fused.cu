@@ -193,7 +193,7 @@ template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool STAGE>
 __global__ void __launch_bounds__(kThreads, kRsMinBlocks<P>)
 rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__ sig, int rank,
                 const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
-                int c1, const gs_step_params* __restrict__ params,
+                int c1, const int32_t* __restrict__ chunk_list, const gs_step_params* __restrict__ params,
                 const uint64_t* __restrict__ peer_partials, const uint64_t* __restrict__ peer_flags,
                 uint32_t epoch, const uint32_t* __restrict__ epoch_base) {
   epoch += *epoch_base;
@@ -204,7 +204,8 @@ rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__
   cx.wd = params->weight_decay;
   const uint8_t* mybase = reinterpret_cast<const uint8_t*>(wires[rank]);
   uint32_t flag_acc = 0;
-  for (int c = c0 + blockIdx.x; c < c1; c += gridDim.x) {
+  for (int ci = c0 + blockIdx.x; ci < c1; ci += gridDim.x) {
+    const int c = chunk_list != nullptr ? chunk_list[ci] : ci;
     const gs_chunk ch = chunks[c];
     const gs_segment* sp = segs + ch.seg;
     const uint32_t sflags = sp->flags;
@@ -360,7 +361,7 @@ extern "C" {
 
 int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
                 const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
+                const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
                 const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
                 int nblocks, void* stream) {
   GS_REQUIRE(p == 2 || p == 4 || p == 8, "gs_rs_pass1: p must be 2, 4 or 8 (got %d)", p);
@@ -370,7 +371,7 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
              "gs_rs_pass1: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const bool pow2 = hint & GS_HINT_POW2, raw = pow2 && (hint & GS_HINT_RAWFLAG),
-             gnorm = hint & GS_HINT_GRADNORM, stage = !(hint & GS_HINT_RS_DIRECT);
+             gnorm = hint & GS_HINT_GRADNORM, stage = (hint & GS_HINT_RS_STAGE) != 0;
   // every CTA waits for its peers at entry: the grid must be co-resident
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -383,13 +384,15 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes<P>);       \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kStageBytes<P>);        \
       nb = min(nblocks, max(1, per_sm * sms));                                                    \
-      k<<<nb, kThreads, kStageBytes<P>, s>>>(wires, sig, rank, segs, chunks, c0, c1, params,      \
+      k<<<nb, kThreads, kStageBytes<P>, s>>>(wires, sig, rank, segs, chunks, c0, c1, chunk_list,  \
+                                             params,                                              \
                                              peer_partials, peer_flags, epoch, epoch_base);       \
     } else {                                                                                      \
       auto k = rs_pass1_kernel<P, PW, RW, GN, false>;                                             \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);                     \
       nb = min(nblocks, max(1, per_sm * sms));                                                    \
-      k<<<nb, kThreads, 0, s>>>(wires, sig, rank, segs, chunks, c0, c1, params, peer_partials,    \
+      k<<<nb, kThreads, 0, s>>>(wires, sig, rank, segs, chunks, c0, c1, chunk_list, params,       \
+                                peer_partials,                                                    \
                                 peer_flags, epoch, epoch_base);                                   \
     }                                                                                             \
   }

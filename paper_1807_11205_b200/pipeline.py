@@ -244,10 +244,10 @@ class GradientPipeline:
             self.plan = LarsPlan(segs, d, order=self.order)
         if bulk:
             self.plan.extra_hint &= ~_native.HINT_NO_BULK
-        if self.sharded and os.environ.get("GS_RS_DIRECT", "0") == "1":
-            # A/B switch: gs_rs_pass1 with per-vector register loads instead of
-            # the cp.async-staged chunk (same results)
-            self.plan.extra_hint |= _native.HINT_RS_DIRECT
+        if self.sharded and os.environ.get("GS_RS_STAGE", "0") == "1":
+            # A/B switch: gs_rs_pass1 staging each chunk through shared memory
+            # with cp.async instead of register loads (same results; slower)
+            self.plan.extra_hint |= _native.HINT_RS_STAGE
         self.plan.fuse_trust = fuse_trust
         self.plan.trust_in_pass2 = trust_in_pass2
         begin, count = self.plan.host_segs["chunk_begin"], self.plan.host_segs["chunk_count"]
@@ -433,20 +433,21 @@ class GradientPipeline:
         push to every peer), and a closing fence."""
         plan, a = self.plan, self.arena
         p, r = self.comm.topo.p, self.comm.rank
-        nb = len(self.buckets)
         parts, flags = dev.ptr(a.peers("partials")), dev.ptr(a.peers("flags"))
-        for b, bk in enumerate(self.buckets):
-            s0.wait_event(evs[b])
-            if timer:
-                timer(f"rs_pass1_{b}")
-            c0, c1 = self._own_bucket[b]
-            _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
-                         dev.ptr(plan.d_chunks), c0, c1, dev.ptr(plan.params), plan.hint,
-                         parts, flags, b + 1, ebase, self._nblocks, sh)
+        # every gradient is already resident: ONE reduce-scatter + pass 1 launch
+        # over the rank's owned chunks of all buckets (one entry barrier, one
+        # NVLink ramp-up) instead of one per bucket -- per-bucket launches each
+        # paid ~20 us of barrier and ramp latency (tools/rs_probe.py); the
+        # per-bucket form is the incremental API's (submit / overlap.py)
         s0.wait_stream(self._pack_stream)
         if timer:
+            timer("rs_pass1")
+        _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
+                     dev.ptr(plan.d_chunks), 0, self._n_own, dev.ptr(self._own_list),
+                     dev.ptr(plan.params), plan.hint, parts, flags, 1, ebase, self._nblocks, sh)
+        if timer:
             timer("fence")
-        _native.call("gs_peer_fence", sig, r, p, nb + 1, ebase, sh)
+        _native.call("gs_peer_fence", sig, r, p, 2, ebase, sh)
         if timer:
             timer("trust")
         plan.trust(sh)
@@ -459,8 +460,8 @@ class GradientPipeline:
                      dev.ptr(a.peers("working")), p, r, sh)
         if timer:
             timer("fence_end")
-        _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
-        _native.call("gs_counter_add", ebase, nb + 3, sh)
+        _native.call("gs_peer_fence", sig, r, p, 3, ebase, sh)
+        _native.call("gs_counter_add", ebase, 4, sh)
         if timer:
             timer("end")
 
@@ -896,7 +897,7 @@ class GradientPipeline:
                 c0, c1 = self._own_bucket[b]
                 wires = self.arena.peers("wireA" if inc["half"] == 0 else "wireB")
                 _native.call("gs_rs_pass1", dev.ptr(wires), dev.ptr(self.arena.peers("sig")), r,
-                             p, dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), c0, c1,
+                             p, dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), c0, c1, None,
                              dev.ptr(plan.params), plan.hint, dev.ptr(self.arena.peers("partials")),
                              dev.ptr(self.arena.peers("flags")), b + 1, dev.ptr(self.epoch_base),
                              self._nblocks, sh)

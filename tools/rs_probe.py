@@ -57,9 +57,9 @@ def main():
         scratch = torch.empty(2 * elems, dtype=torch.uint8, device=dev)
 
         def rs(direct):
-            hint = plan.hint | (_native.HINT_RS_DIRECT if direct else 0)
+            hint = plan.hint | (0 if direct else _native.HINT_RS_STAGE)
             _native.call("gs_rs_pass1", dv.ptr(wires), sig, rank, world, dv.ptr(plan.d_segs),
-                         dv.ptr(plan.d_chunks), c0, c1, dv.ptr(plan.params), hint,
+                         dv.ptr(plan.d_chunks), c0, c1, None, dv.ptr(plan.params), hint,
                          dv.ptr(a.peers("partials")), dv.ptr(a.peers("flags")), 1, ebase,
                          pipe._nblocks, sh_)
             _native.call("gs_counter_add", ebase, 1, sh_)

@@ -371,22 +371,27 @@ class GradientPipeline:
         plan.reset_flags(sh)
         sig, ebase = dev.ptr(a.peers("sig")), dev.ptr(self.epoch_base)
         wires = a.peers("wireA" if half == 0 else "wireB")
+        nb = len(self.buckets)
+        if self.fused_collective:
+            # one reduce-scatter launch follows all packs: pack every bucket
+            # with one launch on the compute stream
+            if timer:
+                timer("pack")
+            self._pack(ptabs, nb, sh)
+            self._launch_sharded_fused(s0, sh, sig, ebase, wires, timer)
+            self._last_wire = wire
+            self._half ^= 1
+            plan.use_segments(None)
+            return
         ps = self._pack_stream
         ps.wait_stream(s0)
         evs = []
-        for b in range(len(self.buckets)):
+        for b in range(nb):
             with torch.cuda.stream(ps):
                 self._pack(ptabs, b, int(ps.cuda_stream))
                 ev = torch.cuda.Event()
                 ev.record(ps)
                 evs.append(ev)
-        nb = len(self.buckets)
-        if self.fused_collective:
-            self._launch_sharded_fused(s0, sh, evs, sig, ebase, wires, timer)
-            self._last_wire = wire
-            self._half ^= 1
-            plan.use_segments(None)
-            return
         for b, bk in enumerate(self.buckets):
             s0.wait_event(evs[b])
             if timer:
@@ -426,7 +431,7 @@ class GradientPipeline:
         if timer:
             timer("end")
 
-    def _launch_sharded_fused(self, s0, sh, evs, sig, ebase, wires, timer) -> None:
+    def _launch_sharded_fused(self, s0, sh, sig, ebase, wires, timer) -> None:
         """The sharded step in fused kernels: per bucket one gs_rs_pass1
         (reduce-scatter + pass 1, partials and flags pushed to every peer),
         a one-CTA peer fence, trust, gs_pass2_push (pass 2 + working-weight
@@ -439,7 +444,6 @@ class GradientPipeline:
         # NVLink ramp-up) instead of one per bucket -- per-bucket launches each
         # paid ~20 us of barrier and ramp latency (tools/rs_probe.py); the
         # per-bucket form is the incremental API's (submit / overlap.py)
-        s0.wait_stream(self._pack_stream)
         if timer:
             timer("rs_pass1")
         _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
@@ -529,11 +533,16 @@ class GradientPipeline:
                     raise ValueError("gradients must be CUDA fp16/uint16 tensors of the "
                                      "parameter sizes")
             wb = dst.data_ptr()
-            tabs = []
+            tabs, host = [], []
             for b in self.buckets:
                 t = copy_table((views[i].data_ptr(), wb + 2 * self.wire_off[i], 2 * self.sizes[i])
                                for i in b.params if self.sizes[i])
                 tabs.append((dev.upload(t, self.device), len(t)))
+                host.append(t)
+            # entry len(buckets): every bucket in one table (one launch when all
+            # gradients are packed before the first collective)
+            allt = np.concatenate(host) if host else copy_table([])
+            tabs.append((dev.upload(allt, self.device), len(allt)))
             if len(self._pack_cache) > 8:
                 self._pack_cache.clear()
                 self._graphs.clear()

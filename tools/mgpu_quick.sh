@@ -22,3 +22,10 @@ if [ "${RSAB:-0}" = "1" ]; then
   P=$((P+1)); GS_RS_STAGE=1 timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero $B > $O/bench_${TAG}_n${N}_zero_stage.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_stage.log
   P=$((P+1)); GS_RS_STAGE=1 MGPU_ALGOS=zero,zero_inc timeout 300 $R --master-port $P tests/mgpu_check.py > $O/mgpu_check_${TAG}_n${N}_stage.log 2>&1; echo "rc=$?" >> $O/mgpu_check_${TAG}_n${N}_stage.log
 fi
+if [ "${ZTHETA:-0}" = "1" ]; then
+  for T in 1048576 4194304 67108864; do
+    P=$((P+1)); timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero --theta $T $B --no-e2e > $O/bench_${TAG}_n${N}_zero_theta$T.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_theta$T.log
+  done
+  P=$((P+1)); timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero --model alexnet $B > $O/bench_${TAG}_n${N}_zero_alexnet.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_alexnet.log
+  P=$((P+1)); timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero --overflow $B --no-e2e > $O/bench_${TAG}_n${N}_zero_overflow.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_overflow.log
+fi

@@ -232,8 +232,13 @@ int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
  * peer's flag word (peer_flags[q]).  Every rank must call it (also with
  * c0 == c1) with the same epoch; p in {2, 4, 8}.  A non-null chunk_list
  * (device int32) makes the chunks chunk_list[c0 .. c1-1] (the rank's owned
- * chunks of several buckets: one launch, one entry barrier). */
-int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
+ * chunks of several buckets: one launch, one entry barrier).
+ * own_wire == NULL: pull form, as above.  own_wire != NULL: inbox form —
+ * every rank's packer already STORED its raw values of this rank's slices
+ * into this rank's inboxes (wires[q] = this rank's inbox holding rank q's
+ * values, wire-shaped); the fold then reads local memory only, own_wire is
+ * this rank's wire base (the segments' g pointers lie in it). */
+int gs_rs_pass1(const uint64_t* wires, const void* own_wire, const uint64_t* sig, int rank, int p,
                 const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
                 const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
                 const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,

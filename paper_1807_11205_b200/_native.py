@@ -94,7 +94,7 @@ SIGNATURES = {
                                               c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
     "gs_ordered_allgather": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_uint32,
                                      c_void_p, c_int, c_void_p]),
-    "gs_rs_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+    "gs_rs_pass1": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                             c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
                             c_void_p]),
     "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32,

@@ -191,18 +191,28 @@ constexpr int kRsMinBlocks = P <= 2 ? 3 : 2;
 
 template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool STAGE>
 __global__ void __launch_bounds__(kThreads, kRsMinBlocks<P>)
-rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint64_t* __restrict__ sig, int rank,
-                const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
+rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint8_t* own_wire,
+                const uint64_t* __restrict__ sig, int rank, const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
                 int c1, const int32_t* __restrict__ chunk_list, const gs_step_params* __restrict__ params,
                 const uint64_t* __restrict__ peer_partials, const uint64_t* __restrict__ peer_flags,
                 uint32_t epoch, const uint32_t* __restrict__ epoch_base) {
   epoch += *epoch_base;
-  peer_barrier(sig, rank, P, 0, epoch);  // every rank's bucket is packed
+  // every rank's bucket is packed.  Pull form (own_wire == nullptr): the
+  // peers read my wire, written by my earlier pack kernel into my own memory
+  // -> relaxed signal.  Inbox form: my earlier pack kernel STORED into the
+  // peers' inboxes over NVLink -> release signal (cumulative over those
+  // stream-ordered remote stores)
+  if (own_wire == nullptr)
+    peer_barrier<false>(sig, rank, P, 0, epoch);
+  else
+    peer_barrier<true>(sig, rank, P, 0, epoch);
   Ctx cx;
   cx.u.load(params);
   cx.mul = params->mul;
   cx.wd = params->weight_decay;
-  const uint8_t* mybase = reinterpret_cast<const uint8_t*>(wires[rank]);
+  // src[q] = wires[q] + (chunk's byte offset in my wire)
+  const uint8_t* mybase =
+      own_wire != nullptr ? own_wire : reinterpret_cast<const uint8_t*>(wires[rank]);
   uint32_t flag_acc = 0;
   for (int ci = c0 + blockIdx.x; ci < c1; ci += gridDim.x) {
     const int c = chunk_list != nullptr ? chunk_list[ci] : ci;
@@ -359,7 +369,7 @@ __global__ void peer_fence_kernel(const uint64_t* __restrict__ sig, int rank, in
 
 extern "C" {
 
-int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
+int gs_rs_pass1(const uint64_t* wires, const void* own_wire, const uint64_t* sig, int rank, int p,
                 const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
                 const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
                 const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
@@ -370,6 +380,7 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
   GS_REQUIRE(wires && sig && segs && chunks && params && peer_partials && peer_flags && epoch_base,
              "gs_rs_pass1: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
+  const uint8_t* ow = static_cast<const uint8_t*>(own_wire);
   const bool pow2 = hint & GS_HINT_POW2, raw = pow2 && (hint & GS_HINT_RAWFLAG),
              gnorm = hint & GS_HINT_GRADNORM, stage = (hint & GS_HINT_RS_STAGE) != 0;
   // every CTA waits for its peers at entry: the grid must be co-resident
@@ -384,14 +395,14 @@ int gs_rs_pass1(const uint64_t* wires, const uint64_t* sig, int rank, int p,
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes<P>);       \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kStageBytes<P>);        \
       nb = min(nblocks, max(1, per_sm * sms));                                                    \
-      k<<<nb, kThreads, kStageBytes<P>, s>>>(wires, sig, rank, segs, chunks, c0, c1, chunk_list,  \
+      k<<<nb, kThreads, kStageBytes<P>, s>>>(wires, ow, sig, rank, segs, chunks, c0, c1, chunk_list,  \
                                              params,                                              \
                                              peer_partials, peer_flags, epoch, epoch_base);       \
     } else {                                                                                      \
       auto k = rs_pass1_kernel<P, PW, RW, GN, false>;                                             \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);                     \
       nb = min(nblocks, max(1, per_sm * sms));                                                    \
-      k<<<nb, kThreads, 0, s>>>(wires, sig, rank, segs, chunks, c0, c1, chunk_list, params,       \
+      k<<<nb, kThreads, 0, s>>>(wires, ow, sig, rank, segs, chunks, c0, c1, chunk_list, params,       \
                                 peer_partials,                                                    \
                                 peer_flags, epoch, epoch_base);                                   \
     }                                                                                             \

@@ -29,7 +29,21 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// block-level cross-rank barrier on signal slot `phase`
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// block-level cross-rank barrier on signal slot `phase`.
+// RELEASE = true: the signal is a release store, cumulative over the block's
+// writes ordered before it by the bar.sync (needed when THIS kernel wrote
+// data a peer reads after the barrier, or stored into peer memory).
+// RELEASE = false (entry barriers): the data a peer reads after the barrier
+// was written by EARLIER kernels on this GPU's stream into this GPU's own
+// memory, which the peer reads through this GPU's L2; kernel completion has
+// already made it visible there, so a relaxed signal suffices (the same
+// protocol as the usual custom-all-reduce start barriers) and the
+// per-block system-scope release is saved.
+template <bool RELEASE = true>
 __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, int rank, int p,
                                              int phase, uint32_t epoch) {
   __syncthreads();
@@ -37,9 +51,10 @@ __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, i
     const int q = threadIdx.x;
     uint32_t* remote = reinterpret_cast<uint32_t*>(sig[q]) +
                        ((size_t)phase * gridDim.x + blockIdx.x) * p + rank;
-    // the release store is cumulative over the block's writes ordered before
-    // it by the bar.sync above, so no separate system-scope fence is needed
-    st_release_sys(remote, epoch);
+    if (RELEASE)
+      st_release_sys(remote, epoch);
+    else
+      st_relaxed_sys(remote, epoch);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(sig[rank]) +
                            ((size_t)phase * gridDim.x + blockIdx.x) * p + q;
     // bounded by time, not spins: ranks can legitimately be seconds apart

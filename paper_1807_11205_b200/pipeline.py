@@ -301,6 +301,9 @@ class GradientPipeline:
             "wireA": 2 * self.total, "wireB": 2 * self.total, "working": 2 * self.total,
             "master": 4 * self.total, "velocity": 4 * self.total,
             "partials": 8 * max(1, 3 * nchunk), "flags": 4 * (4 + len(self.specs) + 1),
+            # inbox form of the reduce-scatter: p wire-shaped slots, slot q
+            # receives rank q's raw values of this rank's slices
+            "inbox": 2 * self.total * p,
         }
         self.arena = SymmetricArena(comm, regions, d, sig_words=2 * self._nblocks * p)
         a = self.arena
@@ -339,6 +342,13 @@ class GradientPipeline:
         self._n_own = len(own_list)
         #: elements this rank updates (pass 2) per step
         self.owned_elems = int(clen[own_list].sum()) if own_list else 0
+        ib = self.arena.bases[r] + self.arena.offsets["inbox"]
+        self._inbox_src = dev.upload(np.array([ib + 2 * self.total * q for q in range(p)],
+                                              dtype=np.uint64), d)
+        #: whole-step reduce-scatter form: "inbox" (the packer stores each
+        #: owner's share straight into its inbox over NVLink, the fold reads
+        #: local memory) or "pull" (pack locally, the owner loads over NVLink)
+        self.rs_mode = os.environ.get("GS_RS_MODE", "inbox")
 
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank (for
@@ -377,8 +387,11 @@ class GradientPipeline:
             # with one launch on the compute stream
             if timer:
                 timer("pack")
-            self._pack(ptabs, nb, sh)
-            self._launch_sharded_fused(s0, sh, sig, ebase, wires, timer)
+            if self.rs_mode == "inbox":
+                self._pack([tabs[2]], 0, sh)  # owners' shares straight into their inboxes
+            else:
+                self._pack(ptabs, nb, sh)
+            self._launch_sharded_fused(s0, sh, sig, ebase, wires, timer, wire)
             self._last_wire = wire
             self._half ^= 1
             plan.use_segments(None)
@@ -431,7 +444,7 @@ class GradientPipeline:
         if timer:
             timer("end")
 
-    def _launch_sharded_fused(self, s0, sh, sig, ebase, wires, timer) -> None:
+    def _launch_sharded_fused(self, s0, sh, sig, ebase, wires, timer, wire) -> None:
         """The sharded step in fused kernels: per bucket one gs_rs_pass1
         (reduce-scatter + pass 1, partials and flags pushed to every peer),
         a one-CTA peer fence, trust, gs_pass2_push (pass 2 + working-weight
@@ -446,7 +459,9 @@ class GradientPipeline:
         # per-bucket form is the incremental API's (submit / overlap.py)
         if timer:
             timer("rs_pass1")
-        _native.call("gs_rs_pass1", dev.ptr(wires), sig, r, p, dev.ptr(plan.d_segs),
+        inbox = self.rs_mode == "inbox"
+        _native.call("gs_rs_pass1", dev.ptr(self._inbox_src if inbox else wires),
+                     wire.data_ptr() if inbox else None, sig, r, p, dev.ptr(plan.d_segs),
                      dev.ptr(plan.d_chunks), 0, self._n_own, dev.ptr(self._own_list),
                      dev.ptr(plan.params), plan.hint, parts, flags, 1, ebase, self._nblocks, sh)
         if timer:
@@ -549,6 +564,39 @@ class GradientPipeline:
             self._pack_cache[key] = tabs
         return tabs
 
+    def _inbox_table(self, views):
+        """One gs_copy table storing this rank's gradients straight into the
+        owners' inboxes (slot = this rank), split at the per-bucket ownership
+        bounds; cached on the gradient addresses."""
+        key = ("inbox",) + tuple((t.data_ptr(), t.numel()) for t in views)
+        tab = self._pack_cache.get(key)
+        if tab is None:
+            p, r = self.comm.topo.p, self.comm.rank
+            off = self.arena.offsets["inbox"]
+            slot = [self.arena.bases[q] + off + 2 * self.total * r for q in range(p)]
+            bucket_of = {}
+            for b, bk in enumerate(self.buckets):
+                for i in bk.params:
+                    bucket_of[i] = b
+            pairs = []
+            for i, t in enumerate(views):
+                n = self.sizes[i]
+                if not n:
+                    continue
+                wo = self.wire_off[i]
+                E = self._bucket_E[bucket_of[i]]
+                for q in range(p):
+                    lo, hi = max(wo, E[q]), min(wo + n, E[q + 1])
+                    if lo < hi:
+                        pairs.append((t.data_ptr() + 2 * (lo - wo), slot[q] + 2 * lo, 2 * (hi - lo)))
+            host = copy_table(pairs)
+            tab = (dev.upload(host, self.device), len(host))
+            if len(self._pack_cache) > 8:
+                self._pack_cache.clear()
+                self._graphs.clear()
+            self._pack_cache[key] = tab
+        return tab
+
     @staticmethod
     def _pack(tabs, b: int, stream_h: int) -> None:
         tab, n = tabs[b]
@@ -607,6 +655,8 @@ class GradientPipeline:
             return tabs, tuple(id(t) for t in tabs)
         if self.sharded:
             tabs = tuple(self._tables_for(views, h) for h in self._halves)
+            if self.fused_collective:
+                tabs = tabs + (self._inbox_table(views),)
             return tabs, tuple(id(t) for t in tabs)
         tabs = self._tables_for(views, self.wire)
         return tabs, id(tabs)
@@ -905,7 +955,7 @@ class GradientPipeline:
                 p, r = self.comm.topo.p, self.comm.rank
                 c0, c1 = self._own_bucket[b]
                 wires = self.arena.peers("wireA" if inc["half"] == 0 else "wireB")
-                _native.call("gs_rs_pass1", dev.ptr(wires), dev.ptr(self.arena.peers("sig")), r,
+                _native.call("gs_rs_pass1", dev.ptr(wires), None, dev.ptr(self.arena.peers("sig")), r,
                              p, dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), c0, c1, None,
                              dev.ptr(plan.params), plan.hint, dev.ptr(self.arena.peers("partials")),
                              dev.ptr(self.arena.peers("flags")), b + 1, dev.ptr(self.epoch_base),

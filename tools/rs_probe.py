@@ -58,7 +58,7 @@ def main():
 
         def rs(direct):
             hint = plan.hint | (0 if direct else _native.HINT_RS_STAGE)
-            _native.call("gs_rs_pass1", dv.ptr(wires), sig, rank, world, dv.ptr(plan.d_segs),
+            _native.call("gs_rs_pass1", dv.ptr(wires), None, sig, rank, world, dv.ptr(plan.d_segs),
                          dv.ptr(plan.d_chunks), c0, c1, None, dv.ptr(plan.params), hint,
                          dv.ptr(a.peers("partials")), dv.ptr(a.peers("flags")), 1, ebase,
                          pipe._nblocks, sh_)

@@ -42,11 +42,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--theta", type=int, default=16 << 20, help="fusion threshold (bytes)")
-    ap.add_argument("--algorithm", default="ordered",
+    ap.add_argument("--algorithm", default="zero",
                     choices=["ring", "hierarchical", "sharded", "ordered", "zero", "zero_unfused"],
-                    help="gradient exchange at N > 1: ordered = own bit-exact NVLink all-reduce "
-                         "(default), zero = own reduce-scatter + sharded LARS update + all-gather "
-                         "of the working weights, ring/hierarchical/sharded = NCCL all-reduce")
+                    help="gradient exchange at N > 1: zero (default) = sharded ZeRO-1 step in "
+                         "fused kernels (reduce-scatter + pass 1, pass 2 + working-weight push); "
+                         "zero_unfused = the same with separate collective kernels; ordered = "
+                         "own bit-exact NVLink all-reduce + replicated update; "
+                         "ring/hierarchical/sharded = NCCL all-reduce + replicated update")
     ap.add_argument("--group-size", type=int, default=4, help="k of Topology(p, k)")
     ap.add_argument("--eta-bytes", type=int, default=None,
                     help="hybrid threshold; default: 0 for ring, inf otherwise")

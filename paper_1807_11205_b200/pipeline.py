@@ -348,7 +348,7 @@ class GradientPipeline:
         #: whole-step reduce-scatter form: "inbox" (the packer stores each
         #: owner's share straight into its inbox over NVLink, the fold reads
         #: local memory) or "pull" (pack locally, the owner loads over NVLink)
-        self.rs_mode = os.environ.get("GS_RS_MODE", "inbox")
+        self.rs_mode = os.environ.get("GS_RS_MODE", "pull")
 
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank (for

@@ -19,8 +19,8 @@ P=$((P+1)); GS_ORDERED_PUSH=1 timeout 300 $R --master-port $P bench.py --gpus $N
 P=$((P+1)); timeout 300 $R --master-port $P bench.py --gpus $N --algorithm ring --no-cpu-baseline --steps 5 --warmup 3 --no-e2e > $O/bench_${TAG}_n${N}_busbw.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_busbw.log
 P=$((P+1)); timeout 600 $R --master-port $P tools/allreduce_sweep.py --variants ring,ordered,ordered_push --min-log2 16 --out $O/sweep_${TAG}_n$N.jsonl > $O/sweep_${TAG}_n$N.log 2>&1; echo "rc=$?" >> $O/sweep_${TAG}_n$N.log
 if [ "${RSAB:-0}" = "1" ]; then
-  P=$((P+1)); GS_RS_MODE=pull timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero $B > $O/bench_${TAG}_n${N}_zero_pull.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_pull.log
-  P=$((P+1)); GS_RS_MODE=pull MGPU_ALGOS=zero timeout 300 $R --master-port $P tests/mgpu_check.py > $O/mgpu_check_${TAG}_n${N}_pull.log 2>&1; echo "rc=$?" >> $O/mgpu_check_${TAG}_n${N}_pull.log
+  P=$((P+1)); GS_RS_MODE=inbox timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero $B > $O/bench_${TAG}_n${N}_zero_inbox.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_inbox.log
+  P=$((P+1)); GS_RS_MODE=inbox MGPU_ALGOS=zero timeout 300 $R --master-port $P tests/mgpu_check.py > $O/mgpu_check_${TAG}_n${N}_inbox.log 2>&1; echo "rc=$?" >> $O/mgpu_check_${TAG}_n${N}_inbox.log
   P=$((P+1)); GS_RS_STAGE=1 timeout 300 $R --master-port $P bench.py --gpus $N --algorithm zero $B > $O/bench_${TAG}_n${N}_zero_stage.log 2>&1; echo "rc=$?" >> $O/bench_${TAG}_n${N}_zero_stage.log
   P=$((P+1)); GS_RS_STAGE=1 MGPU_ALGOS=zero,zero_inc timeout 300 $R --master-port $P tests/mgpu_check.py > $O/mgpu_check_${TAG}_n${N}_stage.log 2>&1; echo "rc=$?" >> $O/mgpu_check_${TAG}_n${N}_stage.log
 fi

@@ -143,7 +143,7 @@ ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
   uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
 
-  peer_barrier<false>(sig, rank, P, 0, epoch);  // A: every bucket packed
+  peer_barrier(sig, rank, P, 0, epoch);  // A: every bucket packed
 
   // B: fold my slice, sub-range blockIdx.x
   int64_t lo, hi;
@@ -180,7 +180,7 @@ ordered_allreduce_push_kernel(const uint64_t* __restrict__ bufs, const uint64_t*
 #pragma unroll
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
   uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
-  peer_barrier<false>(sig, rank, P, 0, epoch);
+  peer_barrier(sig, rank, P, 0, epoch);
   int64_t lo, hi;
   subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
   uint32_t bad = 0;
@@ -206,7 +206,7 @@ ordered_reduce_scatter_kernel(const uint64_t* __restrict__ bufs, const uint64_t*
 #pragma unroll
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]);
   uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]);
-  peer_barrier<false>(sig, rank, P, 0, epoch);  // every rank's bucket is packed
+  peer_barrier(sig, rank, P, 0, epoch);  // every rank's bucket is packed
   int64_t lo, hi;
   split_range(bounds[rank], bounds[rank + 1], gridDim.x, blockIdx.x, 8, lo, hi);
   uint32_t bad = 0;
@@ -225,7 +225,7 @@ ordered_allgather_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
                          const uint32_t* __restrict__ epoch_base) {
   if (epoch_base != nullptr) epoch += *epoch_base;
   uint8_t* mine = reinterpret_cast<uint8_t*>(bufs[rank]);
-  peer_barrier<false>(sig, rank, p, 0, epoch);
+  peer_barrier(sig, rank, p, 0, epoch);
 #pragma unroll 1
   for (int d = 1; d < p; ++d) {
     const int r = (rank + d) % p;
@@ -233,7 +233,7 @@ ordered_allgather_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __re
     split_range(bounds[r], bounds[r + 1], gridDim.x, blockIdx.x, 16, lo, hi);
     copy_range(reinterpret_cast<const uint8_t*>(bufs[r]), mine, lo, hi);
   }
-  peer_barrier<false>(sig, rank, p, 1, epoch);
+  peer_barrier(sig, rank, p, 1, epoch);
 }
 
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }

@@ -197,15 +197,10 @@ rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint8_t* own_wire,
                 const uint64_t* __restrict__ peer_partials, const uint64_t* __restrict__ peer_flags,
                 uint32_t epoch, const uint32_t* __restrict__ epoch_base) {
   epoch += *epoch_base;
-  // every rank's bucket is packed.  Pull form (own_wire == nullptr): the
-  // peers read my wire, written by my earlier pack kernel into my own memory
-  // -> relaxed signal.  Inbox form: my earlier pack kernel STORED into the
-  // peers' inboxes over NVLink -> release signal (cumulative over those
-  // stream-ordered remote stores)
-  if (own_wire == nullptr)
-    peer_barrier<false>(sig, rank, P, 0, epoch);
-  else
-    peer_barrier<true>(sig, rank, P, 0, epoch);
+  // every rank's bucket is packed (pull form: into its own wire; inbox form:
+  // stored into the owners' inboxes over NVLink) -- a release signal,
+  // cumulative over those stream-ordered stores
+  peer_barrier(sig, rank, P, 0, epoch);
   Ctx cx;
   cx.u.load(params);
   cx.mul = params->mul;

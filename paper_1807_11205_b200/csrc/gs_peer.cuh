@@ -37,12 +37,12 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
 // RELEASE = true: the signal is a release store, cumulative over the block's
 // writes ordered before it by the bar.sync (needed when THIS kernel wrote
 // data a peer reads after the barrier, or stored into peer memory).
-// RELEASE = false (entry barriers): the data a peer reads after the barrier
-// was written by EARLIER kernels on this GPU's stream into this GPU's own
-// memory, which the peer reads through this GPU's L2; kernel completion has
-// already made it visible there, so a relaxed signal suffices (the same
-// protocol as the usual custom-all-reduce start barriers) and the
-// per-block system-scope release is saved.
+// RELEASE = false: a relaxed signal, for data written by EARLIER kernels into
+// this GPU's own memory.  Not used: the signal slots are shared by kernels of
+// different grid sizes, and a relaxed signal overtaken by a later kernel's
+// signal to the same slot can move the slot's epoch backwards (a 4-GPU
+// single-bucket run trapped on exactly such a lost wait); every barrier uses
+// release signals.
 template <bool RELEASE = true>
 __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, int rank, int p,
                                              int phase, uint32_t epoch) {

@@ -448,6 +448,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                    "algorithm": args.algorithm if world > 1 else "none",
                    "topology": (f"Topology({world},{comm.topo.k})" if comm else "1 GPU"),
                    "forced_overflow": bool(args.overflow),
+                   "w16_push": (("nvls-multicast" if pipe._mc_working else "per-peer stores")
+                                if pipe.sharded and pipe.fused_collective else None),
                    "parallelism": f"dp{world}", "l2": "flushed before every step (256 MiB write, then read: no step data resident, L2 clean)"},
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),

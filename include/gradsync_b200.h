@@ -248,13 +248,15 @@ int gs_rs_pass1(const uint64_t* wires, const void* own_wire, const uint64_t* sig
  * chunk_list, over chunks chunk_list[c0 .. c1-1]) that also stores each
  * updated binary16 working weight into every peer's working arena
  * (peer_working[q] = peer q's base; the segments' w16 lie in
- * peer_working[rank]).  Replaces gs_lars_pass2 + the all-gather of the
+ * peer_working[rank]).  mc_working != NULL: the NVLS multicast address of
+ * peer_working[rank]'s window (same offsets) — one multimem store per vector
+ * reaches every rank.  Replaces gs_lars_pass2 + the all-gather of the
  * working weights (lars.py:178-181).  Launched as a programmatic dependent of
  * gs_lars_trust. */
 int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
                   const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const float* seg_scale,
                   const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
-                  int rank, void* stream);
+                  int rank, void* mc_working, void* stream);
 
 /* One-CTA barrier: this GPU's remote stores from earlier kernels on the
  * stream are visible to every peer, and every peer's to this GPU. */

@@ -98,8 +98,8 @@ SIGNATURES = {
                             c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
                             c_void_p]),
     "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32,
-                              c_void_p,
-                              c_void_p, c_uint32, c_void_p, c_int, c_int, c_void_p]),
+                              c_void_p, c_void_p, c_uint32, c_void_p, c_int, c_int, c_void_p,
+                              c_void_p]),
     "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_uint32, c_void_p, c_void_p]),
 }
 

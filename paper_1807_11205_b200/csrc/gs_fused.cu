@@ -268,13 +268,25 @@ rs_pass1_kernel(const uint64_t* __restrict__ wires, const uint8_t* own_wire,
   }
 }
 
-// pass 2 over owned chunks, pushing the binary16 result to every peer
+// NVLS multicast store: ONE 16-byte store to a multicast address that the
+// NVSwitch replicates into every rank's copy (the bits travel untouched)
+__device__ __forceinline__ void multimem_st16(uint8_t* mc, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+// pass 2 over owned chunks, pushing the binary16 result to every peer: with
+// a multicast mapping of the working arena (mc != nullptr) one multimem
+// store per vector reaches every rank (outbound NVLink traffic 1x instead of
+// (p-1)x); otherwise one store per peer
 template <bool POW2, bool DECAY>
 __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, float* __restrict__ w,
                                               float* __restrict__ v, uint16_t* __restrict__ w16,
                                               int len, const Ctx& cx, float s,
                                               const uint64_t* __restrict__ peer_working, int p,
-                                              int rank, size_t woff) {
+                                              int rank, size_t woff, uint8_t* mc) {
   using Gt = G<true>;
   const bool vec = gs::is_aligned16(g) && gs::is_aligned16(w) && gs::is_aligned16(v) &&
                    gs::is_aligned16(w16);
@@ -296,8 +308,12 @@ __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, fl
     __stcs(wp, make_float4(ww[0].x, ww[0].y, ww[1].x, ww[1].y));
     __stcs(wp + 1, make_float4(ww[2].x, ww[2].y, ww[3].x, ww[3].y));
     const uint4 h = make_uint4(pack_w16(ww[0]), pack_w16(ww[1]), pack_w16(ww[2]), pack_w16(ww[3]));
-    for (int q = 0; q < p; ++q)
-      reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(peer_working[q]) + woff)[i] = h;
+    if (mc != nullptr) {
+      multimem_st16(mc + woff + 16 * (size_t)i, h);
+    } else {
+      for (int q = 0; q < p; ++q)
+        reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(peer_working[q]) + woff)[i] = h;
+    }
   };
   // batches of two vectors per thread with every load issued first (the
   // stores cannot alias the next batch's loads, which the compiler cannot
@@ -327,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 4)
 pass2_push_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks, int c0,
                   const int32_t* __restrict__ chunk_list, const gs_step_params* __restrict__ params, const float* __restrict__ seg_scale,
                   const uint32_t* __restrict__ flags, uint32_t flag_mask,
-                  const uint64_t* __restrict__ peer_working, int p, int rank) {
+                  const uint64_t* __restrict__ peer_working, int p, int rank, uint8_t* mc) {
   gs::griddep_wait();  // the trust kernel's scales (PDL launch)
   if (*flags & flag_mask) return;  // lars.py:161-163
   const int c = chunk_list != nullptr ? chunk_list[c0 + blockIdx.x] : c0 + blockIdx.x;
@@ -347,10 +363,10 @@ pass2_push_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   const uint16_t* g = static_cast<const uint16_t*>(sp->g) + ch.start;
   if (decay)
     p2_push_chunk<POW2, true>(g, sp->w + ch.start, sp->v + ch.start, w16, ch.len, cx, s,
-                              peer_working, p, rank, woff);
+                              peer_working, p, rank, woff, mc);
   else
     p2_push_chunk<POW2, false>(g, sp->w + ch.start, sp->v + ch.start, w16, ch.len, cx, s,
-                               peer_working, p, rank, woff);
+                               peer_working, p, rank, woff, mc);
 }
 
 __global__ void peer_fence_kernel(const uint64_t* __restrict__ sig, int rank, int p, uint32_t epoch,
@@ -424,7 +440,7 @@ int gs_rs_pass1(const uint64_t* wires, const void* own_wire, const uint64_t* sig
 int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
                   const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const float* seg_scale,
                   const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
-                  int rank, void* stream) {
+                  int rank, void* mc_working, void* stream) {
   GS_REQUIRE(c0 >= 0 && c1 >= c0 && p >= 1 && rank >= 0 && rank < p, "gs_pass2_push: bad arguments");
   if (c1 == c0) return GS_OK;
   GS_REQUIRE(segs && chunks && params && seg_scale && flags && peer_working,
@@ -433,10 +449,12 @@ int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1
   cudaError_t e;
   if (hint & GS_HINT_POW2)
     e = gs_launch_pdl(pass2_push_kernel<true>, dim3(c1 - c0), dim3(kThreads), 0, s, segs, chunks, c0,
-                      chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank);
+                      chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank,
+                      static_cast<uint8_t*>(mc_working));
   else
     e = gs_launch_pdl(pass2_push_kernel<false>, dim3(c1 - c0), dim3(kThreads), 0, s, segs, chunks,
-                      c0, chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank);
+                      c0, chunk_list, params, seg_scale, flags, flag_mask, peer_working, p, rank,
+                      static_cast<uint8_t*>(mc_working));
   if (e != cudaSuccess) {
     gs_set_error("gs_pass2_push: %s", cudaGetErrorString(e));
     return GS_ECUDA;

@@ -248,6 +248,13 @@ class SymmetricArena:
         torch.cuda.synchronize(device)
         self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
         self.bases = [int(x) for x in self.hdl.buffer_ptrs]
+        # NVLS multicast mapping of the whole window (0 when the box has no
+        # NVSwitch multicast): a store to mc_base + off lands at off in every
+        # rank's window
+        try:
+            self.mc_base = int(self.hdl.multicast_ptr or 0)
+        except (AttributeError, RuntimeError):
+            self.mc_base = 0
         self._tabs = {}
         for name in self.offsets:
             self._tabs[name] = dev.upload(
@@ -257,6 +264,10 @@ class SymmetricArena:
     def view(self, name: str, dtype: torch.dtype) -> torch.Tensor:
         o, n = self.offsets[name], self.sizes[name]
         return self.buf[o:o + n].view(dtype)
+
+    def multicast(self, name: str) -> int | None:
+        """Multicast address of region `name` (None without NVLS support)."""
+        return self.mc_base + self.offsets[name] if self.mc_base else None
 
     def peers(self, name: str) -> torch.Tensor:
         """Device uint64[p]: every rank's address of region `name`."""

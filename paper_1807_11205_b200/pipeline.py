@@ -349,6 +349,10 @@ class GradientPipeline:
         #: owner's share straight into its inbox over NVLink, the fold reads
         #: local memory) or "pull" (pack locally, the owner loads over NVLink)
         self.rs_mode = os.environ.get("GS_RS_MODE", "pull")
+        #: NVLS multicast address of the working arena: pass 2 then pushes each
+        #: updated binary16 vector to every rank with ONE store
+        self._mc_working = self.arena.multicast("working") \
+            if os.environ.get("GS_MULTICAST", "1") == "1" else None
 
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank (for
@@ -476,7 +480,7 @@ class GradientPipeline:
         _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), 0,
                      self._n_own, dev.ptr(self._own_list), dev.ptr(plan.params), plan.hint,
                      dev.ptr(plan.seg_scale), dev.ptr(plan.flags), mask,
-                     dev.ptr(a.peers("working")), p, r, sh)
+                     dev.ptr(a.peers("working")), p, r, self._mc_working, sh)
         if timer:
             timer("fence_end")
         _native.call("gs_peer_fence", sig, r, p, 3, ebase, sh)
@@ -993,7 +997,7 @@ class GradientPipeline:
             _native.call("gs_pass2_push", dev.ptr(plan.d_segs), dev.ptr(plan.d_chunks), 0,
                          self._n_own, dev.ptr(self._own_list), dev.ptr(plan.params), plan.hint,
                          dev.ptr(plan.seg_scale), dev.ptr(plan.flags), mask,
-                         dev.ptr(self.arena.peers("working")), p, r, sh)
+                         dev.ptr(self.arena.peers("working")), p, r, self._mc_working, sh)
             _native.call("gs_peer_fence", sig, r, p, nb + 2, ebase, sh)
             _native.call("gs_counter_add", ebase, nb + 3, sh)
             self._half ^= 1

@@ -349,10 +349,13 @@ class GradientPipeline:
         #: owner's share straight into its inbox over NVLink, the fold reads
         #: local memory) or "pull" (pack locally, the owner loads over NVLink)
         self.rs_mode = os.environ.get("GS_RS_MODE", "pull")
-        #: NVLS multicast address of the working arena: pass 2 then pushes each
-        #: updated binary16 vector to every rank with ONE store
+        #: NVLS multicast address of the working arena (GS_MULTICAST=1): pass 2
+        #: then pushes each updated binary16 vector to every rank with ONE
+        #: store.  Off by default: the all-gather is bound by each rank's
+        #: INBOUND traffic, (p-1)/p of the arena either way, and the multicast
+        #: stores measured slower (p=4: pass2_push 87 vs 73 us, r01p)
         self._mc_working = self.arena.multicast("working") \
-            if os.environ.get("GS_MULTICAST", "1") == "1" else None
+            if os.environ.get("GS_MULTICAST", "0") == "1" else None
 
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank (for

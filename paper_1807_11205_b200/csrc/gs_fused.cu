@@ -22,9 +22,11 @@
 
 namespace {
 
-// vectors per thread in flight per batch (P raw loads each); one vector
-// keeps P = 2 / 4 / 8 at 75 / 92 / 118 registers, i.e. 3 / 2 / 2 co-resident
-// CTAs per SM (two vectors: 124-206 registers, 1-2 CTAs per SM)
+// vectors per thread in flight per batch (P raw loads each).  One vector
+// keeps the kernel at <= 64 registers for P = 2 / 4 (4 co-resident CTAs per
+// SM) and <= 80 for P = 8 (3 per SM): the reduce-scatter is bound by NVLink
+// load latency per chunk, so more resident CTAs = more chunks in flight
+// (two vectors took 124-206 registers, 1-2 CTAs per SM)
 template <int P>
 constexpr int kU = 1;
 
@@ -184,10 +186,9 @@ __device__ __forceinline__ void rs_p1_chunk_staged(const uint16_t* const (&src)[
 }
 
 // residency: every CTA waits for its peers at entry, so the whole grid must
-// fit at once; more CTAs per SM hide NVLink load latency behind other CTAs'
-// fp64 work (unbounded, P = 4 took 206 registers = 1 CTA per SM)
+// fit at once (the launcher clamps the grid with the occupancy calculator)
 template <int P>
-constexpr int kRsMinBlocks = P <= 2 ? 3 : 2;
+constexpr int kRsMinBlocks = P <= 4 ? 4 : 3;
 
 template <int P, bool POW2, bool RAWFLAG, bool GNORM, bool STAGE>
 __global__ void __launch_bounds__(kThreads, kRsMinBlocks<P>)

@@ -295,8 +295,8 @@ class GradientPipeline:
         nchunk = len(chunks)
         sms = torch.cuda.get_device_properties(d).multi_processor_count
         # grid of the peer-synchronised kernels (each clamps to what is
-        # co-resident: 3 CTAs per SM for the p = 2 gs_rs_pass1)
-        self._nblocks = 3 * sms
+        # co-resident: 4 CTAs per SM for gs_rs_pass1 at p = 2 / 4)
+        self._nblocks = 4 * sms
         regions = {
             "wireA": 2 * self.total, "wireB": 2 * self.total, "working": 2 * self.total,
             "master": 4 * self.total, "velocity": 4 * self.total,

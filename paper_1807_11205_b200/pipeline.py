@@ -412,7 +412,7 @@ class GradientPipeline:
                 ev = torch.cuda.Event()
                 ev.record(ps)
                 evs.append(ev)
-        for b, bk in enumerate(self.buckets):
+        for b in range(nb):
             s0.wait_event(evs[b])
             if timer:
                 timer(f"rs{b}")
@@ -452,10 +452,11 @@ class GradientPipeline:
             timer("end")
 
     def _launch_sharded_fused(self, s0, sh, sig, ebase, wires, timer, wire) -> None:
-        """The sharded step in fused kernels: per bucket one gs_rs_pass1
-        (reduce-scatter + pass 1, partials and flags pushed to every peer),
-        a one-CTA peer fence, trust, gs_pass2_push (pass 2 + working-weight
-        push to every peer), and a closing fence."""
+        """The sharded step in fused kernels, after the pack: one gs_rs_pass1
+        over the rank's owned chunks of every bucket (reduce-scatter + pass 1,
+        partials and flags pushed to every peer), a one-CTA peer fence, trust,
+        gs_pass2_push (pass 2 + working-weight push to every peer), and a
+        closing fence."""
         plan, a = self.plan, self.arena
         p, r = self.comm.topo.p, self.comm.rank
         parts, flags = dev.ptr(a.peers("partials")), dev.ptr(a.peers("flags"))

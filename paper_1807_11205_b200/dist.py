@@ -203,6 +203,15 @@ class OrderedWire:
         self.push = os.environ.get("GS_ORDERED_PUSH", "0") == "1"
         dist.barrier()
 
+    #: elements per CTA below which a call uses fewer CTAs: a small bucket
+    #: then pays the barriers of a few CTAs instead of the whole co-resident
+    #: grid (every rank derives the same grid from n, so the per-CTA signal
+    #: slots still pair up)
+    MIN_ELEMS_PER_CTA = 16384
+
+    def grid_for(self, n: int) -> int:
+        return max(1, min(self.nblocks, -(-int(n) // self.MIN_ELEMS_PER_CTA)))
+
     def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
         """Bucket all-reduce; `slot` (1-based within the step, < per_step)
         makes the epoch unique among the step's calls."""
@@ -212,7 +221,7 @@ class OrderedWire:
         _native.call("gs_ordered_allreduce_push_f16" if self.push else "gs_ordered_allreduce_f16",
                      dev.ptr(self.bufs_dev[half]),
                      dev.ptr(self.sig_dev), self.rank, self.p, offset, n, slot + 1,
-                     dev.ptr(self.epoch_base), self.nblocks, None, stream_h)
+                     dev.ptr(self.epoch_base), self.grid_for(n), None, stream_h)
 
     def advance(self, per_step: int, stream_h: int) -> None:
         from . import _device as dev

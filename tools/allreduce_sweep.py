@@ -110,7 +110,7 @@ def main() -> None:
                 def run(_fn=fn):
                     _native.call(_fn, dv.ptr(ow.bufs_dev[half[0]]),
                                  dv.ptr(ow.sig_dev), ow.rank, ow.p, 0, nn, 1,
-                                 dv.ptr(ow.epoch_base), ow.nblocks, dv.ptr(flag),
+                                 dv.ptr(ow.epoch_base), ow.grid_for(nn), dv.ptr(flag),
                                  int(s0.cuda_stream))
                     ow.advance(1, int(s0.cuda_stream))
                     half[0] ^= 1

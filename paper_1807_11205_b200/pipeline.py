@@ -290,6 +290,13 @@ class GradientPipeline:
         from .dist import SymmetricArena
 
         p = comm.topo.p
+        #: whole-step reduce-scatter form: "pull" (pack locally, the owner
+        #: loads its peers' shares over NVLink) or "inbox" (the packer stores
+        #: each owner's share straight into its inbox over NVLink, the fold
+        #: reads local memory); measured equal within noise, pull is default
+        self.rs_mode = os.environ.get("GS_RS_MODE", "pull")
+        if self.rs_mode not in ("pull", "inbox"):
+            raise ValueError(f"GS_RS_MODE must be 'pull' or 'inbox', got {self.rs_mode!r}")
         chunks, _, _ = build_chunks(self.sizes, self.order)
         self._host_chunks = chunks
         nchunk = len(chunks)
@@ -303,7 +310,7 @@ class GradientPipeline:
             "partials": 8 * max(1, 3 * nchunk), "flags": 4 * (4 + len(self.specs) + 1),
             # inbox form of the reduce-scatter: p wire-shaped slots, slot q
             # receives rank q's raw values of this rank's slices
-            "inbox": 2 * self.total * p,
+            "inbox": 2 * self.total * p if self.rs_mode == "inbox" else 0,
         }
         self.arena = SymmetricArena(comm, regions, d, sig_words=2 * self._nblocks * p)
         a = self.arena
@@ -345,10 +352,6 @@ class GradientPipeline:
         ib = self.arena.bases[r] + self.arena.offsets["inbox"]
         self._inbox_src = dev.upload(np.array([ib + 2 * self.total * q for q in range(p)],
                                               dtype=np.uint64), d)
-        #: whole-step reduce-scatter form: "inbox" (the packer stores each
-        #: owner's share straight into its inbox over NVLink, the fold reads
-        #: local memory) or "pull" (pack locally, the owner loads over NVLink)
-        self.rs_mode = os.environ.get("GS_RS_MODE", "pull")
         #: NVLS multicast address of the working arena (GS_MULTICAST=1): pass 2
         #: then pushes each updated binary16 vector to every rank with ONE
         #: store.  Off by default: the all-gather is bound by each rank's
@@ -663,7 +666,7 @@ class GradientPipeline:
             return tabs, tuple(id(t) for t in tabs)
         if self.sharded:
             tabs = tuple(self._tables_for(views, h) for h in self._halves)
-            if self.fused_collective:
+            if self.fused_collective and self.rs_mode == "inbox":
                 tabs = tabs + (self._inbox_table(views),)
             return tabs, tuple(id(t) for t in tabs)
         tabs = self._tables_for(views, self.wire)

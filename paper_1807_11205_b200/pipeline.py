@@ -842,6 +842,11 @@ class GradientPipeline:
         the regular step."""
         arena = self.grad_arena()
         s0 = torch.cuda.current_stream(self.device)
+        if self.comm is not None and (self.fused_collective or not self.sharded):
+            ranges = self._bucket_host_ranges()
+            if ranges is not None:
+                self._enqueue_host_incremental(host_flat, arena, ranges, step)
+                return
         ranges = self._bucket_host_ranges() if self.fused_pack else None
         if ranges is None:
             arena.copy_(host_flat.reshape(-1), non_blocking=True)
@@ -1016,6 +1021,31 @@ class GradientPipeline:
         plan.use_segments(None)
         self._last_wire = inc["wire"]
         self._inc = None
+
+    def _enqueue_host_incremental(self, host_flat, arena, ranges, step: int) -> None:
+        """p > 1 from host gradients: bucket b's host->device copy runs on a
+        copy stream and the bucket is submitted (pack + collective + pass 1,
+        the incremental API) as soon as it has landed, so the PCIe transfer
+        of the later buckets hides the earlier buckets' reduction."""
+        s0 = torch.cuda.current_stream(self.device)
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        cs = self._copy_stream
+        cs.wait_stream(s0)
+        src = host_flat.reshape(-1)
+        views = self._grad_views(arena)
+        evs = []
+        with torch.cuda.stream(cs):
+            for lo, hi in ranges:
+                arena[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                evs.append(ev)
+        self.begin(step)
+        for b, ev in enumerate(evs):
+            s0.wait_event(ev)
+            self.submit(b, [views[i] for i in self.buckets[b].params])
+        self.end()
 
     def finish(self) -> StepResult:
         """Read the step's flags (the one host sync) and advance LossScale

@@ -49,17 +49,21 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded,zero_inc,ordered_inc,ring_inc").split(",")
+    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded,zero_inc,ordered_inc,ring_inc,"
+                           "zero_host,ordered_host").split(",")
     for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ring", 1),
                          ("hierarchical", 2), ("sharded", 2), ("zero_inc", 1), ("ordered_inc", 1),
-                         ("ring_inc", 1)):
+                         ("ring_inc", 1), ("zero_host", 1), ("ordered_host", 1)):
         if algo_name not in algos:
             continue
         # *_inc: the same step driven through the incremental API the
         # backward-overlap driver uses (begin / submit per bucket / end),
         # buckets submitted in REVERSE order to exercise the in-order gating
         inc = algo_name.endswith("_inc")
-        algo = algo_name[:-4] if inc else algo_name
+        # *_host: the same step from a pinned HOST gradient (enqueue_host:
+        # per-bucket H2D overlapped with the incremental submission)
+        host = algo_name.endswith("_host")
+        algo = algo_name[:-4] if inc else algo_name[:-5] if host else algo_name
         if world % k or (algo != "ring" and world == 1):
             continue
         comm = Communicator(gs.Topology(world, k))
@@ -83,7 +87,10 @@ def main():
             if step == 2:
                 wires[world - 1][4321] = 0x7C00
             flat = torch.from_numpy(wires[rank]).to(dev)
-            if inc:
+            if host:
+                pipe.enqueue_host(torch.from_numpy(wires[rank]).pin_memory(), step)
+                res = pipe.finish()
+            elif inc:
                 views = split(flat, specs)
                 pipe.begin(step)
                 for b in reversed(range(len(pipe.buckets))):

@@ -842,7 +842,8 @@ class GradientPipeline:
         the regular step."""
         arena = self.grad_arena()
         s0 = torch.cuda.current_stream(self.device)
-        if self.comm is not None and (self.fused_collective or not self.sharded):
+        if self.comm is not None and (self.fused_collective or not self.sharded) and \
+                os.environ.get("GS_HOST_INCREMENTAL", "1") == "1":
             ranges = self._bucket_host_ranges()
             if ranges is not None:
                 self._enqueue_host_incremental(host_flat, arena, ranges, step)

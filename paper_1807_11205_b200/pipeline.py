@@ -842,8 +842,11 @@ class GradientPipeline:
         the regular step."""
         arena = self.grad_arena()
         s0 = torch.cuda.current_stream(self.device)
+        # p > 1: per-bucket H2D + incremental submission is available but
+        # measured slower than one copy + the whole (graph-replayed) step
+        # (p=2: 1.36 vs 1.21 ms, same box A/B, profiles/r01r_n2_host_ab.md)
         if self.comm is not None and (self.fused_collective or not self.sharded) and \
-                os.environ.get("GS_HOST_INCREMENTAL", "1") == "1":
+                os.environ.get("GS_HOST_INCREMENTAL", "0") == "1":
             ranges = self._bucket_host_ranges()
             if ranges is not None:
                 self._enqueue_host_incremental(host_flat, arena, ranges, step)

@@ -418,7 +418,9 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # algorithmic bytes of the update kernels per element: pass 1 reads g (2)
     # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); packing adds
     # 2 (fused into pass 1 at p = 1: the wire write) or 4 (separate packer)
-    update_bytes = (26 + (2 if world == 1 else 4)) * n_params
+    # (p = 1 with the lazy wire: no wire copy at all -- nothing consumes it)
+    update_bytes = (26 + (0 if world == 1 and pipe.lazy_wire else 2 if world == 1 else 4)) \
+        * n_params
     roofline = {"bound": "hbm",
                 "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2",
                 "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,

@@ -163,7 +163,7 @@ class GradientPipeline:
                  local_workers: int = 1, use_graph: bool = True, fused_pack: bool = True,
                  bulk: bool = False, fuse_trust: bool = False, trust_in_pass2: bool = False,
                  flat_variant: str = "ring", sharded_update: bool = False,
-                 fused_collective: bool = True):
+                 fused_collective: bool = True, lazy_wire: bool = True):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -269,6 +269,11 @@ class GradientPipeline:
         # copy itself (gs_segment.gcopy), so packing costs no extra launch and
         # no re-read of the wire
         self.fused_pack = fused_pack and comm is None and not self.local
+        #: p = 1: no collective consumes the fused batches, so the wire copy is
+        #: written only when bucket_payload() asks for it (saves 2 B/element
+        #: of HBM writes per step); lazy_wire=False restores pass 1's copy
+        self.lazy_wire = bool(lazy_wire) and self.fused_pack
+        self._wire_src = None
         self._prepared = None
         self._src_cache: dict = {}
         self._grad_arena = None
@@ -523,6 +528,14 @@ class GradientPipeline:
                           for i, n in enumerate(self.sizes)])
 
     def bucket_payload(self, b: int) -> torch.Tensor:
+        """Bucket b of the last step's wire (the reference's FusedBatch
+        payload, fusion.py:84-90); at p = 1 with the lazy wire it is packed
+        from the last step's gradients on first request."""
+        src = getattr(self, "_wire_src", None)
+        if src is not None:
+            tabs = self._tables_for(src, self.wire)
+            self._pack(tabs, len(self.buckets), int(torch.cuda.current_stream(self.device).cuda_stream))
+            self._wire_src = None
         bk = self.buckets[b]
         return self._last_wire[bk.start:bk.start + bk.length]
 
@@ -658,9 +671,14 @@ class GradientPipeline:
                     raise ValueError("gradients must be CUDA fp16/uint16 tensors of the "
                                      "parameter sizes")
             wb = self.wire.data_ptr()
+            # lazy wire (default): with no collective to feed, pass 1 and
+            # pass 2 read the gradients where they lie and the fused batches
+            # are only materialised when asked for (bucket_payload); eager:
+            # pass 1 also writes the wire copy (gs_segment.gcopy)
             tab = self.plan.alt_segments([t.data_ptr() for t in views],
+                                         None if self.lazy_wire else
                                          [wb + 2 * o for o in self.wire_off])
-            return ("fused", tab), id(tab)
+            return ("fused", tab, views), id(tab)
         if self.ordered is not None:
             tabs = tuple(self._tables_for(views, h) for h in self.ordered.halves)
             return tabs, tuple(id(t) for t in tabs)
@@ -692,6 +710,8 @@ class GradientPipeline:
             self.prepare(step)
         self._prepared = None
         tabs, key = self._sources(grads)
+        if self.lazy_wire:
+            self._wire_src = tabs[2]  # bucket_payload() packs these on demand
         key = (key, self.plan.hint, self._half)
         self.plan.upload_params(s0)
         # graph replay needs every kernel of the step to be ours: comm = None,
@@ -876,6 +896,8 @@ class GradientPipeline:
                 evs.append(ev)
         plan.upload_params(s0)
         plan.use_segments(tabs[1])
+        if self.lazy_wire:
+            self._wire_src = tabs[2]
         plan.reset_flags(sh)
         for bk, ev in zip(self.buckets, evs):
             s0.wait_event(ev)

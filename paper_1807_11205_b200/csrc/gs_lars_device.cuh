@@ -16,6 +16,14 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 #ifndef GS_P1_MINB
 #define GS_P1_MINB 4     // pass-1 __launch_bounds__ min blocks per SM
 #endif
+#ifndef GS_P1_WIDEN
+// fp64 widening of the squared values in pass 1 (all forms give the same
+// double, so the sums are bit-identical): 0 = gradients and masters by
+// integer ops (masters after a warp-uniform subnormal test), the decayed
+// gradient by F2F; 1 = masters by F2F (XU pipe, exact for subnormals: no
+// subnormal test); 2 = gradients by F2F as well
+#define GS_P1_WIDEN 0
+#endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
@@ -179,9 +187,9 @@ __device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& w
     a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
              raw_nonfinite_bits(r.w);
   }
-  constexpr bool GINT = F16 && POW2;
-  bool wsub = false;
-  if (LARS) {
+  constexpr bool GINT = F16 && POW2 && GS_P1_WIDEN != 2;
+  bool wsub = GS_P1_WIDEN != 0;  // != 0: masters always take the F2F path
+  if (LARS && GS_P1_WIDEN == 0) {
     wsub = is_subnormal_nonzero(wv.a.x) | is_subnormal_nonzero(wv.a.y) |
            is_subnormal_nonzero(wv.a.z) | is_subnormal_nonzero(wv.a.w) |
            is_subnormal_nonzero(wv.b.x) | is_subnormal_nonzero(wv.b.y) |

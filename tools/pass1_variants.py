@@ -30,7 +30,8 @@ def main():
     flags = lambda s: (0 if s.kind == "weight" else 1) | (2 if s.kind == "weight" else 0)
     results = {}
     import os
-    combos = ((8192, True),) if os.environ.get("GRADSYNC_B200_LIB") else \
+    gc = os.environ.get("P1_GCOPY", "0") == "1"
+    combos = ((8192, gc),) if os.environ.get("GRADSYNC_B200_LIB") else \
         ((8192, True), (16384, True), (8192, False))
     for ce, gcopy in combos:
         segs = [SegmentSpec(base(g, i, 2), base(w, i, 4), base(v, i, 4), base(h, i, 2), s.numel,

@@ -21,8 +21,11 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 // double, so the sums are bit-identical): 0 = gradients and masters by
 // integer ops (masters after a warp-uniform subnormal test), the decayed
 // gradient by F2F; 1 = masters by F2F (XU pipe, exact for subnormals: no
-// subnormal test); 2 = gradients by F2F as well
-#define GS_P1_WIDEN 0
+// subnormal test); 2 = gradients by F2F as well.  Measured on ResNet-50
+// (tools/pass1_variants.py, profiles/r01s_pass1_variants.log): 44.0 / 45.1 /
+// 41.0 us -- once the write of the wire copy is gone, dropping the
+// per-vector subnormal test and the integer widening wins
+#define GS_P1_WIDEN 2
 #endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192

@@ -17,6 +17,8 @@ Fixtures:
                         on config 1 (shufflenet shapes, p=4, Topology(4,2),
                         theta=256 KiB, eta=inf): hashes of master/velocity/
                         working after each step, per-group fp32 scales, flags
+  netsim_golden.json    simulate() reports and crossover sweeps of the α-β model
+                        (`python tests/golden/make_golden.py make_netsim` alone)
 """
 
 from __future__ import annotations
@@ -308,9 +310,52 @@ def make_step(ref):
     (HERE / "step_golden.json").write_text(json.dumps(doc))
 
 
+def make_netsim(ref):
+    """netsim_golden.json: reference simulate() reports and crossover sweeps
+    (pkg/src/gradsync/netsim.py:77-170) over ring / hierarchical schedules
+    and several link models, floats stored as repr so the check is bitwise."""
+    col = importlib.import_module("gradsync_ref.collectives")
+    ns = importlib.import_module("gradsync_ref.netsim")
+    links = [dict(alpha=1e-5, beta_inv=1e9),
+             dict(alpha=2.5e-6, beta_inv=3.7e11, intra_group_alpha=1.1e-6,
+                  intra_group_beta_inv=8.9e11),
+             dict(alpha=0.0, beta_inv=1e9, intra_group_beta_inv=7e10),
+             dict(alpha=1.3e-5, beta_inv=2.2e10, intra_group_alpha=0.0)]
+    sims = []
+    for (p, k, n, itemsize) in [(2, 1, 1000, 4), (4, 2, 200, 4), (8, 4, 12345, 2),
+                                (16, 4, 1_000_003, 2), (64, 8, 25_557_032, 2),
+                                (6, 3, 7, 4), (1, 1, 100, 4)]:
+        for li, lk in enumerate(links):
+            link = ns.LinkModel(**lk)
+            for name, sched in (("ring", col.ring_schedule(p, n, itemsize, k=k)),
+                                ("hierarchical", col.hierarchical_schedule(
+                                    col.Topology(p, k), n, itemsize))):
+                rep = ns.simulate(sched, link)
+                sims.append({"p": p, "k": k, "n": n, "itemsize": itemsize, "link": li,
+                             "schedule": name, "total_time": repr(rep.total_time),
+                             "per_phase": {ph: repr(t) for ph, t in rep.per_phase_time.items()},
+                             "total_steps": rep.total_steps, "bytes_on_wire": rep.bytes_on_wire})
+    sweeps = []
+    for (p, k, li) in [(64, 8, 0), (16, 4, 1), (8, 2, 3), (4, 2, 1)]:
+        sizes = [4 * 10**i for i in range(9)] + [1 << s for s in range(10, 31, 4)]
+        rows = ns.crossover_sweep(p, k, ns.LinkModel(**links[li]), sizes)
+        sweeps.append({"p": p, "k": k, "link": li, "sizes": sizes,
+                       "rows": [{"bytes": r["bytes"], "ring_time": repr(r["ring_time"]),
+                                 "hierarchical_time": repr(r["hierarchical_time"]),
+                                 "faster": r["faster"]} for r in rows],
+                       "crossover": ns.find_crossover(rows)})
+    (HERE / "netsim_golden.json").write_text(json.dumps({"links": links, "simulate": sims,
+                                                         "sweeps": sweeps}))
+
+
 def main():
     ref = load_reference()
-    for fn in (make_halfprec, make_fusion, make_schedules, make_folds, make_lars, make_step):
+    fns = (make_halfprec, make_fusion, make_schedules, make_folds, make_lars, make_step,
+           make_netsim)
+    only = set(sys.argv[1:])
+    for fn in fns:
+        if only and fn.__name__ not in only:
+            continue
         fn(ref)
         print("wrote", fn.__name__)
 

@@ -173,7 +173,9 @@ class GradientPipeline:
             raise ValueError("local_workers is only for the single-process (comm=None) mode")
         self.p = comm.topo.p if comm is not None else int(local_workers)
         self.local = comm is None and self.p > 1
-        self.eta_bytes = int(eta_bytes)
+        # eta = inf (every bucket hierarchical, the reference's config 1 and
+        # netsim.calibrated_eta when ring never wins) is kept as a float
+        self.eta_bytes = eta_bytes if eta_bytes == float("inf") else int(eta_bytes)
         self.hier_variant = hier_variant
         self.grad_norm_enabled = grad_norm
         self.device = device or dev.require_cuda()

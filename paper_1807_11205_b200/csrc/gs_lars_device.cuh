@@ -24,7 +24,10 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 // subnormal test); 2 = gradients by F2F as well.  Measured on ResNet-50
 // (tools/pass1_variants.py, profiles/r01s_pass1_variants.log): 44.0 / 45.1 /
 // 41.0 us -- once the write of the wire copy is gone, dropping the
-// per-vector subnormal test and the integer widening wins
+// per-vector subnormal test and the integer widening wins; 3 = masters by
+// integer ops (after the subnormal test), gradients and decayed gradient by F2F.
+// Bench phases (profiles/r01u_pass1_widen_modes.log): pass 1 33.9-34.4 us for
+// mode 2, 35.8-35.9 for 3, 37.3 for 0 -- 2 stays the default
 #define GS_P1_WIDEN 2
 #endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
@@ -190,9 +193,10 @@ __device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& w
     a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
              raw_nonfinite_bits(r.w);
   }
-  constexpr bool GINT = F16 && POW2 && GS_P1_WIDEN != 2;
-  bool wsub = GS_P1_WIDEN != 0;  // != 0: masters always take the F2F path
-  if (LARS && GS_P1_WIDEN == 0) {
+  constexpr bool GINT = F16 && POW2 && GS_P1_WIDEN < 2;
+  constexpr bool WTEST = GS_P1_WIDEN == 0 || GS_P1_WIDEN == 3;
+  bool wsub = !WTEST;  // no test: masters always take the F2F path
+  if (LARS && WTEST) {
     wsub = is_subnormal_nonzero(wv.a.x) | is_subnormal_nonzero(wv.a.y) |
            is_subnormal_nonzero(wv.a.z) | is_subnormal_nonzero(wv.a.w) |
            is_subnormal_nonzero(wv.b.x) | is_subnormal_nonzero(wv.b.y) |

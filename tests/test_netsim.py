@@ -198,3 +198,18 @@ def test_calibration_on_measured_b200_sweep():
     measured = {(r["variant"], r["bytes"]): r["us"] for r in rows}
     assert all(measured[("ring", b)] < measured[("hierarchical_2x2", b)]
                for (v, b) in measured if v == "ring" and ("hierarchical_2x2", b) in measured)
+
+
+def test_calibration_flat_only_sweep_and_eta_edges():
+    """2-GPU sweep (profiles/r01t_n2): ring rows only, so no intra-group
+    parameters; eta is infinite when the model never prefers ring and 0 when
+    ring wins from the smallest size."""
+    rows = load_sweep(ROOT / "profiles" / "r01t_n2" / "sweep_r01t_n2.jsonl", variants={"ring"})
+    assert rows and all(r["variant"] == "ring" for r in rows)
+    link = calibrate_from_sweep(rows, 2, 1)
+    assert link.intra_group_alpha is None and link.alpha > 0 and link.beta_inv > 1e10
+    slow_ring = LinkModel(alpha=1.0, beta_inv=1e9)
+    assert calibrated_eta(64, 8, slow_ring, [4, 400], itemsize=4)[0] == float("inf")
+    eta, sweep = calibrated_eta(64, 8, LinkModel(alpha=1e-5, beta_inv=1e9),
+                                [4 * 10**i for i in range(8)], itemsize=4)
+    assert 0 < eta < float("inf") and eta == find_crossover(sweep)

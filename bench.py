@@ -128,6 +128,50 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ shared
+
+def workload_config(args, world: int) -> dict:
+    """The config object both arms print (same keys, same values)."""
+    from paper_1807_11205_b200 import shapes as sh
+    from paper_1807_11205_b200.fusion import plan_buckets
+
+    specs = sh.load_shapes(args.model)
+    sizes = [s.numel for s in specs]
+    nb = len(plan_buckets([sizes[i] for i in reversed(range(len(sizes)))], 2, args.theta))
+    algo = args.algorithm if world > 1 else "none"
+    k = args.group_size if algo in ("hierarchical", "sharded") and world % args.group_size == 0 \
+        else 1
+    return {"workload": f"{args.model} fused MP-LARS step, fp16 wire, p={world}",
+            "model": args.model, "params": sum(sizes), "tensors": len(specs),
+            "theta": args.theta, "buckets": nb, "algorithm": algo,
+            "topology": f"Topology({world},{k})" if world > 1 else "1 GPU",
+            "forced_overflow": bool(args.overflow), "parallelism": f"dp{world}"}
+
+
+def host_info() -> dict:
+    """CPU model, core count and the numpy / BLAS build of this host."""
+    import platform
+
+    import numpy as np
+    model = platform.processor() or ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '?')} {b.get('version', '')}".strip()
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "blas": blas,
+            "openblas_num_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
 # ------------------------------------------------------------------ reference arm
 
 def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, warmup: int,
@@ -191,13 +235,19 @@ def cpu_reference(model: str, p: int, theta: int, eta_bytes: int, steps: int, wa
         rp.compose_step_fp16(s_wires, s_names, s_sizes, s_order, s_groups, hp, 0.1,
                              rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
     times = []
+    stages: dict = {}
     for _ in range(steps):
+        marks = []
         t0 = time.perf_counter()
         rp.compose_step_fp16(s_wires, s_names, s_sizes, s_order, s_groups, hp, 0.1,
-                             rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads)
+                             rp.LossScaleState(1024.0), theta, eta_bytes, threads=threads,
+                             timer=lambda name: marks.append((name, time.perf_counter())))
         times.append((time.perf_counter() - t0) / frac)
+        for (a, ta), (_, tb) in zip(marks, marks[1:]):
+            stages.setdefault(a, []).append((tb - ta) / frac)
     ms = 1e3 * statistics.mean(times)
     return {"ms": ms, "threads": threads, "frac": frac, "t_full_s": t_full, "params": sum(sizes),
+            "stages_ms": {k: round(1e3 * statistics.median(v), 2) for k, v in stages.items()},
             "sample": (f"{model} p={p} theta={theta}: "
                        + ("full workload" if frac == 1.0 else
                           f"first {frac:.3f} of the parameters (wire order), time scaled by 1/frac")
@@ -215,11 +265,11 @@ def run_reference(args, rank: int, world: int) -> None:
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.model} fused MP-LARS step, fp16 wire, CPU oracle port",
-                   "model": args.model, "params": r["params"], "theta": args.theta, "p": world,
-                   "parallelism": f"dp{world} simulated in one process"},
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": r["threads"],
-                         "kind": "port", "sample": r["sample"]},
+                         "kind": "port", "sample": r["sample"] + f"; p={world} workers simulated "
+                         "in one process as the reference does", "stages_ms": r["stages_ms"],
+                         **host_info()},
         "e2e": {"value": round(r["ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -262,6 +312,16 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         wire_np[len(wire_np) // 2] = 0x7C00  # +Inf: every step is skipped
     grads_host = torch.from_numpy(wire_np).pin_memory()
     grads = grads_host.to(dev)
+    if pipe.sharded and pipe.fused_collective:
+        # the gradients live in their bucket slots of the raw wire (DDP's
+        # gradient-as-bucket-view): the fused step reads them in place and
+        # never modifies them, so no pack runs inside the step
+        o = 0
+        views = pipe.grad_views()
+        for v, spec in zip(views, specs):
+            v.copy_(grads[o:o + spec.numel])
+            o += spec.numel
+        grads = views
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     s0 = torch.cuda.current_stream(dev)
 
@@ -300,8 +360,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     t_end = time.perf_counter() + (0.0 if args.no_soak else 1.5)
     while time.perf_counter() < t_end:
         for _ in range(20):
-            pipe.enqueue(grads, args.warmup)
-        pipe.finish()
+            pipe.step(grads, args.warmup)
 
     # ---- timed region: K steps, each alone between an L2 flush and its flag
     # read; device time by CUDA events on the launching stream
@@ -392,7 +451,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         r = cpu_reference(args.model, 1, args.theta, eta, steps=3, warmup=1, budget_s=30.0)
         cpu = {"value": round(r["ms"], 2), "unit": "ms", "cores": r["threads"], "kind": "port",
-               "sample": r["sample"]}
+               "sample": r["sample"], "stages_ms": r["stages_ms"], **host_info(),
+               "note": "numpy restatement of the reference (oracle/reference_port.py) on a "
+                       "thread pool; the reference's own single-threaded code measured ~2.4 s "
+                       "per ResNet-50 step in the survey, so this baseline is conservative"}
 
     nvlink = None
     if pipe.sharded and pipe.fused_collective and world > 1:
@@ -416,11 +478,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(args.model)
     # algorithmic bytes of the update kernels per element: pass 1 reads g (2)
-    # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); packing adds
-    # 2 (fused into pass 1 at p = 1: the wire write) or 4 (separate packer)
-    # (p = 1 with the lazy wire: no wire copy at all -- nothing consumes it)
-    update_bytes = (26 + (0 if world == 1 and pipe.lazy_wire else 2 if world == 1 else 4)) \
-        * n_params
+    # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); a pack adds
+    # 4 (p = 1 lazy wire and the in-place sharded step: no pack at all)
+    packs = world > 1 and not (pipe.sharded and pipe.fused_collective)
+    update_bytes = (26 + (4 if packs or pipe.snapshot_wire else 0)) * n_params
     roofline = {"bound": "hbm",
                 "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2",
                 "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
@@ -438,21 +499,17 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "wire_dtype": "f16", "data": "synthetic",
-        "config": {"workload": f"{args.model} fused MP-LARS step (" + (
-                       "pack -> pass1 -> trust -> pass2" if world == 1 else
-                       "pack -> [reduce-scatter+pass1, partials pushed] -> fence -> trust -> "
-                       "[pass2+w16 push] -> fence" if args.algorithm == "zero" else
-                       "pack -> reduce-scatter -> pass1(shard) -> gather partials -> trust -> "
-                       "pass2(shard) -> all-gather w16" if args.algorithm == "zero_unfused" else
-                       "pack -> allreduce -> pass1 -> trust -> pass2") + ")",
-                   "model": args.model, "params": n_params, "tensors": len(specs),
-                   "theta": args.theta, "buckets": len(pipe.buckets),
-                   "algorithm": args.algorithm if world > 1 else "none",
-                   "topology": (f"Topology({world},{comm.topo.k})" if comm else "1 GPU"),
-                   "forced_overflow": bool(args.overflow),
-                   "w16_push": (("nvls-multicast" if pipe._mc_working else "per-peer stores")
-                                if pipe.sharded and pipe.fused_collective else None),
-                   "parallelism": f"dp{world}", "l2": "flushed before every step (256 MiB write, then read: no step data resident, L2 clean)"},
+        "config": workload_config(args, world),
+        "kernels": (
+            "pass1 -> trust -> pass2 (lazy wire: the kernels read the gradients in place; the "
+            "FusedBatch payloads are packed only on request)" if world == 1 else
+            "[reduce-scatter+pass1, partials pushed] -> fence -> trust -> [pass2+w16 push] -> "
+            "fence (gradients in their wire slots: no pack)" if args.algorithm == "zero" else
+            "pack -> reduce-scatter -> pass1(shard) -> gather partials -> trust -> "
+            "pass2(shard) -> all-gather w16" if args.algorithm == "zero_unfused" else
+            "pack -> allreduce -> pass1 -> trust -> pass2"),
+        "l2": "flushed before every step (256 MiB write, then read: no step data resident, "
+              "L2 clean)",
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
         "roofline": roofline,

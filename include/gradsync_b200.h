@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 #define GS_OK 0
 #define GS_EINVAL (-1)
@@ -68,8 +68,7 @@ typedef struct gs_segment {
   int32_t chunk_count;  /* number of chunks of this segment */
   uint32_t flags;       /* GS_SEG_* */
   uint32_t reserved;
-  void* gcopy;          /* optional: pass 1 also copies the raw fp16 gradient
-                           chunk here (the fused packer), or NULL */
+  void* reserved2;
 } gs_segment; /* 64 bytes */
 
 /* A contiguous piece [start, start+len) of segment `seg`; len <= 65536. */
@@ -86,8 +85,8 @@ typedef struct gs_copy {
   int64_t nbytes;
 } gs_copy; /* 24 bytes */
 
-/* Per-step scalars, in device memory so a captured CUDA graph can be replayed
- * with a new loss scale / learning rate by rewriting this struct. */
+/* Per-step scalars, passed BY VALUE to every kernel of a step (kernel
+ * parameter space): a step needs no host->device copy. */
 typedef struct gs_step_params {
   double eta;           /* LarsConfig.eta (lars.py:76) */
   double epsilon;       /* LarsConfig.epsilon */
@@ -101,20 +100,56 @@ typedef struct gs_step_params {
                            scalings (see GS_HINT_POW2), else unused */
 } gs_step_params; /* 56 bytes */
 
+/* Per-pipeline control block in device memory (zero-initialised).  The flag
+ * words and the grad-norm arrival counter are double-buffered by step
+ * parity: step k uses index k & 1, and its gs_lars_trust clears index
+ * (k + 1) & 1 for the next step (the host read it after step k - 1). */
+typedef struct gs_ctl {
+  uint32_t flags[2];    /* GS_FLAG_* of the step with that parity */
+  uint32_t counter[2];  /* gs_lars_trust's grad-norm arrival counter */
+  uint32_t status;      /* peer-wait status, sticky: 0 = ok, else
+                           0x80000000 | site << 20 | phase << 16 | peer << 8 | rank
+                           of the first wait that timed out */
+  uint32_t reserved[3];
+  double grad_norm;     /* experiment.py:408-411 of the last step */
+  double reserved2;
+} gs_ctl; /* 48 bytes */
+
+/* One rank of a peer-synchronised launch (the collectives and the fused
+ * collective + LARS kernels).  A launch covers a device table of `nranks`
+ * entries: 1 on a multi-GPU box (this GPU's rank), p when the p ranks of a
+ * job are emulated on one device — CTA b then serves entry b / nb.  Built
+ * and uploaded once per pipeline. */
+typedef struct gs_rank_ctx {
+  int32_t rank;                 /* 0 .. p-1 */
+  int32_t reserved;
+  uint64_t timeout_ns;          /* bound of every peer wait; 0 = 120 s */
+  uint32_t* status;             /* where a timed-out wait is reported (usually
+                                   &ctl->status); NULL = trap instead */
+  const uint32_t* epoch_base;   /* device-resident epoch base added to every
+                                   call's epoch (advanced by gs_counter_add), or NULL */
+  const gs_segment* segs;       /* this rank's segment table (fused kernels) */
+  const gs_chunk* chunks;       /* this rank's chunk table (fused kernels) */
+  const int32_t* own_list;      /* chunk ids this rank folds / updates, bucket by bucket */
+  const int32_t* own_off;       /* [nbuckets + 1]: bucket b owns own_list[own_off[b] .. own_off[b+1]) */
+  gs_ctl* ctl;                  /* this rank's control block */
+  const float* seg_scale;       /* trust scales (gs_pass2_push) */
+  uint32_t* nonfinite;          /* ordered all-reduce / reduce-scatter: OR 1 here when a
+                                   folded value is Inf/NaN (may be NULL) */
+  void* red;                    /* gs_rs_pass1: base of this rank's reduced wire (the
+                                   segments' g pointers lie in it; same layout as the
+                                   raw wires the fold reads) */
+} gs_rank_ctx; /* 96 bytes */
+
 /* Host-side launch hints: which specialised pass-1/pass-2 kernel may be used.
- * A hint is a promise about the contents of *params at execution time; 0 is
- * always correct (generic kernel, per-element IEEE division). */
+ * A hint is a promise about the params of the launch; 0 is always correct
+ * (generic kernel, per-element IEEE division). */
 #define GS_HINT_POW2 1u       /* g/div1/div2 == g*mul exactly: every active
                                  divisor is a power of two and (fp32 input) no
                                  divisor is active, or (fp16 input) div1 <= 2^100 */
 #define GS_HINT_RAWFLAG 2u    /* fp16 input, GS_HINT_POW2 and mul <= 1: a value is
                                  non-finite iff its binary16 exponent is all ones */
-#define GS_HINT_GRADNORM 4u   /* must equal (params->mode & GS_MODE_GRADNORM) != 0 */
-#define GS_HINT_RS_STAGE 16u  /* gs_rs_pass1: stage a chunk's peer vectors in shared
-                                 memory with cp.async (all in flight at once) instead
-                                 of register loads per vector (measured slower) */
-#define GS_HINT_NO_BULK 8u    /* fp16 pass 1: use the register-staged kernel instead of
-                                 the TMA (cp.async.bulk) pipelined persistent kernel */
+#define GS_HINT_GRADNORM 4u   /* must equal (params.mode & GS_MODE_GRADNORM) != 0 */
 
 int gs_abi_version(void);
 const char* gs_last_error(void);
@@ -167,169 +202,131 @@ int gs_fold_f32(const uint64_t* slots, int p, int64_t offset, float* out, int64_
 int gs_fold_f16_tree(const uint64_t* slots, int p, int64_t offset, uint16_t* out,
                      int64_t n, uint32_t* nonfinite, void* stream);
 
-/* Bit-exact all-reduce of one binary16 bucket over NVLink peer memory: the
- * reference's pairwise tree (fold_f16_tree, collectives.py:273-283) with the
- * bytes of a ring (reduce-scatter by peer loads, then all-gather by peer
- * loads; tcp.py:122-130 is the same design over TCP).  Call on every rank
- * with the same arguments except `rank`:
- *   bufs   device array of p peer-mapped base pointers of the (symmetric)
- *          wire buffers, bufs[rank] = this rank's own;
- *   sig    device array of p peer-mapped pointers to zero-initialised uint32
- *          signal areas of >= 2 * nblocks * p words each;
- *   offset, n  the bucket (elements) inside every wire;
- *   epoch  nonzero, strictly increasing per call on a given sig area; with
- *          epoch_base != NULL the kernel uses epoch + *epoch_base instead, so
- *          a captured CUDA graph stays valid when the caller advances the
- *          device-resident base between replays (gs_counter_add);
- *   nblocks  grid size; all CTAs must be co-resident (<= SMs).
- * The wire must be double-buffered across consecutive calls on the same
- * range (the kernel has no exit barrier).  p <= 8. */
-int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                             int64_t offset, int64_t n, uint32_t epoch,
-                             const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
-                             void* stream);
+/* ---- peer collectives (gs_collective.cu) -------------------------------
+ * Every entry point below takes `ranks` / `nranks` (gs_rank_ctx) and is
+ * called on every rank with otherwise identical arguments:
+ *   bufs / sig / peer_*  device arrays of p peer-mapped base pointers (NVLink
+ *          on a box; plain local pointers when ranks are emulated), entry
+ *          [rank] = that rank's own; sig areas are zero-initialised uint32 of
+ *          >= 2 * nblocks * p words;
+ *   epoch  nonzero, strictly increasing per call on a given sig area (plus
+ *          *ranks[i].epoch_base, so a step's calls can be replayed after the
+ *          caller advances the base with gs_counter_add);
+ *   nblocks  CTAs per rank; clamped so every rank's CTAs are co-resident.
+ * A wait that exceeds ranks[i].timeout_ns reports through ranks[i].status
+ * and drains instead of hanging the GPU. */
 
-/* Same contract and result as gs_ordered_allreduce_f16, push form: the
- * owner of a slice stores the folded slice into every peer's buffer as it
- * folds (remote stores), then one exit barrier; no gather phase.  The wire
- * must still be double-buffered across calls. */
-int gs_ordered_allreduce_push_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                                  int64_t offset, int64_t n, uint32_t epoch,
-                                  const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
-                                  void* stream);
+/* Bit-exact all-reduce of one binary16 bucket [offset, offset + n) of every
+ * rank's (double-buffered) wire: the reference's pairwise tree
+ * (fold_f16_tree, collectives.py:273-283) with the bytes of a ring (each rank
+ * folds its slice from every peer's raw values; tcp.py:122-130 is the same
+ * design over TCP).  push = 0: the slices are then gathered by peer loads
+ * after a barrier; push = 1: the owner stores its folded slice into every
+ * peer as it folds, one exit barrier.  Same result bit for bit.  p <= 8. */
+int gs_ordered_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
+                             int nblocks, int push, void* stream);
 
 /* Reduce-scatter half of the above with explicit slices: rank r folds
  * elements [bounds[r], bounds[r+1]) (device int64 array of p + 1 offsets)
  * of every peer's buffer into its own, in the reference's tree order.  Used
- * by the sharded (ZeRO-1) update, whose slices follow chunk boundaries. */
-int gs_ordered_reduce_scatter_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                                  const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
-                                  int nblocks, uint32_t* nonfinite, void* stream);
+ * by the sharded (ZeRO-1) update with separate collectives. */
+int gs_ordered_reduce_scatter_f16(const gs_rank_ctx* ranks, int nranks, int p,
+                                  const uint64_t* bufs, const uint64_t* sig, const int64_t* bounds,
+                                  uint32_t epoch, int nblocks, void* stream);
 
 /* All-gather of byte ranges over peer memory: rank r owns bytes
  * [bounds[r], bounds[r+1]) of its buffer; every rank copies the other ranks'
- * ranges from their buffers (entry and exit barriers).  Used to gather the
- * LARS chunk partials and the binary16 working weights of the sharded
- * update. */
-int gs_ordered_allgather(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                         const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
-                         int nblocks, void* stream);
+ * ranges from their buffers (entry and exit barriers).  Gathers the LARS
+ * chunk partials, the binary16 working weights and (gather_state) the
+ * sharded masters / velocities. */
+int gs_ordered_allgather(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                         const uint64_t* sig, const int64_t* bounds, uint32_t epoch, int nblocks,
+                         void* stream);
 
-/* *counter += inc on the device (stream-ordered; graph-capturable). */
+/* *counter += inc on the device (stream-ordered). */
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 
 /* ---- collective + LARS fused (sharded update, gs_fused.cu) ------------- */
 
-/* Reduce-scatter fused with LARS pass 1 (replaces gs_ordered_reduce_scatter_f16
- * + gs_lars_pass1 + the all-gather of the chunk partials; reference:
- * collectives.py:273-283 fold_f16_tree then lars.py:142-177 norms).  After an
- * entry barrier, chunks [c0, c1) of the local chunk table — this rank's
- * chunks of one bucket — are folded from every peer's wire (wires[q] = peer
- * q's base, the segment's g pointers lie in wires[rank]) in the reference's
- * tree order, stored into the local wire, and reduced to fp64 partials that
- * are STORED into every peer's partials array (peer_partials[q], 3 doubles
- * per chunk at the chunk's global index); the step flags are OR-ed into every
- * peer's flag word (peer_flags[q]).  Every rank must call it (also with
- * c0 == c1) with the same epoch; p in {2, 4, 8}.  A non-null chunk_list
- * (device int32) makes the chunks chunk_list[c0 .. c1-1] (the rank's owned
- * chunks of several buckets: one launch, one entry barrier).
- * own_wire == NULL: pull form, as above.  own_wire != NULL: inbox form —
- * every rank's packer already STORED its raw values of this rank's slices
- * into this rank's inboxes (wires[q] = this rank's inbox holding rank q's
- * values, wire-shaped); the fold then reads local memory only, own_wire is
- * this rank's wire base (the segments' g pointers lie in it). */
-int gs_rs_pass1(const uint64_t* wires, const void* own_wire, const uint64_t* sig, int rank, int p,
-                const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const uint64_t* peer_partials,
-                const uint64_t* peer_flags, uint32_t epoch, const uint32_t* epoch_base,
-                int nblocks, void* stream);
+/* Reduce-scatter fused with LARS pass 1 (replaces the reduce-scatter +
+ * gs_lars_pass1 + the all-gather of the chunk partials; reference:
+ * collectives.py:273-283 fold_f16_tree, then lars.py:142-177 norms).  After an
+ * entry barrier, each rank takes its owned chunks of buckets [b0, b1)
+ * (ranks[i].own_list / own_off; the segments' g pointers lie in
+ * ranks[i].red), folds every peer's raw binary16 values of the chunk
+ * (wires[q], never written) in the reference's tree order, stores the folded
+ * chunk in its reduced wire, reduces
+ * it to fp64 partials and STORES them into every peer's partials
+ * (peer_partials[q], 3 doubles at the chunk's index); the step flags are
+ * OR-ed into every peer's gs_ctl.flags[parity] (peer_ctl[q]).  p in {2,4,8}. */
+int gs_rs_pass1(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* wires,
+                const uint64_t* sig, const uint64_t* peer_partials, const uint64_t* peer_ctl,
+                int b0, int b1, gs_step_params params, uint32_t hint, uint32_t parity,
+                uint32_t epoch, int nblocks, void* stream);
 
-/* LARS pass 2 over chunks [c0, c1) (binary16 gradients; with a non-null
- * chunk_list, over chunks chunk_list[c0 .. c1-1]) that also stores each
- * updated binary16 working weight into every peer's working arena
- * (peer_working[q] = peer q's base; the segments' w16 lie in
- * peer_working[rank]).  mc_working != NULL: the NVLS multicast address of
- * peer_working[rank]'s window (same offsets) — one multimem store per vector
- * reaches every rank.  Replaces gs_lars_pass2 + the all-gather of the
- * working weights (lars.py:178-181).  Launched as a programmatic dependent of
- * gs_lars_trust. */
-int gs_pass2_push(const gs_segment* segs, const gs_chunk* chunks, int c0, int c1,
-                  const int32_t* chunk_list, const gs_step_params* params, uint32_t hint, const float* seg_scale,
-                  const uint32_t* flags, uint32_t flag_mask, const uint64_t* peer_working, int p,
-                  int rank, void* mc_working, void* stream);
+/* LARS pass 2 over each rank's owned chunks of buckets [b0, b1) (one CTA
+ * per chunk, grid = nranks * max_chunks where max_chunks >= every rank's
+ * owned count) that also stores each updated binary16 working weight into
+ * every peer's working arena (peer_working[q] = peer q's base; the
+ * segments' w16 lie in peer_working[rank]).  Replaces gs_lars_pass2 + the
+ * all-gather of the working weights (lars.py:178-181).  Launched as a
+ * programmatic dependent of gs_lars_trust. */
+int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* peer_working,
+                  int b0, int b1, int max_chunks, gs_step_params params, uint32_t hint,
+                  uint32_t parity, uint32_t flag_mask, void* stream);
 
-/* One-CTA barrier: this GPU's remote stores from earlier kernels on the
- * stream are visible to every peer, and every peer's to this GPU. */
-int gs_peer_fence(const uint64_t* sig, int rank, int p, uint32_t epoch, const uint32_t* epoch_base,
+/* One CTA per rank: this rank's remote stores from earlier kernels on the
+ * stream are visible to every peer, and every peer's to this rank. */
+int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
                   void* stream);
 
 /* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
 
 /* Pass 1 over `nchunk` chunks starting at chunk index `chunk0`: widen (fp16
- * grads) / mean / unscale per params->mode, OR the non-finite flags, and write
- * per-chunk fp64 partials {sum w^2, sum eff^2, sum g^2} (lars.py:145-146,
- * 169-172; experiment.py:408-411) to partials[3*chunk + k].  g_is_f16 selects
- * the gradient element type for every segment. */
+ * grads) / mean / unscale per params.mode, OR the non-finite flags into
+ * ctl->flags[parity], and write per-chunk fp64 partials {sum w^2, sum eff^2,
+ * sum g^2} (lars.py:145-146, 169-172; experiment.py:408-411) to
+ * partials[3*chunk + k].  g_is_f16 selects the gradient element type.
+ * wsq (optional, nchunk doubles): per-chunk sum w^2 left by gs_lars_pass2 of
+ * the previous step over the same masters; a non-NaN entry replaces the
+ * chunk's w^2 accumulation (same order, same bits).  Pass NULL whenever the
+ * masters may have changed since (a load, a checkpoint restore). */
 int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, uint32_t hint, double* partials,
-                  uint32_t* flags, void* stream);
+                  int g_is_f16, gs_step_params params, uint32_t hint, double* partials,
+                  gs_ctl* ctl, uint32_t parity, const double* wsq, void* stream);
 
-/* gs_lars_pass1 fused with gs_lars_trust.  counters: device uint32[nseg + 1],
- * zero before the first chunk of a step is launched (reset together with
- * the flags).  The last CTA to finish a segment folds that segment's
- * partials (same fixed order as gs_lars_trust) and writes seg_scale /
- * seg_out; the last segment to finish (of nseg_active segments that own at
- * least one chunk) fills the empty segments and writes *grad_norm_out.  May
- * be called over several disjoint chunk ranges per step (e.g. one per
- * bucket as its all-reduce lands). */
-int gs_lars_pass1_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
-                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params,
-                        uint32_t hint, double* partials, uint32_t* flags, uint32_t* counters,
-                        float* seg_scale, double* seg_out, double* grad_norm_out, void* stream);
+/* One CTA per segment: fold the chunk partials in a fixed order, take the
+ * fp64 norms, local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150,
+ * 173-176) and seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out
+ * (nseg x 4 doubles) receives {||w||, ||eff||, local, sum g^2}; with
+ * GS_MODE_GRADNORM one more CTA writes ctl->grad_norm = sqrt of the sum of
+ * all nchunk chunks' g^2 (experiment.py:408-411).  Clears
+ * ctl->flags/counter[parity ^ 1] for the next step.  peer_ctl (npeers device
+ * pointers, sharded update with separate collectives): OR every rank's
+ * flags[parity] into this rank's, so a non-finite value anywhere rejects the
+ * step everywhere.  Launched as a programmatic dependent of pass 1. */
+int gs_lars_trust(const gs_segment* segs, int nseg, int nchunk, const double* partials,
+                  gs_step_params params, float* seg_scale, double* seg_out, gs_ctl* ctl,
+                  uint32_t parity, const uint64_t* peer_ctl, int npeers, void* stream);
 
-/* Per segment (one CTA each): fold the chunk partials in a fixed order (the
- * same order as gs_lars_pass1_trust), take the fp64 norms,
- * local = eta*||w|| / (||eff|| + eps) or 1.0 (lars.py:142-150, 173-176) and
- * seg_scale[s] = float32(local * gamma) (lars.py:177).  seg_out (nseg x 4
- * doubles) receives {||w||, ||eff||, local, sum g^2}; grad_norm_out (optional)
- * receives sqrt of the sum of per-segment g^2 in segment order
- * (experiment.py:408-411) and then needs `counter`, one zeroed uint32.
- * peer_flags (npeers device pointers, sharded update): OR every rank's step
- * flags into *flags so a non-finite value anywhere rejects the step
- * everywhere; npeers = 0 otherwise. */
-int gs_lars_trust(const gs_segment* segs, int nseg, const double* partials,
-                  const gs_step_params* params, float* seg_scale, double* seg_out,
-                  double* grad_norm_out, uint32_t* counter, const uint64_t* peer_flags,
-                  int npeers, uint32_t* flags, void* stream);
-
-/* Pass 2: if (*flags & flag_mask) do nothing (lars.py:161-163 — the step is
- * rejected with no mutation).  Otherwise per element
+/* Pass 2: if (ctl->flags[parity] & flag_mask) do nothing (lars.py:161-163 —
+ * the step is rejected with no mutation).  Otherwise per element
  *   eff = g  or  g + wd*w                 (lars.py:169-172)
  *   v   = momentum*v + seg_scale[s]*eff   (lars.py:178)
  *   w   = w - v                           (lars.py:179)
  *   w16 = f32_to_f16(w)                   (lars.py:180)
- */
+ * Chunks are visited in reverse order (L2 reuse after pass 1).  wsq
+ * (optional): receives, per LARS chunk, the sum of the updated w^2 in pass
+ * 1's order (NaN where pass 1's vector order cannot be reproduced) for the
+ * next step's gs_lars_pass1. */
 int gs_lars_pass2(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                  int g_is_f16, const gs_step_params* params, uint32_t hint,
-                  const float* seg_scale, const uint32_t* flags, uint32_t flag_mask,
+                  int g_is_f16, gs_step_params params, uint32_t hint, const float* seg_scale,
+                  const gs_ctl* ctl, uint32_t parity, uint32_t flag_mask, double* wsq,
                   void* stream);
 
-/* Write `nbytes` of 0 to dst with a kernel (L2 flush helper / flag reset). */
+/* Write `nbytes` of 0 to dst with a kernel (L2 flush helper). */
 int gs_fill_zero(void* dst, int64_t nbytes, void* stream);
-
-/* gs_lars_trust fused into gs_lars_pass2 (one launch over the whole chunk
- * table): every CTA folds its own segment's chunk partials (same order as
- * gs_lars_trust, so every CTA of a segment derives the same fp32 scale)
- * while its chunk is prefetched into L2; the segment's first CTA writes
- * seg_scale/seg_out, and the last of those (of nseg_active segments owning a
- * chunk; arrival counter, one zeroed uint32) writes the empty segments and
- * *grad_norm_out.  Nothing is written
- * when (*flags & flag_mask) (lars.py:161-163). */
-int gs_lars_pass2_trust(const gs_segment* segs, int nseg, int nseg_active, const gs_chunk* chunks,
-                        int chunk0, int nchunk, int g_is_f16, const gs_step_params* params, uint32_t hint,
-                        const double* partials, float* seg_scale, double* seg_out,
-                        double* grad_norm_out, uint32_t* counter, const uint32_t* flags,
-                        uint32_t flag_mask, void* stream);
 
 #ifdef __cplusplus
 }

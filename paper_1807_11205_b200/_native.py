@@ -34,14 +34,12 @@ FLAG_GRAD_NONFINITE = 2
 HINT_POW2 = 1
 HINT_RAWFLAG = 2
 HINT_GRADNORM = 4
-HINT_NO_BULK = 8
-HINT_RS_STAGE = 16
 
 # numpy mirrors of the device structs (layout asserted against the header)
 SEGMENT_DTYPE = np.dtype([
     ("g", "<u8"), ("w", "<u8"), ("v", "<u8"), ("w16", "<u8"),
     ("n", "<i8"), ("chunk_begin", "<i4"), ("chunk_count", "<i4"),
-    ("flags", "<u4"), ("reserved", "<u4"), ("gcopy", "<u8"),
+    ("flags", "<u4"), ("reserved", "<u4"), ("reserved2", "<u8"),
 ])
 CHUNK_DTYPE = np.dtype([("start", "<i8"), ("seg", "<i4"), ("len", "<i4")])
 COPY_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("nbytes", "<i8")])
@@ -51,10 +49,37 @@ STEP_PARAMS_DTYPE = np.dtype([
     ("div1", "<f4"), ("rcp1", "<f4"), ("div2", "<f4"), ("rcp2", "<f4"),
     ("mode", "<u4"), ("mul", "<f4"),
 ])
+CTL_DTYPE = np.dtype([
+    ("flags", "<u4", (2,)), ("counter", "<u4", (2,)), ("status", "<u4"), ("reserved", "<u4", (3,)),
+    ("grad_norm", "<f8"), ("reserved2", "<f8"),
+])
+RANK_CTX_DTYPE = np.dtype([
+    ("rank", "<i4"), ("reserved", "<i4"), ("timeout_ns", "<u8"), ("status", "<u8"),
+    ("epoch_base", "<u8"), ("segs", "<u8"), ("chunks", "<u8"), ("own_list", "<u8"),
+    ("own_off", "<u8"), ("ctl", "<u8"), ("seg_scale", "<u8"), ("nonfinite", "<u8"),
+    ("red", "<u8"),
+])
 assert SEGMENT_DTYPE.itemsize == 64
+assert CTL_DTYPE.itemsize == 48
+assert RANK_CTX_DTYPE.itemsize == 96
 assert CHUNK_DTYPE.itemsize == 16
 assert COPY_DTYPE.itemsize == 24
 assert STEP_PARAMS_DTYPE.itemsize == 56
+
+
+class StepParams(ctypes.Structure):
+    """gs_step_params, passed BY VALUE to the LARS / fused kernels."""
+    _fields_ = [("eta", c_double), ("epsilon", c_double), ("gamma", c_double),
+                ("weight_decay", c_float), ("momentum", c_float),
+                ("div1", c_float), ("rcp1", c_float), ("div2", c_float), ("rcp2", c_float),
+                ("mode", c_uint32), ("mul", c_float)]
+
+    @classmethod
+    def of(cls, p: np.ndarray) -> "StepParams":
+        return cls.from_buffer_copy(np.ascontiguousarray(p).view(np.uint8).tobytes())
+
+
+assert ctypes.sizeof(StepParams) == STEP_PARAMS_DTYPE.itemsize
 
 #: every symbol include/gradsync_b200.h declares, with its ctypes signature
 SIGNATURES = {
@@ -71,39 +96,29 @@ SIGNATURES = {
     "gs_fold_f32": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int, c_void_p]),
     "gs_fold_f16_tree": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p,
                                  c_void_p]),
-    "gs_lars_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
-                              c_void_p, c_void_p, c_void_p]),
-    "gs_lars_pass1_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int,
-                                    c_void_p, c_uint32, c_void_p, c_void_p, c_void_p, c_void_p,
-                                    c_void_p, c_void_p, c_void_p]),
-    "gs_lars_trust": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                              c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
-    "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_uint32,
-                              c_void_p, c_void_p, c_uint32, c_void_p]),
+    "gs_lars_pass1": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, StepParams, c_uint32,
+                              c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),
+    "gs_lars_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, StepParams, c_void_p, c_void_p,
+                              c_void_p, c_uint32, c_void_p, c_int, c_void_p]),
+    "gs_lars_pass2": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, StepParams, c_uint32,
+                              c_void_p, c_void_p, c_uint32, c_uint32, c_void_p, c_void_p]),
     "gs_fill_zero": (c_int, [c_void_p, c_int64, c_void_p]),
-    "gs_lars_pass2_trust": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, c_void_p,
-                                    c_uint32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                    c_void_p, c_uint32, c_void_p]),
-    "gs_ordered_allreduce_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64, c_int64,
-                                         c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
-    "gs_ordered_allreduce_push_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64,
-                                              c_int64, c_uint32, c_void_p, c_int, c_void_p,
-                                              c_void_p]),
+    "gs_ordered_allreduce_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int64,
+                                         c_int64, c_uint32, c_int, c_int, c_void_p]),
+    "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p,
+                                              c_void_p, c_uint32, c_int, c_void_p]),
+    "gs_ordered_allgather": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                     c_uint32, c_int, c_void_p]),
     "gs_counter_add": (c_int, [c_void_p, c_uint32, c_void_p]),
-    "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p,
-                                              c_uint32, c_void_p, c_int, c_void_p, c_void_p]),
-    "gs_ordered_allgather": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_uint32,
-                                     c_void_p, c_int, c_void_p]),
-    "gs_rs_pass1": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
-                            c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_uint32, c_void_p, c_int,
+    "gs_rs_pass1": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                            c_int, c_int, StepParams, c_uint32, c_uint32, c_uint32, c_int,
                             c_void_p]),
-    "gs_pass2_push": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32,
-                              c_void_p, c_void_p, c_uint32, c_void_p, c_int, c_int, c_void_p,
-                              c_void_p]),
-    "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_uint32, c_void_p, c_void_p]),
+    "gs_pass2_push": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, StepParams,
+                              c_uint32, c_uint32, c_uint32, c_void_p]),
+    "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_void_p]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 _lock = threading.Lock()

@@ -133,16 +133,22 @@ class SegmentSpec:
     w16: int
     n: int
     flags: int
-    gcopy: int = 0
 
 
 class LarsPlan:
     """Device tables + scratch for running pass1 -> trust -> pass2 over a
-    fixed set of segments."""
+    fixed set of segments.
+
+    The step scalars are passed by value to every kernel (no per-step
+    host->device copy).  The flag words live in a gs_ctl block, double-
+    buffered by step parity: step k (``self.seq``) uses index k & 1 and its
+    trust kernel clears index (k + 1) & 1 for the next step; ``end_step()``
+    advances k.  ``ctl`` may be supplied (the sharded update keeps it in the
+    symmetric window so peers can OR their flags into it)."""
 
     def __init__(self, specs: list[SegmentSpec], device: torch.device, order=None,
                  chunk_elems: int = CHUNK_ELEMS, partials: torch.Tensor | None = None,
-                 flagbuf: torch.Tensor | None = None):
+                 ctl: torch.Tensor | None = None):
         self.device = device
         self.nseg = len(specs)
         chunks, begin, count = build_chunks([s.n for s in specs], order, chunk_elems)
@@ -151,7 +157,6 @@ class LarsPlan:
             segs[i]["g"], segs[i]["w"], segs[i]["v"], segs[i]["w16"] = s.g, s.w, s.v, s.w16
             segs[i]["n"] = s.n
             segs[i]["flags"] = s.flags
-            segs[i]["gcopy"] = s.gcopy
         segs["chunk_begin"] = begin
         segs["chunk_count"] = count
         self.host_segs, self.host_chunks = segs, chunks
@@ -164,54 +169,48 @@ class LarsPlan:
             torch.zeros(max(1, 3 * self.nchunk), dtype=torch.float64, device=device)
         self.seg_scale = torch.zeros(max(1, self.nseg), dtype=torch.float32, device=device)
         self.seg_out = torch.zeros(max(1, 4 * self.nseg), dtype=torch.float64, device=device)
-        self.grad_norm = torch.zeros(1, dtype=torch.float64, device=device)
-        # one int32 block, reset by one kernel per step: [0] = non-finite
-        # flags, [4 : 4 + nseg + 1] = per-segment / global arrival counters
-        # of the fused pass1 + trust kernel
-        # the step scalars and (when the plan owns it) the flag block share one
-        # device allocation, [params | pad | flags], uploaded by ONE copy per
-        # step whose zero tail resets the flags — no separate reset launch
-        psz = _native.STEP_PARAMS_DTYPE.itemsize
-        pad = (psz + 15) // 16 * 16
-        nflag = 4 + self.nseg + 1
-        own_flags = flagbuf is None
-        ctl_bytes = pad + 4 * nflag if own_flags else psz
-        self._ctl = torch.zeros(ctl_bytes, dtype=torch.uint8, device=device)
-        self._pinned_ctl = torch.zeros(ctl_bytes, dtype=torch.uint8).pin_memory()
-        self.params = self._ctl[:psz]
-        self._pinned_params = self._pinned_ctl[:psz]
-        self.flagbuf = self._ctl[pad:].view(torch.int32) if own_flags else flagbuf
-        self._flags_in_ctl = own_flags
-        self._ctl_fresh = False
-        self.flags = self.flagbuf[0:1]
-        self.counters = self.flagbuf[4:]
-        self.nseg_active = int((count > 0).sum())
+        csz = _native.CTL_DTYPE.itemsize
+        self.ctl = ctl if ctl is not None else torch.zeros(csz, dtype=torch.uint8, device=device)
+        assert self.ctl.numel() * self.ctl.element_size() >= csz
+        self._ctl_host = torch.zeros(csz, dtype=torch.uint8).pin_memory()
+        #: step sequence number (parity = seq & 1 selects the flag word)
+        self.seq = 0
+        #: per-chunk sum w^2 carried from pass 2 to the next step's pass 1
+        #: (enable_w2_cache); valid only while nothing else writes the masters
+        self.wsq = None
+        self.wsq_valid = False
         self.hint = 0
-        # pass 1 runs the register-staged kernel by default: on B200 it beats
-        # the TMA-pipelined persistent kernel (43 vs 47 us on ResNet-50,
-        # tools/pass1_variants.py); clear HINT_NO_BULK to select the latter
-        self.extra_hint = _native.HINT_NO_BULK
-        # the trust ratio as a separate single-CTA kernel: fusing it into
-        # pass 1 through per-chunk arrival counters costs a release atomic
-        # per chunk on the critical path (61 vs 43 us); see DESIGN.md §4
-        self.fuse_trust = False
-        # the trust ratio folded into pass 2 (each CTA re-derives its
-        # segment's scale) measured no faster than the separate trust kernel
-        # chained to pass 2 by programmatic dependent launch; DESIGN.md §4
-        self.trust_in_pass2 = False
+        self.sp = _native.StepParams()
+        self.params_np = np.zeros(1, dtype=_native.STEP_PARAMS_DTYPE)
 
-    def alt_segments(self, g_ptrs, gcopy_ptrs=None) -> torch.Tensor:
+    def enable_w2_cache(self) -> None:
+        """Let pass 2 leave the updated masters' per-chunk sum w^2 for the
+        next step's pass 1 (for owners of the master arena: the pipeline)."""
+        if self.wsq is None:
+            self.wsq = torch.full((max(1, self.nchunk),), float("nan"), dtype=torch.float64,
+                                  device=self.device)
+
+    def invalidate_w2_cache(self) -> None:
+        """The masters changed outside pass 2: the next pass 1 re-derives w^2."""
+        self.wsq_valid = False
+
+    @property
+    def parity(self) -> int:
+        return self.seq & 1
+
+    def end_step(self) -> None:
+        self.seq += 1
+
+    def alt_segments(self, g_ptrs) -> torch.Tensor:
         """A segment table identical to the base one except for the gradient
-        (and gcopy) pointers, uploaded once per pointer set and cached."""
-        key = (tuple(g_ptrs), tuple(gcopy_ptrs) if gcopy_ptrs is not None else None)
+        pointers, uploaded once per pointer set (bounded cache)."""
+        key = tuple(g_ptrs)
         tab = self._alt.get(key)
         if tab is None:
             segs = self.host_segs.copy()
             segs["g"] = np.asarray(g_ptrs, dtype=np.uint64)
-            if gcopy_ptrs is not None:
-                segs["gcopy"] = np.asarray(gcopy_ptrs, dtype=np.uint64)
-            if len(self._alt) > 8:
-                self._alt.clear()
+            if len(self._alt) >= 16:
+                self._alt.pop(next(iter(self._alt)))
             tab = self._alt[key] = dev.upload(segs, self.device)
         return tab
 
@@ -220,92 +219,62 @@ class LarsPlan:
         self.d_segs = self.base_segs if table is None else table
 
     # -- individual launches (all async on `stream`) --------------------
-    def set_params(self, params: np.ndarray, stream=None, g_is_f16: bool = False) -> None:
-        """Stage the step scalars into the device struct and derive the launch
-        hint.  The pinned staging buffer is reused, so the caller must not call
-        this again before the previous copy executed (lars_step and the
-        pipeline both sync on the step's flags every step)."""
-        self.stage_params(params, g_is_f16)
-        self.upload_params(stream)
-
-    def stage_params(self, params: np.ndarray, g_is_f16: bool = False) -> int:
-        """Host half of set_params: hint + pinned staging (no CUDA call)."""
-        self.hint = launch_hint(params, g_is_f16) | self.extra_hint
-        self._pinned_params.numpy()[:] = params.view(np.uint8).reshape(-1)
+    def set_params(self, params: np.ndarray, g_is_f16: bool = False) -> int:
+        """The step scalars of the next launches (host only: they travel by
+        value) and the launch hint derived from them."""
+        self.hint = launch_hint(params, g_is_f16)
+        self.params_np = params.copy()
+        self.sp = _native.StepParams.of(params)
         return self.hint
 
-    def upload_params(self, stream=None) -> None:
-        """Device half of set_params: one async copy of the step scalars and,
-        when the plan owns the flag block, of its zeros (the flag reset)."""
-        s = stream or torch.cuda.current_stream(self.device)
-        with torch.cuda.stream(s):
-            self._ctl.copy_(self._pinned_ctl, non_blocking=True)
-        self._ctl_fresh = self._flags_in_ctl
-
     def reset_flags(self, stream_h: int) -> None:
-        """Zero the flag block, unless the step's parameter upload just did."""
-        if self._ctl_fresh:
-            self._ctl_fresh = False
-            return
-        _native.call("gs_fill_zero", dev.ptr(self.flagbuf), 4 * self.flagbuf.numel(), stream_h)
+        """Zero both flag words and counters (only needed after a step that
+        ran pass 1 without trust, e.g. lars_step's gate-only probe)."""
+        _native.call("gs_fill_zero", dev.ptr(self.ctl), 16, stream_h)
 
-    @property
-    def fused(self) -> bool:
-        """pass1 computes the trust ratios itself (no separate trust launch)."""
-        return self.fuse_trust and self.nseg_active > 0
-
-    def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None,
-              fuse: bool = True):
+    def pass1(self, stream_h: int, g_is_f16: bool, chunk0: int = 0, nchunk: int | None = None):
         n = self.nchunk - chunk0 if nchunk is None else nchunk
-        if fuse and self.fused:
-            _native.call("gs_lars_pass1_trust", dev.ptr(self.d_segs), self.nseg, self.nseg_active,
-                         dev.ptr(self.d_chunks), chunk0, n, 1 if g_is_f16 else 0,
-                         dev.ptr(self.params), self.hint, dev.ptr(self.partials), dev.ptr(self.flags),
-                         dev.ptr(self.counters), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
-                         dev.ptr(self.grad_norm), stream_h)
-        else:
-            _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
-                         1 if g_is_f16 else 0, dev.ptr(self.params), self.hint,
-                         dev.ptr(self.partials), dev.ptr(self.flags), stream_h)
+        _native.call("gs_lars_pass1", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
+                     1 if g_is_f16 else 0, self.sp, self.hint, dev.ptr(self.partials),
+                     dev.ptr(self.ctl), self.parity,
+                     dev.ptr(self.wsq) if self.wsq_valid else None, stream_h)
 
-    def trust(self, stream_h: int, peer_flags: torch.Tensor | None = None, npeers: int = 0):
-        _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, dev.ptr(self.partials),
-                     dev.ptr(self.params), dev.ptr(self.seg_scale), dev.ptr(self.seg_out),
-                     dev.ptr(self.grad_norm), dev.ptr(self.counters[self.nseg:]),
-                     dev.ptr(peer_flags) if peer_flags is not None else None, npeers,
-                     dev.ptr(self.flags), stream_h)
+    def trust(self, stream_h: int, peer_ctl: torch.Tensor | None = None, npeers: int = 0):
+        _native.call("gs_lars_trust", dev.ptr(self.d_segs), self.nseg, self.nchunk,
+                     dev.ptr(self.partials),
+                     self.sp, dev.ptr(self.seg_scale), dev.ptr(self.seg_out), dev.ptr(self.ctl),
+                     self.parity, dev.ptr(peer_ctl) if peer_ctl is not None else None, npeers,
+                     stream_h)
 
     def pass2(self, stream_h: int, g_is_f16: bool, flag_mask: int, chunk0: int = 0,
-              nchunk: int | None = None, trust: bool = False):
-        """trust=True: gs_lars_pass2_trust (the trust ratio folded per CTA,
-        no separate trust launch; needs pass 1 without fusion)."""
+              nchunk: int | None = None):
         n = self.nchunk - chunk0 if nchunk is None else nchunk
-        if trust:
-            _native.call("gs_lars_pass2_trust", dev.ptr(self.d_segs), self.nseg, self.nseg_active,
-                         dev.ptr(self.d_chunks), chunk0, n, 1 if g_is_f16 else 0,
-                         dev.ptr(self.params), self.hint, dev.ptr(self.partials),
-                         dev.ptr(self.seg_scale), dev.ptr(self.seg_out), dev.ptr(self.grad_norm),
-                         dev.ptr(self.counters[self.nseg:]), dev.ptr(self.flags), flag_mask,
-                         stream_h)
-            return
         _native.call("gs_lars_pass2", dev.ptr(self.d_segs), dev.ptr(self.d_chunks), chunk0, n,
-                     1 if g_is_f16 else 0, dev.ptr(self.params), self.hint, dev.ptr(self.seg_scale),
-                     dev.ptr(self.flags), flag_mask, stream_h)
-
-    @property
-    def trust_via_pass2(self) -> bool:
-        return not self.fused and self.trust_in_pass2 and self.nseg_active > 0
+                     1 if g_is_f16 else 0, self.sp, self.hint, dev.ptr(self.seg_scale),
+                     dev.ptr(self.ctl), self.parity, flag_mask,
+                     dev.ptr(self.wsq) if self.wsq is not None else None, stream_h)
 
     def finish(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
-        """trust (unless pass 1 fused it) + pass 2, in the configured form."""
-        if self.trust_via_pass2:
-            self.pass2(stream_h, g_is_f16, flag_mask, trust=True)
-            return
-        if not self.fused:
-            self.trust(stream_h)
+        """trust + pass 2 (pass 2 is a programmatic dependent of trust)."""
+        self.trust(stream_h)
         self.pass2(stream_h, g_is_f16, flag_mask)
 
     def run(self, stream_h: int, g_is_f16: bool, flag_mask: int) -> None:
-        self.reset_flags(stream_h)
+        """One whole step: pass 1 -> trust -> pass 2, then advance the parity."""
         self.pass1(stream_h, g_is_f16)
         self.finish(stream_h, g_is_f16, flag_mask)
+        self.end_step()
+
+    def read_ctl(self, stream=None) -> np.void:
+        """Copy the control block to the host (syncs `stream`) and return it
+        as a CTL_DTYPE record: flags[parity], status, grad_norm."""
+        s = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            self._ctl_host.copy_(self.ctl.view(torch.uint8)[: self._ctl_host.numel()],
+                                 non_blocking=True)
+        s.synchronize()
+        return self._ctl_host.numpy().view(_native.CTL_DTYPE)[0]
+
+    def last_flags(self, rec) -> int:
+        """Flags of the last completed step (end_step() already advanced)."""
+        return int(rec["flags"][(self.seq - 1) & 1])

@@ -22,8 +22,10 @@
 // needed: a rank can only overwrite a buffer after all peers passed the
 // entry barrier of the following step, i.e. finished this kernel.
 // Buffers come from a symmetric-memory window (torch's _symmetric_memory):
-// peer pointers are plain device addresses mapped over NVLink.  Every spin
-// is bounded and traps rather than hanging the GPU.
+// peer pointers are plain device addresses mapped over NVLink; with p ranks
+// emulated on one device they are plain local addresses and one launch
+// carries every rank (gs_peer.cuh).  Every wait is time-bounded and reports
+// a timeout through gs_rank_ctx.status instead of hanging the GPU.
 #include "gs_peer.cuh"
 
 namespace {
@@ -132,63 +134,44 @@ __device__ __forceinline__ void split_range(int64_t s0, int64_t s1, int nb, int 
   hi = min(s1, lo + sub);
 }
 
-template <int P>
+// A: entry barrier -> B: fold my slice -> C: barrier -> D: gather (pull
+// form), or A -> fold my slice and store it into EVERY rank's buffer (push
+// form: remote stores overlap the next loads) -> exit barrier.  Same bytes
+// either way; push has one barrier and no gather phase.
+template <int P, bool PUSH>
 __global__ void __launch_bounds__(kThreads)
-ordered_allreduce_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
-                         int rank, int64_t offset, int64_t n, uint32_t epoch,
-                         const uint32_t* __restrict__ epoch_base, uint32_t* __restrict__ nonfinite) {
-  if (epoch_base != nullptr) epoch += *epoch_base;  // device-resident epochs: graph-replayable
+ordered_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                         const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                         int64_t offset, int64_t n, uint32_t epoch) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;  // graph-replayable epochs
   const uint16_t* src[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
   uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
 
-  peer_barrier(sig, rank, P, 0, epoch);  // A: every bucket packed
+  peer_barrier(sig, c, P, 0, epoch, kSiteOrderedAllreduce);  // A: every bucket packed
 
-  // B: fold my slice, sub-range blockIdx.x
   int64_t lo, hi;
-  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
+  subrange(n, P, rank, nb, c.lb, lo, hi);
   uint32_t bad = 0;
-  fold_range<P>(src, mine, lo, hi, bad);
+  fold_range<P, PUSH>(src, mine, lo, hi, bad);
   bad = __reduce_or_sync(0xFFFFFFFFu, bad);
-  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
-
-  peer_barrier(sig, rank, P, 1, epoch);  // C: every slice folded
-
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+  if (PUSH) {
+    __threadfence_system();  // this thread's remote stores, before the release below
+    peer_barrier(sig, c, P, 1, epoch, kSiteOrderedAllreduce);
+    return;
+  }
+  peer_barrier(sig, c, P, 1, epoch, kSiteOrderedAllreduce);  // C: every slice folded
   // D: gather the other ranks' folded sub-ranges
 #pragma unroll 1
   for (int d = 1; d < P; ++d) {
     const int r = (rank + d) % P;
-    subrange(n, P, r, gridDim.x, blockIdx.x, lo, hi);
+    subrange(n, P, r, nb, c.lb, lo, hi);
     copy_range(reinterpret_cast<const uint8_t*>(src[r]), reinterpret_cast<uint8_t*>(mine), 2 * lo, 2 * hi);
   }
-}
-
-// Push form: A entry barrier -> fold my slice and store it into EVERY rank's
-// buffer (remote stores over NVLink, overlapping the next loads) -> exit
-// barrier per block (block b of every peer has pushed its sub-range b; the
-// kernel ends only when all blocks passed, i.e. the whole bucket arrived).
-// Same bytes as the pull form; one barrier and no separate gather phase.
-template <int P>
-__global__ void __launch_bounds__(kThreads)
-ordered_allreduce_push_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
-                              int rank, int64_t offset, int64_t n, uint32_t epoch,
-                              const uint32_t* __restrict__ epoch_base,
-                              uint32_t* __restrict__ nonfinite) {
-  if (epoch_base != nullptr) epoch += *epoch_base;
-  const uint16_t* src[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]) + offset;
-  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
-  peer_barrier(sig, rank, P, 0, epoch);
-  int64_t lo, hi;
-  subrange(n, P, rank, gridDim.x, blockIdx.x, lo, hi);
-  uint32_t bad = 0;
-  fold_range<P, true>(src, mine, lo, hi, bad);
-  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
-  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
-  __threadfence_system();  // this thread's remote stores, before the release below
-  peer_barrier(sig, rank, P, 1, epoch);
 }
 
 // Reduce-scatter with explicit slice bounds (elements, p + 1 entries):
@@ -197,22 +180,23 @@ ordered_allreduce_push_kernel(const uint64_t* __restrict__ bufs, const uint64_t*
 // this call, and the caller double-buffers the wire across steps.
 template <int P>
 __global__ void __launch_bounds__(kThreads)
-ordered_reduce_scatter_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
-                              int rank, const int64_t* __restrict__ bounds, uint32_t epoch,
-                              const uint32_t* __restrict__ epoch_base,
-                              uint32_t* __restrict__ nonfinite) {
-  if (epoch_base != nullptr) epoch += *epoch_base;
+ordered_reduce_scatter_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                              const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                              const int64_t* __restrict__ bounds, uint32_t epoch) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
   const uint16_t* src[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const uint16_t*>(bufs[q]);
   uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]);
-  peer_barrier(sig, rank, P, 0, epoch);  // every rank's bucket is packed
+  peer_barrier(sig, c, P, 0, epoch, kSiteReduceScatter);  // every rank's bucket is packed
   int64_t lo, hi;
-  split_range(bounds[rank], bounds[rank + 1], gridDim.x, blockIdx.x, 8, lo, hi);
+  split_range(bounds[rank], bounds[rank + 1], nb, c.lb, 8, lo, hi);
   uint32_t bad = 0;
   fold_range<P>(src, mine, lo, hi, bad);
   bad = __reduce_or_sync(0xFFFFFFFFu, bad);
-  if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
 }
 
 // All-gather of byte ranges: rank r owns [bounds[r], bounds[r+1]) of the
@@ -220,54 +204,57 @@ ordered_reduce_scatter_kernel(const uint64_t* __restrict__ bufs, const uint64_t*
 // barrier (the owners' ranges are final) and exit barrier (nobody reads a
 // range its owner may overwrite next).
 __global__ void __launch_bounds__(kThreads)
-ordered_allgather_kernel(const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
-                         int rank, int p, const int64_t* __restrict__ bounds, uint32_t epoch,
-                         const uint32_t* __restrict__ epoch_base) {
-  if (epoch_base != nullptr) epoch += *epoch_base;
+ordered_allgather_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, int p,
+                         const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                         const int64_t* __restrict__ bounds, uint32_t epoch) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
   uint8_t* mine = reinterpret_cast<uint8_t*>(bufs[rank]);
-  peer_barrier(sig, rank, p, 0, epoch);
+  peer_barrier(sig, c, p, 0, epoch, kSiteAllgather);
 #pragma unroll 1
   for (int d = 1; d < p; ++d) {
     const int r = (rank + d) % p;
     int64_t lo, hi;
-    split_range(bounds[r], bounds[r + 1], gridDim.x, blockIdx.x, 16, lo, hi);
+    split_range(bounds[r], bounds[r + 1], nb, c.lb, 16, lo, hi);
     copy_range(reinterpret_cast<const uint8_t*>(bufs[r]), mine, lo, hi);
   }
-  peer_barrier(sig, rank, p, 1, epoch);
+  peer_barrier(sig, c, p, 1, epoch, kSiteAllgather);
 }
 
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
 
 }  // namespace
 
+// validation shared by the peer entry points
+#define GS_PEER_ARGS(fn)                                                                       \
+  GS_REQUIRE(p >= 1 && p <= 8, fn ": 1 <= p <= 8 (got %d)", p);                                \
+  GS_REQUIRE(nranks >= 1 && nranks <= p, fn ": 1 <= nranks <= p (got %d)", nranks);            \
+  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, fn ": bad block count %d", nblocks);              \
+  GS_REQUIRE(epoch != 0, fn ": epoch 0 is the reset value")
+
 extern "C" {
 
-int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                             int64_t offset, int64_t n, uint32_t epoch,
-                             const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
-                             void* stream) {
-  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allreduce_f16: 1 <= p <= 8 (got %d)", p);
-  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allreduce_f16: bad rank %d", rank);
+int gs_ordered_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
+                             int nblocks, int push, void* stream) {
+  GS_PEER_ARGS("gs_ordered_allreduce_f16");
   GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_f16: negative size/offset");
-  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allreduce_f16: bad block count");
-  GS_REQUIRE(epoch != 0 || epoch_base != nullptr,
-             "gs_ordered_allreduce_f16: epoch 0 is the reset value");
   if (p == 1 || n == 0) return GS_OK;
-  GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_f16: null pointer");
+  GS_REQUIRE(ranks && bufs && sig, "gs_ordered_allreduce_f16: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  // every CTA waits for its counterparts on the peers, so the whole grid must
-  // be co-resident: clamp to what the occupancy calculator guarantees (the
-  // same on every rank of a homogeneous box, so the signal layout agrees)
-#define GS_OAR(P)                                                                                 \
-  case P: {                                                                                       \
-    int per_sm = 0, dev = 0, sms = 0;                                                             \
-    cudaGetDevice(&dev);                                                                          \
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                            \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_allreduce_kernel<P>, kThreads, 0); \
-    const int nb = per_sm > 0 ? min(nblocks, per_sm * sms) : 1;                                  \
-    ordered_allreduce_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,        \
-                                                        epoch_base, nonfinite);                   \
-    break;                                                                                        \
+#define GS_OAR(P)                                                                                \
+  case P: {                                                                                      \
+    if (push) {                                                                                  \
+      auto k = ordered_allreduce_kernel<P, true>;                                                \
+      const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                    \
+      k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);                \
+    } else {                                                                                     \
+      auto k = ordered_allreduce_kernel<P, false>;                                               \
+      const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                    \
+      k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);                \
+    }                                                                                            \
+    break;                                                                                       \
   }
   switch (p) {
     GS_OAR(2)
@@ -282,68 +269,19 @@ int gs_ordered_allreduce_f16(const uint64_t* bufs, const uint64_t* sig, int rank
   return gs_check_launch("gs_ordered_allreduce_f16");
 }
 
-int gs_ordered_allreduce_push_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                                  int64_t offset, int64_t n, uint32_t epoch,
-                                  const uint32_t* epoch_base, int nblocks, uint32_t* nonfinite,
-                                  void* stream) {
-  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allreduce_push_f16: 1 <= p <= 8 (got %d)", p);
-  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allreduce_push_f16: bad rank %d", rank);
-  GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_push_f16: negative size/offset");
-  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allreduce_push_f16: bad block count");
-  GS_REQUIRE(epoch != 0 || epoch_base != nullptr,
-             "gs_ordered_allreduce_push_f16: epoch 0 is the reset value");
-  if (p == 1 || n == 0) return GS_OK;
-  GS_REQUIRE(bufs && sig, "gs_ordered_allreduce_push_f16: null pointer");
-  cudaStream_t s = (cudaStream_t)stream;
-#define GS_OARP(P)                                                                                \
-  case P: {                                                                                       \
-    int per_sm = 0, dev = 0, sms = 0;                                                             \
-    cudaGetDevice(&dev);                                                                          \
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                            \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ordered_allreduce_push_kernel<P>,      \
-                                                  kThreads, 0);                                   \
-    const int nb = per_sm > 0 ? min(nblocks, per_sm * sms) : 1;                                  \
-    ordered_allreduce_push_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, offset, n, epoch,   \
-                                                             epoch_base, nonfinite);              \
-    break;                                                                                        \
-  }
-  switch (p) {
-    GS_OARP(2)
-    GS_OARP(3)
-    GS_OARP(4)
-    GS_OARP(5)
-    GS_OARP(6)
-    GS_OARP(7)
-    GS_OARP(8)
-  }
-#undef GS_OARP
-  return gs_check_launch("gs_ordered_allreduce_push_f16");
-}
-
-static int coresident_blocks(const void* kernel, int want) {
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-  return per_sm > 0 ? min(want, per_sm * sms) : 1;
-}
-
-int gs_ordered_reduce_scatter_f16(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                                  const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
-                                  int nblocks, uint32_t* nonfinite, void* stream) {
-  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_reduce_scatter_f16: 1 <= p <= 8 (got %d)", p);
-  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_reduce_scatter_f16: bad rank %d", rank);
-  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_reduce_scatter_f16: bad block count");
-  GS_REQUIRE(epoch != 0 || epoch_base != nullptr, "gs_ordered_reduce_scatter_f16: epoch 0");
+int gs_ordered_reduce_scatter_f16(const gs_rank_ctx* ranks, int nranks, int p,
+                                  const uint64_t* bufs, const uint64_t* sig, const int64_t* bounds,
+                                  uint32_t epoch, int nblocks, void* stream) {
+  GS_PEER_ARGS("gs_ordered_reduce_scatter_f16");
   if (p == 1) return GS_OK;
-  GS_REQUIRE(bufs && sig && bounds, "gs_ordered_reduce_scatter_f16: null pointer");
+  GS_REQUIRE(ranks && bufs && sig && bounds, "gs_ordered_reduce_scatter_f16: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-#define GS_ORS(P)                                                                                 \
-  case P: {                                                                                       \
-    const int nb = coresident_blocks((const void*)ordered_reduce_scatter_kernel<P>, nblocks);     \
-    ordered_reduce_scatter_kernel<P><<<nb, kThreads, 0, s>>>(bufs, sig, rank, bounds, epoch,      \
-                                                             epoch_base, nonfinite);              \
-    break;                                                                                        \
+#define GS_ORS(P)                                                                                \
+  case P: {                                                                                      \
+    auto k = ordered_reduce_scatter_kernel<P>;                                                   \
+    const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                      \
+    k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, bounds, epoch);                     \
+    break;                                                                                       \
   }
   switch (p) {
     GS_ORS(2)
@@ -358,18 +296,15 @@ int gs_ordered_reduce_scatter_f16(const uint64_t* bufs, const uint64_t* sig, int
   return gs_check_launch("gs_ordered_reduce_scatter_f16");
 }
 
-int gs_ordered_allgather(const uint64_t* bufs, const uint64_t* sig, int rank, int p,
-                         const int64_t* bounds, uint32_t epoch, const uint32_t* epoch_base,
-                         int nblocks, void* stream) {
-  GS_REQUIRE(p >= 1 && p <= 8, "gs_ordered_allgather: 1 <= p <= 8 (got %d)", p);
-  GS_REQUIRE(rank >= 0 && rank < p, "gs_ordered_allgather: bad rank %d", rank);
-  GS_REQUIRE(nblocks >= 1 && nblocks <= 1024, "gs_ordered_allgather: bad block count");
-  GS_REQUIRE(epoch != 0 || epoch_base != nullptr, "gs_ordered_allgather: epoch 0");
+int gs_ordered_allgather(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                         const uint64_t* sig, const int64_t* bounds, uint32_t epoch, int nblocks,
+                         void* stream) {
+  GS_PEER_ARGS("gs_ordered_allgather");
   if (p == 1) return GS_OK;
-  GS_REQUIRE(bufs && sig && bounds, "gs_ordered_allgather: null pointer");
-  const int nb = coresident_blocks((const void*)ordered_allgather_kernel, nblocks);
-  ordered_allgather_kernel<<<nb, kThreads, 0, (cudaStream_t)stream>>>(bufs, sig, rank, p, bounds,
-                                                                      epoch, epoch_base);
+  GS_REQUIRE(ranks && bufs && sig && bounds, "gs_ordered_allgather: null pointer");
+  const int nb = peer_grid((const void*)ordered_allgather_kernel, kThreads, 0, nblocks, nranks);
+  ordered_allgather_kernel<<<nb * nranks, kThreads, 0, (cudaStream_t)stream>>>(ranks, nb, p, bufs,
+                                                                               sig, bounds, epoch);
   return gs_check_launch("gs_ordered_allgather");
 }
 

@@ -16,20 +16,6 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 #ifndef GS_P1_MINB
 #define GS_P1_MINB 4     // pass-1 __launch_bounds__ min blocks per SM
 #endif
-#ifndef GS_P1_WIDEN
-// fp64 widening of the squared values in pass 1 (all forms give the same
-// double, so the sums are bit-identical): 0 = gradients and masters by
-// integer ops (masters after a warp-uniform subnormal test), the decayed
-// gradient by F2F; 1 = masters by F2F (XU pipe, exact for subnormals: no
-// subnormal test); 2 = gradients by F2F as well.  Measured on ResNet-50
-// (tools/pass1_variants.py, profiles/r01s_pass1_variants.log): 44.0 / 45.1 /
-// 41.0 us -- once the write of the wire copy is gone, dropping the
-// per-vector subnormal test and the integer widening wins; 3 = masters by
-// integer ops (after the subnormal test), gradients and decayed gradient by F2F.
-// Bench phases (profiles/r01u_pass1_widen_modes.log): pass 1 33.9-34.4 us for
-// mode 2, 35.8-35.9 for 3, 37.3 for 0 -- 2 stays the default
-#define GS_P1_WIDEN 2
-#endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
@@ -54,29 +40,9 @@ __device__ __forceinline__ void sq_acc(double& acc, float x) {
   acc = fma(d, d, acc);
 }
 
-// |x| widened to fp64 with integer ops (exact for normal floats and +-0;
-// NOT for subnormals; Inf/NaN map to garbage finite values, which only occurs
-// on steps the flags reject).  F2F.F64.F32 issues on the XU pipe at a quarter
-// of the ALU rate and was pass 1's co-limiter (ncu: XU 43 % busy), so the
-// squares of normal values are widened on the ALU instead.
-__device__ __forceinline__ double f2d_normal_abs(float x) {
-  const uint32_t a = __float_as_uint(x) & 0x7FFFFFFFu;
-  const uint32_t hi = a ? (a >> 3) + 0x38000000u : 0u;
-  return __hiloint2double((int)hi, (int)(a << 29));
-}
-
-__device__ __forceinline__ void sq_acc_int(double& acc, float x) {
-  const double d = f2d_normal_abs(x);
-  acc = fma(d, d, acc);
-}
-
-__device__ __forceinline__ bool is_subnormal_nonzero(float x) {
-  return (__float_as_uint(x) & 0x7FFFFFFFu) - 1u < 0x007FFFFFu;
-}
-
-// release-ordered arrival: the partials this thread stored become visible no
-// later than the counter increment (no full fence / L1 invalidate on the
-// common path; the rare last arriver fences before reading everyone's data)
+// release-ordered arrival: the values this thread stored become visible no
+// later than the counter increment (the last arriver fences before reading
+// everyone's data)
 __device__ __forceinline__ uint32_t arrive_release(uint32_t* p) {
   uint32_t old;
   asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
@@ -100,12 +66,13 @@ struct Acc {
 };
 
 // ------------------------------------------------------------ pass 1 body
-// One element pair (x = widened gradient, w = master).
-// GINT: gradients are widened for the squares with integer ops (fp16 input
-// with exact power-of-two scaling: every value is 0, normal, or non-finite).
-// WINT: the same for the masters (the caller checked for subnormals).
-template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool GINT = false,
-          bool WINT = false>
+// One element pair (x = widened gradient, w = master).  Every square is
+// widened by F2F.F64.F32 and accumulated with an fp64 fma (exact products,
+// fixed order): the integer widening forms measured slower on B200 (the ALU
+// pipe, not XU, became the limiter; profiles/r01u_pass1_widen_modes.log).
+// W2 = false: sum w^2 is not accumulated (pass 2 of the previous step
+// already produced it for this chunk, in this very order: w2_vec below).
+template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2 = true>
 __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& a) {
   float2 gu;
   if (POW2) {
@@ -123,10 +90,7 @@ __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& 
     a.fl |= (gs::is_finite_f32(gu.x) && gs::is_finite_f32(gu.y)) ? 0u : GS_FLAG_GRAD_NONFINITE;
   }
   if (LARS) {
-    if (WINT) {
-      sq_acc_int(a.sw, w.x);
-      sq_acc_int(a.sw, w.y);
-    } else {
+    if (W2) {
       sq_acc(a.sw, w.x);
       sq_acc(a.sw, w.y);
     }
@@ -138,13 +102,8 @@ __device__ __forceinline__ void p1_pair(float2 x, float2 w, const Ctx& cx, Acc& 
     }
   }
   if (GNORM || (LARS && !DECAY)) {
-    if (GINT) {
-      sq_acc_int(a.sg, gu.x);
-      sq_acc_int(a.sg, gu.y);
-    } else {
-      sq_acc(a.sg, gu.x);
-      sq_acc(a.sg, gu.y);
-    }
+    sq_acc(a.sg, gu.x);
+    sq_acc(a.sg, gu.y);
   }
 }
 
@@ -185,7 +144,7 @@ __device__ __forceinline__ float2 wpair(const F8& v, int q) {
        : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);
 }
 
-template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2 = true>
 __device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& wv, const Ctx& cx,
                                        Acc& a) {
   if (RAWFLAG) {
@@ -193,36 +152,26 @@ __device__ __forceinline__ void p1_vec(const typename G<F16>::V& gv, const F8& w
     a.raw |= raw_nonfinite_bits(r.x) | raw_nonfinite_bits(r.y) | raw_nonfinite_bits(r.z) |
              raw_nonfinite_bits(r.w);
   }
-  constexpr bool GINT = F16 && POW2 && GS_P1_WIDEN < 2;
-  constexpr bool WTEST = GS_P1_WIDEN == 0 || GS_P1_WIDEN == 3;
-  bool wsub = !WTEST;  // no test: masters always take the F2F path
-  if (LARS && WTEST) {
-    wsub = is_subnormal_nonzero(wv.a.x) | is_subnormal_nonzero(wv.a.y) |
-           is_subnormal_nonzero(wv.a.z) | is_subnormal_nonzero(wv.a.w) |
-           is_subnormal_nonzero(wv.b.x) | is_subnormal_nonzero(wv.b.y) |
-           is_subnormal_nonzero(wv.b.z) | is_subnormal_nonzero(wv.b.w);
-    wsub = __any_sync(__activemask(), wsub);  // warp-uniform: a subnormal master is rare
-  }
-  if (!wsub) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, true>(
-          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, GINT, false>(
-          G<F16>::pair(gv, q), LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx, a);
-  }
+  for (int q = 0; q < 4; ++q)
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(G<F16>::pair(gv, q),
+                                                   LARS ? wpair(wv, q) : make_float2(0.f, 0.f), cx,
+                                                   a);
 }
 
-template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY>
+// the vector path of pass 1 (the order its sums run in)
+template <bool LARS>
+__device__ __forceinline__ bool p1_vec_path(const void* g, const float* w) {
+  return gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w));
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2 = true>
 __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ g,
-                                         const float* __restrict__ w, uint16_t* __restrict__ gcopy,
-                                         int len, const Ctx& cx, Acc& a) {
+                                         const float* __restrict__ w, int len, const Ctx& cx,
+                                         Acc& a) {
   using Gt = G<F16>;
-  const bool vec = gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w)) &&
-                   (gcopy == nullptr || gs::is_aligned16(gcopy));
+  constexpr bool kW = LARS && (W2 || DECAY);  // does pass 1 read w at all
+  const bool vec = p1_vec_path<LARS>(g, w);
   const int nv = vec ? len / 8 : 0;
   const int t = threadIdx.x;
   // full batches of kRounds vectors per thread: issue every load of the
@@ -236,37 +185,31 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
     F8 wv[kP1Rounds];
 #pragma unroll
     for (int k = 0; k < kP1Rounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
-    if (LARS) {
+    if (kW) {
 #pragma unroll
       for (int k = 0; k < kP1Rounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
     }
-    if (F16 && gcopy != nullptr) {
 #pragma unroll
-      for (int k = 0; k < kP1Rounds; ++k)
-        reinterpret_cast<uint4*>(gcopy)[done + t + k * kThreads] = reinterpret_cast<const uint4&>(gv[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < kP1Rounds; ++k) p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv[k], wv[k], cx, a);
+    for (int k = 0; k < kP1Rounds; ++k)
+      p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(gv[k], kW ? wv[k] : F8{}, cx, a);
   }
   for (int i = done + t; i < nv; i += kThreads) {
     const typename Gt::V gv = Gt::ld(g + 8 * i);
     F8 wv{};
-    if (LARS) wv = ldw(w + 8 * i);
-    if (F16 && gcopy != nullptr) reinterpret_cast<uint4*>(gcopy)[i] = reinterpret_cast<const uint4&>(gv);
-    p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY>(gv, wv, cx, a);
+    if (kW) wv = ldw(w + 8 * i);
+    p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(gv, wv, cx, a);
   }
   // scalar tail (and misaligned segments): pair the element with a zero
   // partner that contributes nothing
   for (int i = nv * 8 + t; i < len; i += kThreads) {
     if (F16) {
-      const uint16_t h = reinterpret_cast<const uint16_t*>(g)[i];
-      if (gcopy != nullptr) gcopy[i] = h;
-      if (RAWFLAG) a.raw |= raw_nonfinite_bits(h);
+      if (RAWFLAG) a.raw |= raw_nonfinite_bits(reinterpret_cast<const uint16_t*>(g)[i]);
     }
     const float x = Gt::one(g + i);
-    const float wx = LARS ? w[i] : 0.0f;
+    const float wx = kW ? w[i] : 0.0f;
     Acc b;
-    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY>(make_float2(x, 0.0f), make_float2(wx, 0.0f), cx, b);
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(make_float2(x, 0.0f), make_float2(wx, 0.0f), cx,
+                                                   b);
     a.sw += b.sw;
     a.se += b.se;
     a.sg += b.sg;
@@ -278,28 +221,20 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
 // sqrt of the fp64 dots, local = (eta * w_norm) / (g_norm + eps) or 1.0 when
 // degenerate / LARS disabled, scale = float32(local * gamma).
 __device__ __forceinline__ void trust_eval(uint32_t sflags, double sw, double se, double sg,
-                                           const gs_step_params* __restrict__ params,
-                                           float* scale_out, double* o) {
+                                           const gs_step_params& params, float* scale_out,
+                                           double* o) {
   const double w_norm = __dsqrt_rn(sw);
   const double g_norm = __dsqrt_rn(se);
   double local = 1.0;
   if (sflags & GS_SEG_LARS_ENABLED) {
-    const double denom = __dadd_rn(g_norm, params->epsilon);
-    if (!(w_norm == 0.0 || denom == 0.0)) local = __ddiv_rn(__dmul_rn(params->eta, w_norm), denom);
+    const double denom = __dadd_rn(g_norm, params.epsilon);
+    if (!(w_norm == 0.0 || denom == 0.0)) local = __ddiv_rn(__dmul_rn(params.eta, w_norm), denom);
   }
-  *scale_out = __double2float_rn(__dmul_rn(local, params->gamma));
+  *scale_out = __double2float_rn(__dmul_rn(local, params.gamma));
   o[0] = w_norm;
   o[1] = g_norm;
   o[2] = local;
   o[3] = sg;
-}
-
-// experiment.py:408-411: sqrt(sum over groups of float(dot(g, g))), summed in
-// group order starting from 0.
-__device__ __forceinline__ double grad_norm_eval(const double* seg_out, int nseg) {
-  double acc = 0.0;
-  for (int s = 0; s < nseg; ++s) acc = __dadd_rn(acc, __ldcg(seg_out + 4 * (int64_t)s + 3));
-  return __dsqrt_rn(acc);
 }
 
 // ----------------------------------------------------------------- pass 2
@@ -318,6 +253,24 @@ __device__ __forceinline__ void p2_pair(float2 x, float2& w, float2& v, const Ct
   w = sub2(w, v);
 }
 
+// sum w^2 of the UPDATED masters in exactly pass 1's order (p1_vec: pairs
+// q = 0..3, x then y; the scalar tail pairs an element with a zero partner
+// and adds the pair sum), so the next step's pass 1 can take the chunk's sum
+// instead of re-deriving it (one F2F + DFMA less per LARS element there)
+__device__ __forceinline__ void w2_vec(const float2 (&ww)[4], double& s) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    sq_acc(s, ww[q].x);
+    sq_acc(s, ww[q].y);
+  }
+}
+__device__ __forceinline__ void w2_tail(float w, double& s) {
+  double b = 0.0;
+  sq_acc(b, w);
+  sq_acc(b, 0.0f);
+  s += b;
+}
+
 // binary16 pack with NaN canonicalisation for two lanes
 __device__ __forceinline__ uint32_t pack_w16(float2 w) {
   __half2 h = __floats2half2_rn(w.x, w.y);
@@ -327,16 +280,18 @@ __device__ __forceinline__ uint32_t pack_w16(float2 w) {
   return (bits & ~nan) | (0x7E007E00u & nan);
 }
 
-template <bool F16, bool POW2, bool DECAY>
+template <bool F16, bool POW2, bool DECAY, bool W2 = false>
 __device__ __forceinline__ void p2_vec(const typename G<F16>::V& gv, const F8& wv, const F8& vv,
                                        float* __restrict__ w, float* __restrict__ v,
-                                       uint16_t* __restrict__ w16, int i, const Ctx& cx, float s) {
+                                       uint16_t* __restrict__ w16, int i, const Ctx& cx, float s,
+                                       double* w2 = nullptr) {
   float2 ww[4] = {make_float2(wv.a.x, wv.a.y), make_float2(wv.a.z, wv.a.w),
                   make_float2(wv.b.x, wv.b.y), make_float2(wv.b.z, wv.b.w)};
   float2 xv[4] = {make_float2(vv.a.x, vv.a.y), make_float2(vv.a.z, vv.a.w),
                   make_float2(vv.b.x, vv.b.y), make_float2(vv.b.z, vv.b.w)};
 #pragma unroll
   for (int q = 0; q < 4; ++q) p2_pair<POW2, DECAY>(G<F16>::pair(gv, q), ww[q], xv[q], cx, s);
+  if (W2) w2_vec(ww, *w2);
   float4* vp = reinterpret_cast<float4*>(v) + 2 * i;
   float4* wp = reinterpret_cast<float4*>(w) + 2 * i;
   __stcs(vp, make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y));

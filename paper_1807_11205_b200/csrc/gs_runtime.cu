@@ -4,6 +4,14 @@
 
 #include "gs_common.cuh"
 
+// the Python mirrors (_native.py *_DTYPE) assert the same sizes
+static_assert(sizeof(gs_segment) == 64, "gs_segment layout");
+static_assert(sizeof(gs_chunk) == 16, "gs_chunk layout");
+static_assert(sizeof(gs_copy) == 24, "gs_copy layout");
+static_assert(sizeof(gs_step_params) == 56, "gs_step_params layout");
+static_assert(sizeof(gs_ctl) == 48, "gs_ctl layout");
+static_assert(sizeof(gs_rank_ctx) == 96, "gs_rank_ctx layout");
+
 static thread_local char g_err[512] = "";
 
 void gs_set_error(const char* fmt, ...) {

@@ -156,16 +156,33 @@ class Communicator:
         """Hybrid rule (collectives.py:238-244) mapped onto the variants."""
         return hier_variant if choose_algorithm(nbytes, eta_bytes) == "hierarchical" else flat_variant
 
+    # -- peer-memory plumbing of the own-kernel paths (emulation.LocalComm
+    # provides the same three on one device)
+    emulated = False
+    #: CTAs per rank of the peer kernels (None: the pipeline's default)
+    peer_ctas = None
+    #: bound of every device-side peer wait (gs_rank_ctx.timeout_ns)
+    timeout_s = 120.0
+
+    def make_arena(self, regions: dict, device, sig_words: int) -> "SymmetricArena":
+        return SymmetricArena(self, regions, device, sig_words)
+
+    def make_ordered_wire(self, total: int, device, push: bool = False) -> "OrderedWire":
+        return OrderedWire(self, total, device, push=push)
+
 
 class OrderedWire:
     """Double-buffered symmetric-memory wire for the bit-exact ordered
     all-reduce (gs_ordered_allreduce_f16): one allocation per rank,
-    [wire A | wire B | signal area], exchanged once through torch's
+    [wire A | wire B | signal area | control], exchanged once through torch's
     symmetric-memory rendezvous so every rank holds every peer's NVLink-mapped
     base address.  Both halves have the pipeline's wire layout, so a bucket is
-    the same element range in every rank's buffer."""
+    the same element range in every rank's buffer.  `push` selects the push
+    form of the kernel (fold + remote stores, one exit barrier) over the pull
+    form (fold, barrier, gather by remote loads); same result bit for bit."""
 
-    def __init__(self, comm: "Communicator", total: int, device, nblocks: int | None = None):
+    def __init__(self, comm: "Communicator", total: int, device, nblocks: int | None = None,
+                 push: bool = False):
         import numpy as np
         import torch.distributed._symmetric_memory as symm
 
@@ -176,32 +193,40 @@ class OrderedWire:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         # all CTAs must be co-resident (they wait on their peers' CTAs): two
         # 512-thread CTAs per SM fit next to anything else that is running
-        self.nblocks = nblocks or 2 * sms
+        self.nblocks = nblocks or comm.peer_ctas or 2 * sms
         self.total = (total + 255) // 256 * 256
         sig_words = 2 * self.nblocks * self.p
         sig_elems = (4 * sig_words + 1) // 2 + 256
-        self.buf = symm.empty(2 * self.total + sig_elems, dtype=torch.uint16, device=device)
+        self.buf = symm.empty(2 * self.total + sig_elems + 64, dtype=torch.uint16, device=device)
         self.buf.zero_()
         torch.cuda.synchronize(device)
         self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
         bases = [int(x) for x in self.hdl.buffer_ptrs]
+        self._setup(bases, device, push, comm.timeout_s)
+        dist.barrier()
+
+    def _setup(self, bases, device, push: bool, timeout_s: float) -> None:
+        """Tables and this rank's context from every rank's base address
+        (shared with emulation.LocalOrderedWire)."""
+        import numpy as np
+
+        from . import _device as dev
+        from ._peer import rank_ctx
+
         self.halves = (self.buf[: self.total], self.buf[self.total: 2 * self.total])
-        tabs = []
-        for h in range(2):
-            tabs.append(dev.upload(np.array([b + 2 * h * self.total for b in bases],
-                                            dtype=np.uint64), device))
-        self.bufs_dev = tabs
+        self.bufs_dev = [dev.upload(np.array([b + 2 * h * self.total for b in bases],
+                                             dtype=np.uint64), device) for h in range(2)]
         self.sig_dev = dev.upload(np.array([b + 4 * self.total for b in bases], dtype=np.uint64),
                                   device)
         # device-resident epoch base: every call of a step uses base + slot,
-        # and advance() bumps the base once per step on the stream, so the
-        # kernels can be captured into a CUDA graph and replayed
+        # and advance() bumps the base once per step on the stream
         self.epoch_base = torch.zeros(1, dtype=torch.int32, device=device)
-        self.slots = 0
-        # push form (fold + remote stores, one exit barrier) vs pull form
-        # (fold, barrier, gather by remote loads); same result bit for bit
-        self.push = os.environ.get("GS_ORDERED_PUSH", "0") == "1"
-        dist.barrier()
+        # status word (a timed-out peer wait is reported here) at the tail
+        self.status = self.buf[-64:].view(torch.int32)
+        self.ctx = rank_ctx(self.rank, timeout_s=timeout_s, status=dev.ptr(self.status),
+                            epoch_base=dev.ptr(self.epoch_base))
+        self.push = bool(push)
+        self.device = device
 
     #: elements per CTA below which a call uses fewer CTAs: a small bucket
     #: then pays the barriers of a few CTAs instead of the whole co-resident
@@ -212,16 +237,20 @@ class OrderedWire:
     def grid_for(self, n: int) -> int:
         return max(1, min(self.nblocks, -(-int(n) // self.MIN_ELEMS_PER_CTA)))
 
-    def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
-        """Bucket all-reduce; `slot` (1-based within the step, < per_step)
-        makes the epoch unique among the step's calls."""
+    def allreduce_op(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0):
+        """The bucket all-reduce as a peer op; `slot` (0-based within the
+        step, < per_step) makes the epoch unique among the step's calls."""
         from . import _device as dev
-        from . import _native
+        from ._peer import PeerOp
 
-        _native.call("gs_ordered_allreduce_push_f16" if self.push else "gs_ordered_allreduce_f16",
-                     dev.ptr(self.bufs_dev[half]),
-                     dev.ptr(self.sig_dev), self.rank, self.p, offset, n, slot + 1,
-                     dev.ptr(self.epoch_base), self.grid_for(n), None, stream_h)
+        return PeerOp("gs_ordered_allreduce_f16", self.ctx,
+                      (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
+                       slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
+                      device=self.device)
+
+    def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
+        from ._peer import launch
+        launch([self.allreduce_op(half, offset, n, stream_h, slot)])
 
     def advance(self, per_step: int, stream_h: int) -> None:
         from . import _device as dev
@@ -229,54 +258,54 @@ class OrderedWire:
 
         _native.call("gs_counter_add", dev.ptr(self.epoch_base), per_step, stream_h)
 
+    def status_word(self) -> int:
+        return int(self.status[0].item())
+
 
 class SymmetricArena:
     """One symmetric-memory allocation per rank carved into named regions
     (byte sizes given up front), plus device tables of every peer's address
     of each region — the building block of the sharded (ZeRO-1) update, in
     which the wire, the binary16 working weights, the masters, the
-    velocities, the LARS chunk partials and the step flags are all reachable
-    by every peer over NVLink."""
+    velocities, the LARS chunk partials and the control block (step flags)
+    are all reachable by every peer over NVLink."""
 
     ALIGN = 512
 
     def __init__(self, comm: "Communicator", regions: dict, device, sig_words: int):
-        import numpy as np
         import torch.distributed._symmetric_memory as symm
 
-        from . import _device as dev
-
         self.p, self.rank = comm.topo.p, comm.rank
+        self.layout(regions, sig_words)
+        self.buf = symm.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        torch.cuda.synchronize(device)
+        self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
+        self.bases = [int(x) for x in self.hdl.buffer_ptrs]
+        self.tables(device)
+        dist.barrier()
+
+    def layout(self, regions: dict, sig_words: int) -> None:
         self.offsets, off = {}, 0
         for name, nbytes in list(regions.items()) + [("sig", 4 * sig_words)]:
             self.offsets[name] = off
             off += (int(nbytes) + self.ALIGN - 1) // self.ALIGN * self.ALIGN
         self.sizes = dict(regions, sig=4 * sig_words)
-        self.buf = symm.empty(off, dtype=torch.uint8, device=device)
-        self.buf.zero_()
-        torch.cuda.synchronize(device)
-        self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
-        self.bases = [int(x) for x in self.hdl.buffer_ptrs]
-        # NVLS multicast mapping of the whole window (0 when the box has no
-        # NVSwitch multicast): a store to mc_base + off lands at off in every
-        # rank's window
-        try:
-            self.mc_base = int(self.hdl.multicast_ptr or 0)
-        except (AttributeError, RuntimeError):
-            self.mc_base = 0
+        self.nbytes = off
+
+    def tables(self, device) -> None:
+        import numpy as np
+
+        from . import _device as dev
+
         self._tabs = {}
         for name in self.offsets:
             self._tabs[name] = dev.upload(
                 np.array([b + self.offsets[name] for b in self.bases], dtype=np.uint64), device)
-        dist.barrier()
 
     def view(self, name: str, dtype: torch.dtype) -> torch.Tensor:
         o, n = self.offsets[name], self.sizes[name]
         return self.buf[o:o + n].view(dtype)
-
-    def multicast(self, name: str) -> int | None:
-        """Multicast address of region `name` (None without NVLS support)."""
-        return self.mc_base + self.offsets[name] if self.mc_base else None
 
     def peers(self, name: str) -> torch.Tensor:
         """Device uint64[p]: every rank's address of region `name`."""

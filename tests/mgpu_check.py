@@ -88,9 +88,7 @@ def main():
                 wires[world - 1][4321] = 0x7C00
             flat = torch.from_numpy(wires[rank]).to(dev)
             if host:
-                os.environ["GS_HOST_INCREMENTAL"] = "1"
                 pipe.enqueue_host(torch.from_numpy(wires[rank]).pin_memory(), step)
-                os.environ.pop("GS_HOST_INCREMENTAL")
                 res = pipe.finish()
             elif inc:
                 views = split(flat, specs)

@@ -37,12 +37,20 @@ def test_every_declared_symbol_is_exported_and_bound():
 
 def test_abi_version_and_errors_without_gpu():
     lib = _native.load()
-    assert lib.gs_abi_version() == 1
+    assert lib.gs_abi_version() == _native.ABI_VERSION == 2
     # argument validation happens before any launch
     assert lib.gs_f32_to_f16(None, None, -1, 1.0, None, None) == -1
     assert b"negative" in lib.gs_last_error()
     assert lib.gs_fold_f16_tree(None, 0, 0, None, 4, None, None) == -1
-    assert lib.gs_lars_pass1(None, None, 0, -1, 1, None, 0, None, None, None) == -1
+    assert lib.gs_lars_pass1(None, None, 0, -1, 1, _native.StepParams(), 0, None, None, 0,
+                             None, None) == -1
+    # peer launches validate before touching the rank table
+    assert lib.gs_rs_pass1(None, 1, 3, None, None, None, None, 0, 1, _native.StepParams(), 0, 0,
+                           1, 8, None) == -1
+    assert b"p must be 2, 4 or 8" in lib.gs_last_error()
+    assert lib.gs_ordered_allreduce_f16(None, 1, 2, None, None, 0, 16, 0, 8, 0, None) == -1
+    assert b"epoch 0" in lib.gs_last_error()
+    assert lib.gs_peer_fence(None, 3, 2, None, 1, None) == -1
 
 
 def test_struct_layouts_match_header():
@@ -50,7 +58,9 @@ def test_struct_layouts_match_header():
     for dt, name, size in ((_native.SEGMENT_DTYPE, "gs_segment", 64),
                            (_native.CHUNK_DTYPE, "gs_chunk", 16),
                            (_native.COPY_DTYPE, "gs_copy", 24),
-                           (_native.STEP_PARAMS_DTYPE, "gs_step_params", 56)):
+                           (_native.STEP_PARAMS_DTYPE, "gs_step_params", 56),
+                           (_native.CTL_DTYPE, "gs_ctl", 48),
+                           (_native.RANK_CTX_DTYPE, "gs_rank_ctx", 96)):
         assert dt.itemsize == size
         assert re.search(rf"}}\s*{name};\s*/\*\s*{size} bytes", text), name
     m = {k: int(v, 0) for k, v in re.findall(r"#define (GS_[A-Z0-9_]+) (\d+|0x[0-9a-f]+)u?", text)}
@@ -82,6 +92,6 @@ def test_no_packed_fp32_contraction_in_sass():
         assert op not in sass
     # pass-2 specialisation for power-of-two scaling: pure FMUL/FADD
     funcs = sass.split("Function : ")
-    p2 = [f for f in funcs if "lars_pass2_kernelILb1ELb1ELb0E" in f.split("\n", 1)[0]]
+    p2 = [f for f in funcs if "lars_pass2_kernelILb1ELb1EE" in f.split("\n", 1)[0]]
     assert p2, "pow2 pass-2 kernel missing"
     assert "FFMA" not in p2[0]

@@ -1,12 +1,14 @@
 """Backward-overlap driver (overlap.py): buckets launched from
-autograd hooks during backward must give bit-for-bit the state
-GradientPipeline.step() gives on the same gradients, including a skipped
-(overflow) step, and the model's fp16 weights must be the working arena."""
+autograd hooks during backward must give bit-for-bit the state the CPU oracle
+(the reference's step composition, experiment.py:368-413 on the fp16 wire)
+computes from the same hooked gradients, including a skipped (overflow) step,
+and the model's fp16 weights must be the working arena."""
 
 import numpy as np
 import pytest
 import torch
 
+from oracle import reference_port as rp
 import paper_1807_11205_b200 as gs
 
 pytestmark = pytest.mark.gpu
@@ -33,10 +35,14 @@ def _setup(theta):
     cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
     drv = gs.BackwardOverlap.for_module(net, cfg, threshold_bytes=theta,
                                         loss_scale=gs.LossScale(1024.0))
-    master = drv.pipe.registration_view(drv.pipe.master).clone()
-    ref = gs.GradientPipeline(drv.pipe.specs, cfg, threshold_bytes=theta, init_master=master,
-                              loss_scale=gs.LossScale(1024.0))
-    return net, drv, ref
+    master = drv.pipe.registration_view(drv.pipe.master).cpu().numpy()
+    groups, o = [], 0
+    for s in drv.pipe.specs:
+        w = master[o:o + s.numel].copy()
+        groups.append(rp.Group(s.name, s.kind, w, np.zeros(s.numel, np.float32),
+                               np.zeros(s.numel, np.float32), rp.narrow(w)))
+        o += s.numel
+    return net, drv, groups
 
 
 def _bits(t):
@@ -44,8 +50,10 @@ def _bits(t):
 
 
 @pytest.mark.parametrize("theta", [0, 2048, 1 << 30])
-def test_overlap_matches_step(theta):
-    net, drv, ref = _setup(theta)
+def test_overlap_matches_oracle(theta):
+    net, drv, groups = _setup(theta)
+    specs = drv.pipe.specs
+    oloss = rp.LossScaleState(1024.0)
     assert drv.pipe.specs[0].kind == "weight" and drv.pipe.specs[1].kind == "bn_gamma"
     assert drv.pipe.specs[2].kind == "bn_beta" and drv.pipe.specs[-1].kind == "bias"
     seen = {}
@@ -67,15 +75,19 @@ def test_overlap_matches_step(theta):
         if inf_hook is not None:
             inf_hook.remove()
             inf_hook = None
-        grads = [seen[i] for i in range(len(drv.params))]
-        want = ref.step(grads, step)
-        assert (res.applied, res.scale, res.flags) == (want.applied, want.scale, want.flags)
-        assert res.grad_norm == want.grad_norm
+        grads = [seen[i].cpu().numpy().reshape(-1) for i in range(len(drv.params))]
+        want = rp.compose_step_fp16([grads], [s.name for s in specs], [s.numel for s in specs],
+                                    list(reversed(range(len(specs)))), groups,
+                                    rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1, oloss, theta, 0)
+        assert (res.applied, res.scale) == (want.applied, want.scale_used)
+        assert drv.pipe.loss_scale.scale == oloss.scale
+        assert res.grad_norm == pytest.approx(want.grad_norm, rel=1e-12)
         assert res.applied == (step != 2)
-        for name in ("master", "velocity", "working"):
-            a = ref.registration_view(getattr(ref, name))
-            b = drv.pipe.registration_view(getattr(drv.pipe, name))
-            assert np.array_equal(_bits(a), _bits(b)), f"step {step}: {name} differs"
+        for name, attr in (("master", "master"), ("velocity", "velocity"),
+                           ("working", "working")):
+            a = np.concatenate([getattr(g, attr) for g in groups])
+            b = _bits(drv.pipe.registration_view(getattr(drv.pipe, name)))
+            assert np.array_equal(a.view(b.dtype), b), f"step {step}: {name} differs"
         # the model's weights ARE the working arena
         flat = torch.cat([p.detach().reshape(-1) for p in drv.params]).view(torch.uint16)
         assert torch.equal(flat, drv.pipe.registration_view(drv.pipe.working))

@@ -119,12 +119,13 @@ def run_vs_oracle(model, p, theta, steps=2, loss_scale=1024.0, wd=5e-4, eta_byte
     return pipe
 
 
-@pytest.mark.parametrize("kw", [{}, {"trust_in_pass2": True}, {"bulk": True},
-                                {"fuse_trust": True}, {"bulk": True, "fuse_trust": True},
-                                {"fused_pack": False}, {"use_graph": False}])
-def test_resnet50_single_gpu_matches_oracle(kw):
-    pipe = run_vs_oracle("resnet50", 1, 4 << 20, steps=3, **kw)
-    # the fused packer left the reference's bucket payloads in the wire
+@pytest.mark.parametrize("theta", [4 << 20, 16 << 20])
+@pytest.mark.parametrize("kw", [{}, {"snapshot_wire": True}])
+def test_resnet50_single_gpu_matches_oracle(kw, theta):
+    """The bench configuration (theta = 16 MiB) and theta = 4 MiB; lazy wire
+    (payloads packed on request) and the in-step snapshot."""
+    pipe = run_vs_oracle("resnet50", 1, theta, steps=3, **kw)
+    # the wire holds the reference's bucket payloads of the last step
     specs = sh.load_shapes("resnet50")
     flat = sh.synth_wire_grads(specs, rank=0, seed=2)
     parts = split(flat, specs)

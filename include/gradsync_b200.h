@@ -227,6 +227,18 @@ int gs_ordered_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const 
                              const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
                              int nblocks, int push, void* stream);
 
+/* The same all-reduce over Topology(p, k)'s two levels (
+ * hierarchical_schedule, collectives.py:183-235): an intra-group
+ * reduce-scatter (each member folds its slice over the group's k raw
+ * copies), an inter-group fold of each sub-slice over the p/k same-offset
+ * group partials, then the all-gather.  For power-of-two k the reference's
+ * rank tree factors exactly this way, so the result equals
+ * gs_ordered_allreduce_f16's bit for bit.  Signal areas need >= 3 * nblocks
+ * * p words.  k in {2, 4, 8}, p <= 8. */
+int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
+                          const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
+                          uint32_t epoch, int nblocks, void* stream);
+
 /* Reduce-scatter half of the above with explicit slices: rank r folds
  * elements [bounds[r], bounds[r+1]) (device int64 array of p + 1 offsets)
  * of every peer's buffer into its own, in the reference's tree order.  Used

@@ -54,20 +54,28 @@ def _fingerprint() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every csrc/*.cu for sm_100a and link the shared library."""
-    stamp = LIBDIR / ".fingerprint"
-    fp = _fingerprint()
-    if not force and LIBPATH.exists() and stamp.exists() and stamp.read_text() == fp:
-        return LIBPATH
-    LIBDIR.mkdir(exist_ok=True)
-    objdir = LIBDIR / "obj"
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> Path:
+    """Compile every csrc/*.cu for sm_100a and link the shared library.
+
+    variant/defines: a tuning build (extra -D flags) linked to
+    _lib/variants/libgradsync_b200_<variant>.so for A/B measurements (load
+    it with GRADSYNC_B200_LIB); the product library is untouched."""
+    libdir = LIBDIR / "variants" if variant else LIBDIR
+    libpath = libdir / (f"libgradsync_b200_{variant}.so" if variant else LIBNAME)
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
+    stamp = libdir / (f".fingerprint_{variant}" if variant else ".fingerprint")
+    fp = _fingerprint() + " ".join(defines)
+    if not force and libpath.exists() and stamp.exists() and stamp.read_text() == fp:
+        return libpath
+    libdir.mkdir(parents=True, exist_ok=True)
+    objdir = libdir / (f"obj_{variant}" if variant else "obj")
     objdir.mkdir(exist_ok=True)
     nvcc = _nvcc()
     objs, cmds = [], []
     for src in _sources():
         obj = objdir / (src.stem + ".o")
-        cmds.append([nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)])
+        cmds.append([nvcc, *flags, "-c", str(src), "-o", str(obj)])
         objs.append(str(obj))
     # one nvcc per translation unit, concurrently (the LARS unit dominates)
     procs = []
@@ -78,14 +86,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     failed = [cmd for cmd, pr in procs if pr.wait() != 0]
     if failed:
         raise subprocess.CalledProcessError(1, failed[0])
-    tmp = LIBDIR / (LIBNAME + ".tmp")
+    tmp = libdir / (libpath.name + ".tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
            "-cudart", "static", "-o", str(tmp), *objs]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIBPATH)
+    os.replace(tmp, libpath)
     stamp.write_text(fp)
-    return LIBPATH
+    return libpath
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_1807_11205_b200._build [--force] [--variant NAME -DMACRO=V ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args, verbose=True, variant=var, defines=defs))

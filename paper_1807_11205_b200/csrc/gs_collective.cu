@@ -222,6 +222,76 @@ ordered_allgather_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, int p,
   peer_barrier(sig, c, p, 1, epoch, kSiteAllgather);
 }
 
+// Hierarchical form for Topology(p = K*G, K) with K a power of two: the
+// reference's pairwise tree over ranks 0..p-1 then factors into a tree over
+// the K members of each group (its first log2(K) levels) followed by a tree
+// over the G group partials (the remaining levels, odd tail carried the same
+// way), so the paper's two-level exchange (collectives.py:
+// 183-235) reproduces allreduce_f16 bit for bit.  The bucket is cut into p
+// sub-slices u = j*G + g; rank (g, j) = g*K + j owns sub-slice j*G + g.
+//   A  barrier (every rank's raw wire is packed)
+//   B  intra-group reduce-scatter: rank (g, j) folds slice j (its group's
+//      sub-slices j*G .. j*G+G-1) over the K members' raw values, in place
+//   C  barrier; inter-group: rank (g, j) folds its own sub-slice over the G
+//      same-offset ranks' group partials, in place
+//   D  barrier; all-gather of the p final sub-slices by peer loads
+// Every phase works on piece lb of each sub-slice, so CTA lb only ever reads
+// what CTA lb of its peers wrote and the per-CTA barriers suffice.  Same
+// inbound volume as the flat ring, 2(p-1)/p * S; no exit barrier (the wire
+// is double-buffered across calls, as for the flat kernel).
+template <int K, int G>
+__global__ void __launch_bounds__(kThreads)
+hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                      const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                      int64_t offset, int64_t n, uint32_t epoch) {
+  constexpr int P = K * G;
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  const int g = rank / K, j = rank % K;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+  peer_barrier(sig, c, P, 0, epoch, kSiteHierarchical);  // A
+  uint32_t bad = 0;
+  {  // B: slice j over the group's members, member order
+    const uint16_t* grp[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) grp[m] = reinterpret_cast<const uint16_t*>(bufs[g * K + m]) + offset;
+#pragma unroll 1
+    for (int gp = 0; gp < G; ++gp) {
+      int64_t lo, hi;
+      subrange(n, P, j * G + gp, nb, c.lb, lo, hi);
+      fold_range<K>(grp, mine, lo, hi, bad);
+    }
+  }
+  if (G > 1) {
+    peer_barrier(sig, c, P, 1, epoch, kSiteHierarchical);  // C
+    bad = 0;
+    const uint16_t* crs[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) crs[q] = reinterpret_cast<const uint16_t*>(bufs[q * K + j]) + offset;
+    int64_t lo, hi;
+    subrange(n, P, j * G + g, nb, c.lb, lo, hi);
+    fold_range<G>(crs, mine, lo, hi, bad);
+  } else {
+    // one group: the group partial of sub-slice j is the final value
+    int64_t lo, hi;
+    subrange(n, P, j, nb, c.lb, lo, hi);
+    bad = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) bad |= (mine[i] & 0x7C00u) == 0x7C00u;
+  }
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+  peer_barrier(sig, c, P, 2, epoch, kSiteHierarchical);  // D
+#pragma unroll 1
+  for (int d = 1; d < P; ++d) {
+    const int r = (rank + d) % P;
+    int64_t lo, hi;
+    subrange(n, P, (r % K) * G + r / K, nb, c.lb, lo, hi);
+    copy_range(reinterpret_cast<const uint8_t*>(bufs[r]) + 2 * offset,
+               reinterpret_cast<uint8_t*>(mine), 2 * lo, 2 * hi);
+  }
+}
+
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
 
 }  // namespace
@@ -306,6 +376,36 @@ int gs_ordered_allgather(const gs_rank_ctx* ranks, int nranks, int p, const uint
   ordered_allgather_kernel<<<nb * nranks, kThreads, 0, (cudaStream_t)stream>>>(ranks, nb, p, bufs,
                                                                                sig, bounds, epoch);
   return gs_check_launch("gs_ordered_allgather");
+}
+
+int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
+                          const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
+                          uint32_t epoch, int nblocks, void* stream) {
+  GS_PEER_ARGS("gs_hier_allreduce_f16");
+  GS_REQUIRE(k == 2 || k == 4 || k == 8, "gs_hier_allreduce_f16: group size k must be 2, 4 or 8 "
+             "(the reference tree factors over groups only for power-of-two k; got %d)", k);
+  GS_REQUIRE(p % k == 0, "gs_hier_allreduce_f16: k=%d does not divide p=%d", k, p);
+  GS_REQUIRE(n >= 0 && offset >= 0, "gs_hier_allreduce_f16: negative size/offset");
+  if (n == 0) return GS_OK;
+  GS_REQUIRE(ranks && bufs && sig, "gs_hier_allreduce_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  bool done = false;
+#define GS_HAR(K, G)                                                                             \
+  if (!done && k == K && p == K * G) {                                                           \
+    auto kern = hier_allreduce_kernel<K, G>;                                                     \
+    const int nb = peer_grid((const void*)kern, kThreads, 0, nblocks, nranks);                   \
+    kern<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);               \
+    done = true;                                                                                 \
+  }
+  GS_HAR(2, 1)
+  GS_HAR(2, 2)
+  GS_HAR(2, 3)
+  GS_HAR(2, 4)
+  GS_HAR(4, 1)
+  GS_HAR(4, 2)
+  GS_HAR(8, 1)
+#undef GS_HAR
+  return gs_check_launch("gs_hier_allreduce_f16");
 }
 
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream) {

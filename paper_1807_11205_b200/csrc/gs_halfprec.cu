@@ -66,6 +66,12 @@ f32_to_f16_kernel(const float* __restrict__ x, uint16_t* __restrict__ h, int64_t
   if (nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
+// f16_to_f32's NaN is numpy's float32 NaN, 0x7FC00000, whatever the binary16
+// payload or sign (halfprec.py:103-104); cvt.f32.f16 would keep both
+__device__ __forceinline__ float canon(float x) {
+  return x != x ? __uint_as_float(0x7FC00000u) : x;
+}
+
 __global__ void __launch_bounds__(kThreads)
 f16_to_f32_kernel(const uint16_t* __restrict__ h, float* __restrict__ x, int64_t n, int vec) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -77,12 +83,14 @@ f16_to_f32_kernel(const uint16_t* __restrict__ h, float* __restrict__ x, int64_t
       const uint4 a = reinterpret_cast<const uint4*>(h)[i];
       const float2 p0 = gs::widen2(a.x), p1 = gs::widen2(a.y), p2 = gs::widen2(a.z),
                    p3 = gs::widen2(a.w);
-      reinterpret_cast<float4*>(x)[2 * i] = make_float4(p0.x, p0.y, p1.x, p1.y);
-      reinterpret_cast<float4*>(x)[2 * i + 1] = make_float4(p2.x, p2.y, p3.x, p3.y);
+      reinterpret_cast<float4*>(x)[2 * i] =
+          make_float4(canon(p0.x), canon(p0.y), canon(p1.x), canon(p1.y));
+      reinterpret_cast<float4*>(x)[2 * i + 1] =
+          make_float4(canon(p2.x), canon(p2.y), canon(p3.x), canon(p3.y));
     }
     tail_begin = nv * 8;
   }
-  for (int64_t i = tail_begin + tid; i < n; i += stride) x[i] = gs::widen(h[i]);
+  for (int64_t i = tail_begin + tid; i < n; i += stride) x[i] = canon(gs::widen(h[i]));
 }
 
 __global__ void __launch_bounds__(kThreads)

@@ -36,62 +36,183 @@
 
 namespace {
 
-// 64 registers (4 CTAs/SM) for the power-of-two forms; the IEEE-division
-// forms (non-power-of-two p or loss scale) get 128 so nothing spills
-template <bool F16, bool POW2, bool RAWFLAG, bool GNORM>
-__global__ void __launch_bounds__(kThreads, F16 && POW2 ? GS_P1_MINB : 2)
-lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
-                  int chunk0, const gs_step_params params, double* __restrict__ partials,
-                  gs_ctl* __restrict__ ctl, uint32_t parity, const double* __restrict__ wsq) {
+// ------------------------------------------------------------------ pass 1
+// Persistent, software-pipelined: CTA b handles chunks b, b + grid, ... and
+// per chunk (one 8192-element batch: 4 vectors of g and of w per thread)
+//   compute the batch it already holds   | the NEXT chunk's table entries
+//   issue the next chunk's loads          |   (issued before the compute)
+//   block-reduce + store this chunk's partials while those loads fly,
+// so neither the chunk -> segment table lookups nor the reduction sit on the
+// memory critical path (one CTA per chunk spent ~40 % of its life there).
+// Per-thread vector order t, t+256, t+512, t+768, then the scalar tail: the
+// summation order of every other pass-1 form (rs_pass1, p1_chunk), so the
+// partials are bit-identical.
+struct P1Meta {
+  const void* g;
+  const float* w;
+  double wc;  // sum w^2 left by the previous pass 2 (NaN: not available)
+  int len, c;
+  uint32_t sflags;
+};
+
+template <bool F16>
+__device__ __forceinline__ P1Meta p1_meta(const gs_segment* __restrict__ segs,
+                                          const gs_chunk* __restrict__ chunks, int c,
+                                          const double* __restrict__ wsq) {
   using T = typename G<F16>::T;
-  const int c = chunk0 + blockIdx.x;
+  P1Meta m;
+  m.c = c;
+  m.wc = wsq != nullptr ? wsq[c] : __longlong_as_double(0x7FF8000000000000ll);
   const gs_chunk ch = chunks[c];
-  const gs_segment* sgp = segs + ch.seg;
-  const uint32_t sflags = sgp->flags;
-  const T* g = static_cast<const T*>(sgp->g) + ch.start;
-  const float* w = sgp->w + ch.start;
+  const gs_segment* sp = segs + ch.seg;
+  m.g = static_cast<const T*>(sp->g) + ch.start;
+  m.w = sp->w + ch.start;
+  m.len = ch.len;
+  m.sflags = sp->flags;
+  return m;
+}
+
+template <bool F16>
+struct P1Batch {
+  typename G<F16>::V gv[kP1Rounds];
+  F8 wv[kP1Rounds];
+};
+
+// does the chunk take the register-batched vector path (else p1_chunk)
+template <bool F16>
+__device__ __forceinline__ bool p1_batched(const P1Meta& m) {
+  const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
+  return m.len <= kThreads * 8 * kP1Rounds &&
+         (lars ? p1_vec_path<true>(m.g, m.w) : p1_vec_path<false>(m.g, m.w));
+}
+
+template <bool F16>
+__device__ __forceinline__ void p1_issue(const P1Meta& m, P1Batch<F16>& bt) {
+  using Gt = G<F16>;
+  if (!p1_batched<F16>(m)) return;
+  const int nv = m.len / 8, t = threadIdx.x;
+  const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
+  const typename Gt::T* g = static_cast<const typename Gt::T*>(m.g);
+#pragma unroll
+  for (int k = 0; k < kP1Rounds; ++k)
+    if (t + k * kThreads < nv) bt.gv[k] = Gt::ld(g + 8 * (t + k * kThreads));
+  if (lars) {
+#pragma unroll
+    for (int k = 0; k < kP1Rounds; ++k)
+      if (t + k * kThreads < nv) bt.wv[k] = ldw(m.w + 8 * (t + k * kThreads));
+  }
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2>
+__device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& bt, const Ctx& cx,
+                                           Acc& a) {
+  using Gt = G<F16>;
+  if (!p1_batched<F16>(m)) {  // misaligned / oversized: the generic loop
+    p1_chunk<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(
+        static_cast<const typename Gt::T*>(m.g), m.w, m.len, cx, a);
+    return;
+  }
+  const int nv = m.len / 8, t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < kP1Rounds; ++k)
+    if (t + k * kThreads < nv)
+      p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(bt.gv[k], LARS ? bt.wv[k] : F8{}, cx, a);
+  // scalar tail, exactly as p1_chunk's
+  const typename Gt::T* g = static_cast<const typename Gt::T*>(m.g);
+  for (int i = nv * 8 + t; i < m.len; i += kThreads) {
+    if (F16 && RAWFLAG) a.raw |= raw_nonfinite_bits(reinterpret_cast<const uint16_t*>(g)[i]);
+    Acc b;
+    p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(make_float2(Gt::one(g + i), 0.0f),
+                                                   make_float2(LARS ? m.w[i] : 0.0f, 0.0f), cx, b);
+    a.sw += b.sw;
+    a.se += b.se;
+    a.sg += b.sg;
+    a.fl |= b.fl;
+  }
+}
+
+// 3 resident CTAs per SM for the power-of-two forms (80 registers: one batch
+// in flight + the next chunk's table entries); the IEEE-division forms get
+// 128 registers so nothing spills
+#ifndef GS_P1_MINB
+#define GS_P1_MINB 3
+#endif
+template <bool F16, bool POW2>
+constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? GS_P1_MINB : 2;
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM>
+__global__ void __launch_bounds__(kThreads, (kP1MinBlocks<F16, POW2>))
+lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
+                  int chunk0, int nchunk, const gs_step_params params,
+                  double* __restrict__ partials, gs_ctl* __restrict__ ctl, uint32_t parity,
+                  const double* __restrict__ wsq) {
   Ctx cx;
   cx.u.load(&params);
   cx.mul = params.mul;
   cx.wd = params.weight_decay;
-  const bool lars = (sflags & GS_SEG_LARS_ENABLED) != 0;
-  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(sflags & GS_SEG_DECAY_EXEMPT);
-  // sum w^2 of this chunk as the previous step's pass 2 left it (same
-  // order, so the same bits; NaN = not available for this chunk)
-  double wc = 0.0;
-  bool cached = false;
-  if (wsq != nullptr && lars && p1_vec_path<true>(g, w)) {
-    wc = wsq[c];
-    cached = !isnan(wc);
+  __shared__ double red[2][3][kThreads / 32];
+  uint32_t flag_acc = 0;
+  int i = blockIdx.x;
+  if (i >= nchunk) return;
+  P1Meta cur = p1_meta<F16>(segs, chunks, chunk0 + i, wsq);
+  P1Batch<F16> bt;
+  p1_issue<F16>(cur, bt);
+  for (int it = 0; i < nchunk; ++it) {
+    const int inext = i + gridDim.x;
+    P1Meta nxt;
+    if (inext < nchunk) nxt = p1_meta<F16>(segs, chunks, chunk0 + inext, wsq);
+    const bool lars = (cur.sflags & GS_SEG_LARS_ENABLED) != 0;
+    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(cur.sflags & GS_SEG_DECAY_EXEMPT);
+    // the previous pass 2's sum w^2 stands in for this chunk's when it was
+    // formed in this very order (pass 2 stores NaN where it was not)
+    const bool cached = lars && !isnan(cur.wc) && p1_batched<F16>(cur);
+    Acc a;
+    if (lars && decay) {
+      if (cached)
+        p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, false>(cur, bt, cx, a);
+      else
+        p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, true>(cur, bt, cx, a);
+    } else if (lars) {
+      if (cached)
+        p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, false>(cur, bt, cx, a);
+      else
+        p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, true>(cur, bt, cx, a);
+    } else {
+      p1_consume<F16, POW2, RAWFLAG, GNORM, false, false, true>(cur, bt, cx, a);
+    }
+    if (inext < nchunk) p1_issue<F16>(nxt, bt);  // in flight during the reduction below
+    if (lars && !decay) {
+      a.se = a.sg;  // eff == g exactly: same terms, same order
+      if (!GNORM) a.sg = 0.0;
+    }
+    flag_acc |= a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
+    // the fixed block tree of gs::block_sum3, double-buffered scratch so one
+    // barrier per chunk suffices
+    double x = gs::warp_sum(a.sw), y = gs::warp_sum(a.se), z = gs::warp_sum(a.sg);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double(*rb)[kThreads / 32] = red[it & 1];
+    if (lane == 0) {
+      rb[0][warp] = x;
+      rb[1][warp] = y;
+      rb[2][warp] = z;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int w8 = 1; w8 < kThreads / 32; ++w8) {
+        x += rb[0][w8];
+        y += rb[1][w8];
+        z += rb[2][w8];
+      }
+      partials[3 * (int64_t)cur.c + 0] = cached ? cur.wc : x;
+      partials[3 * (int64_t)cur.c + 1] = y;
+      partials[3 * (int64_t)cur.c + 2] = z;
+    }
+    cur = nxt;
+    i = inext;
   }
-  Acc a;
-  if (lars && decay) {
-    if (cached)
-      p1_chunk<F16, POW2, RAWFLAG, GNORM, true, true, false>(g, w, ch.len, cx, a);
-    else
-      p1_chunk<F16, POW2, RAWFLAG, GNORM, true, true>(g, w, ch.len, cx, a);
-  } else if (lars) {
-    if (cached)
-      p1_chunk<F16, POW2, RAWFLAG, GNORM, true, false, false>(g, w, ch.len, cx, a);
-    else
-      p1_chunk<F16, POW2, RAWFLAG, GNORM, true, false>(g, w, ch.len, cx, a);
-  } else {
-    p1_chunk<F16, POW2, RAWFLAG, GNORM, false, false>(g, w, ch.len, cx, a);
-  }
-  if (lars && !decay) {
-    a.se = a.sg;  // eff == g exactly: same terms, same order
-    if (!GNORM) a.sg = 0.0;
-  }
-  uint32_t fl = a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
-  fl = __reduce_or_sync(0xFFFFFFFFu, fl);
-  if (fl != 0u && (threadIdx.x & 31) == 0) atomicOr(&ctl->flags[parity], fl);
-  double sw = a.sw, se = a.se, sg = a.sg;
-  gs::block_sum3<kThreads>(sw, se, sg);
-  if (threadIdx.x == 0) {
-    partials[3 * (int64_t)c + 0] = cached ? wc : sw;
-    partials[3 * (int64_t)c + 1] = se;
-    partials[3 * (int64_t)c + 2] = sg;
-  }
+  flag_acc = __reduce_or_sync(0xFFFFFFFFu, flag_acc);
+  if (flag_acc != 0u && (threadIdx.x & 31) == 0) atomicOr(&ctl->flags[parity], flag_acc);
 }
 
 // ----------------------------------------------------------------- trust
@@ -251,6 +372,16 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   }
 }
 
+// persistent pass 1: every resident CTA slot, at most one CTA per chunk
+int p1_grid(const void* kernel, int nchunk) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  const int g = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  return nchunk < g ? nchunk : g;
+}
+
 }  // namespace
 
 extern "C" {
@@ -265,8 +396,11 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   const bool pow2 = hint & GS_HINT_POW2, raw = g_is_f16 && pow2 && (hint & GS_HINT_RAWFLAG),
              gnorm = hint & GS_HINT_GRADNORM;
 #define GS_P1(F, P, R, N)                                                                       \
-  lars_pass1_kernel<F, P, R, N><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, params,      \
-                                                             partials, ctl, parity, wsq)
+  do {                                                                                          \
+    auto k = lars_pass1_kernel<F, P, R, N>;                                                     \
+    k<<<p1_grid((const void*)k, nchunk), kThreads, 0, s>>>(segs, chunks, chunk0, nchunk, params, \
+                                                          partials, ctl, parity, wsq);          \
+  } while (0)
   if (g_is_f16) {
     if (raw) {
       if (gnorm) GS_P1(true, true, true, true); else GS_P1(true, true, true, false);

@@ -13,9 +13,6 @@ constexpr int kRounds = 4;                      // 8-element vectors per thread
 #ifndef GS_P1_ROUNDS
 #define GS_P1_ROUNDS 4   // pass-1 load batch (vectors per thread)
 #endif
-#ifndef GS_P1_MINB
-#define GS_P1_MINB 4     // pass-1 __launch_bounds__ min blocks per SM
-#endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
 constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;

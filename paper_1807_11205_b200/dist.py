@@ -19,7 +19,10 @@ one GPU and the bucket all-reduce runs over NVLink 5 / NVSwitch:
   "sharded"       bandwidth-optimal hierarchy for NVSwitch: intra-group
                   reduce-scatter -> all-reduce among same-offset ranks of all
                   groups -> intra-group all-gather (moves 2(p-1)/p S per GPU,
-                  the flat ring's volume, instead of the master's 3S).
+                  the flat ring's volume, instead of the master's 3S);
+  "ordered_hier"  the same two-level structure in ONE own kernel
+                  (gs_hier_allreduce_f16), bit-exact: the reference's rank
+                  tree factors over power-of-two groups.
 
 Sums never use ncclAvg: the reference sums and then divides by float32(p)
 (collectives.py:268-269), which the LARS pass-1 kernel does on the fly.
@@ -40,7 +43,7 @@ from .collectives import Topology, choose_algorithm
 
 __all__ = ["Communicator", "init_from_env", "ALGORITHMS"]
 
-ALGORITHMS = ("ring", "hierarchical", "sharded", "ordered")
+ALGORITHMS = ("ring", "hierarchical", "sharded", "ordered", "ordered_hier")
 
 
 def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
@@ -195,7 +198,7 @@ class OrderedWire:
         # 512-thread CTAs per SM fit next to anything else that is running
         self.nblocks = nblocks or comm.peer_ctas or 2 * sms
         self.total = (total + 255) // 256 * 256
-        sig_words = 2 * self.nblocks * self.p
+        sig_words = 3 * self.nblocks * self.p  # 3 barrier phases (hierarchical form)
         sig_elems = (4 * sig_words + 1) // 2 + 256
         self.buf = symm.empty(2 * self.total + sig_elems + 64, dtype=torch.uint16, device=device)
         self.buf.zero_()
@@ -247,6 +250,16 @@ class OrderedWire:
                       (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
                        slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
                       device=self.device)
+
+    def hier_op(self, half: int, offset: int, n: int, k: int, stream_h: int, slot: int = 0):
+        """The bucket all-reduce over Topology(p, k)'s two levels
+        (gs_hier_allreduce_f16; bit-identical to allreduce_op)."""
+        from . import _device as dev
+        from ._peer import PeerOp
+
+        return PeerOp("gs_hier_allreduce_f16", self.ctx,
+                      (self.p, k, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
+                       slot + 1, self.grid_for(n), stream_h), device=self.device)
 
     def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
         from ._peer import launch

@@ -70,7 +70,8 @@ class LocalComm:
 
     def _no_nccl(self, *a, **k):
         raise NotImplementedError("NCCL collectives cannot be emulated on one device; use the "
-                                  "own-kernel paths (sharded_update / flat_variant='ordered')")
+                                  "own-kernel paths (sharded_update, flat_variant='ordered', "
+                                  "hier_variant='ordered_hier')")
 
     allreduce = allreduce_ring = allreduce_hierarchical = allreduce_sharded = _no_nccl
 
@@ -98,6 +99,7 @@ class LocalOrderedWire:
     _setup = _OW._setup
     grid_for = _OW.grid_for
     allreduce_op = _OW.allreduce_op
+    hier_op = _OW.hier_op
     allreduce = _OW.allreduce
     advance = _OW.advance
     status_word = _OW.status_word
@@ -147,7 +149,7 @@ class LocalWorld:
         total = (total + 255) // 256 * 256
         if self._wires is None or self._wires[0] != total or self._wires[1][rank] is None:
             nb = self.peer_ctas
-            sig_elems = (4 * 2 * nb * p + 1) // 2 + 256
+            sig_elems = (4 * 3 * nb * p + 1) // 2 + 256
             bufs = [torch.zeros(2 * total + sig_elems + 64, dtype=torch.uint16, device=device)
                     for _ in range(p)]
             bases = [b.data_ptr() for b in bufs]

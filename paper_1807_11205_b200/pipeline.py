@@ -154,8 +154,9 @@ class GradientPipeline:
       comm: dist.Communicator (or emulation.LocalComm) for p > 1; None = a
         single worker, no collective.
       eta_bytes: hybrid threshold (collectives.py:238-244) on fp16 bucket bytes.
-      hier_variant: NCCL variant for hierarchical buckets ("hierarchical" =
-        literal master path, "sharded" = RS/AR/AG).
+      hier_variant: variant for hierarchical buckets: "hierarchical" = the
+        literal master path over NCCL, "sharded" = RS/AR/AG over NCCL,
+        "ordered_hier" = own bit-exact two-level kernel (power-of-two k).
       flat_variant: flat buckets: "ring" (NCCL) or "ordered" (own bit-exact
         NVLink all-reduce, gs_ordered_allreduce_f16).
       ordered_push: the ordered all-reduce's push form (same bits).
@@ -226,7 +227,7 @@ class GradientPipeline:
                 b.algorithm = comm.pick(b.nbytes, self.eta_bytes, hier_variant, flat_variant)
             else:
                 b.algorithm = "ordered" if self.local else "none"
-        if self.emulated and any(b.algorithm not in ("ordered", "sharded-update")
+        if self.emulated and any(b.algorithm not in ("ordered", "ordered_hier", "sharded-update")
                                  for b in self.buckets):
             raise ValueError("emulated ranks run the own-kernel paths only: sharded_update=True "
                              "or flat_variant='ordered' with eta_bytes=0")
@@ -236,7 +237,8 @@ class GradientPipeline:
         self._half = 0
         if self.sharded:
             self._init_sharded_arena(comm, d)
-        elif comm is not None and any(b.algorithm == "ordered" for b in self.buckets):
+        elif comm is not None and any(b.algorithm in ("ordered", "ordered_hier")
+                                      for b in self.buckets):
             # the ordered (bit-exact) collective reads peers' wires over
             # NVLink: the wire lives in a double-buffered symmetric window
             self.ordered = comm.make_ordered_wire(self.total, d, push=ordered_push)
@@ -404,8 +406,11 @@ class GradientPipeline:
         """Make the sharded masters and velocities whole on every rank."""
         self._drive(self._gather_gen())
 
-    @staticmethod
-    def _drive(gen) -> None:
+    def _drive(self, gen) -> None:
+        """Launch this rank's peer ops as they come (one rank per launch)."""
+        if self.emulated:
+            raise RuntimeError("an emulated rank is driven by its LocalWorld (world.step / "
+                               "world.gather_state / world.begin ...), with its peers in lockstep")
         for op in gen:
             launch([op])
 
@@ -736,7 +741,7 @@ class GradientPipeline:
                     if bk.algorithm == "ring":
                         works.append(self.comm.allreduce_ring(payload, async_op=True))
                     else:
-                        if bk.algorithm != "ordered":
+                        if bk.algorithm not in ("ordered", "ordered_hier"):
                             self.comm.allreduce(payload, bk.algorithm)
                         ev = torch.cuda.Event()
                         ev.record(ps)
@@ -747,10 +752,10 @@ class GradientPipeline:
                     s0.wait_event(w)
                 else:
                     w.wait()
-                if bk.algorithm == "ordered":
+                if bk.algorithm in ("ordered", "ordered_hier"):
                     if timer:
                         timer(f"allreduce{b}")
-                    yield self.ordered.allreduce_op(half, bk.start, bk.length, sh, slot=b)
+                    yield self._ordered_op(half, bk, sh, b)
                 if timer:
                     timer(f"pass1_{b}")
                 plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
@@ -769,6 +774,14 @@ class GradientPipeline:
         plan.use_segments(None)
         if timer:
             timer("end")
+
+    def _ordered_op(self, half: int, bk: Bucket, sh: int, slot: int) -> PeerOp:
+        """Own bit-exact all-reduce of one bucket: flat, or over
+        Topology(p, k)'s two levels (hierarchical buckets, hier_variant =
+        'ordered_hier'); identical results."""
+        if bk.algorithm == "ordered_hier":
+            return self.ordered.hier_op(half, bk.start, bk.length, self.comm.topo.k, sh, slot=slot)
+        return self.ordered.allreduce_op(half, bk.start, bk.length, sh, slot=slot)
 
     def _bucket_host_ranges(self):
         """Per bucket, the [lo, hi) element range of the registration-order
@@ -930,8 +943,8 @@ class GradientPipeline:
                                dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")), b, b + 1,
                                plan.sp, plan.hint, plan.parity, b + 1, self._nblocks, sh)
                 return
-            if bk.algorithm == "ordered":
-                yield self.ordered.allreduce_op(inc["half"], bk.start, bk.length, sh, slot=b)
+            if bk.algorithm in ("ordered", "ordered_hier"):
+                yield self._ordered_op(inc["half"], bk, sh, b)
             elif bk.algorithm != "none":
                 self.comm.allreduce(inc["wire"][bk.start:bk.start + bk.padded], bk.algorithm)
             if bk.nchunk:

@@ -19,6 +19,10 @@ Fixtures:
                         working after each step, per-group fp32 scales, flags
   netsim_golden.json    simulate() reports and crossover sweeps of the α-β model
                         (`python tests/golden/make_golden.py make_netsim` alone)
+  checkpoint_golden.lars  a LARS v1 checkpoint written by the reference's
+                        save_checkpoint (lars.py:197-207) after two lars_step
+                        calls on the first 14 shufflenet tensors, and
+  checkpoint_golden.npz the groups' arrays it holds (`make_checkpoint`)
 """
 
 from __future__ import annotations
@@ -348,10 +352,34 @@ def make_netsim(ref):
                                                          "sweeps": sweeps}))
 
 
+def make_checkpoint(ref):
+    lars = importlib.import_module("gradsync_ref.lars")
+    spec = json.loads((ROOT / "paper_1807_11205_b200" / "shapes.json").read_text())
+    rows = spec["shufflenet_v2_x0_5"][:14]
+    rng = np.random.default_rng(77)
+    groups = []
+    for name, shape, kind in rows:
+        n = int(np.prod(shape)) if shape else 1
+        w0 = (rng.standard_normal(n) * 0.1).astype(np.float32)
+        groups.append(lars.make_param_group(name, kind, w0))
+    cfg = lars.LarsConfig(schedule=lars.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0,
+                          weight_decay=5e-4, momentum=0.9)
+    for step in range(2):
+        for g in groups:
+            g.grad[:] = (rng.standard_normal(g.size) * 1e-3).astype(np.float32)
+        assert lars.lars_step(groups, cfg, step)
+    lars.save_checkpoint(HERE / "checkpoint_golden.lars", groups, step=2)
+    out = {"names": np.array([g.name for g in groups]), "kinds": np.array([g.kind for g in groups]),
+           "shapes": np.array([json.dumps(r[1]) for r in rows])}
+    for i, g in enumerate(groups):
+        out[f"w_{i}"], out[f"v_{i}"], out[f"h_{i}"] = g.master_w, g.velocity, g.working_w16
+    np.savez_compressed(HERE / "checkpoint_golden.npz", **out)
+
+
 def main():
     ref = load_reference()
     fns = (make_halfprec, make_fusion, make_schedules, make_folds, make_lars, make_step,
-           make_netsim)
+           make_netsim, make_checkpoint)
     only = set(sys.argv[1:])
     for fn in fns:
         if only and fn.__name__ not in only:

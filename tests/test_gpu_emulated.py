@@ -73,6 +73,29 @@ def test_ordered_allreduce_bit_exact(p, push):
             assert w.status_word() == 0
 
 
+@pytest.mark.parametrize("p,k", [(2, 2), (4, 2), (4, 4), (6, 2), (8, 2), (8, 4), (8, 8)])
+def test_hierarchical_allreduce_bit_exact(p, k):
+    """gs_hier_allreduce_f16 over Topology(p, k): intra-group reduce-scatter,
+    inter-group fold of the group partials, all-gather — the reference's
+    rank tree (fold_f16_tree) bit for bit."""
+    d = dev.require_cuda()
+    world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
+    wires = [c.make_ordered_wire(1 << 16, d) for c in world.comms]
+    rng = np.random.default_rng(300 + 10 * p + k)
+    sh_ = torch.cuda.current_stream().cuda_stream
+    for slot, (off, n) in enumerate([(0, 50001), (24, 7), (1000, 8 * p * 16 + 3)]):
+        data = [random_f16(rng, n) for _ in range(p)]
+        for w, x in zip(wires, data):
+            w.halves[0][off:off + n].copy_(torch.from_numpy(x))
+        launch([w.hier_op(0, off, n, k, sh_, slot=slot) for w in wires])
+        torch.cuda.synchronize()
+        want = rp.fold_f16_tree(data)
+        for r, w in enumerate(wires):
+            assert np.array_equal(w.halves[0][off:off + n].cpu().numpy(), want), \
+                f"Topology({p},{k}) rank {r} bucket {slot}"
+            assert w.status_word() == 0
+
+
 @pytest.mark.parametrize("p", [2, 4, 8])
 def test_reduce_scatter_and_allgather_bit_exact(p):
     """gs_ordered_reduce_scatter_f16 folds rank r's slice in tree order;
@@ -126,11 +149,11 @@ def test_missing_peer_times_out_without_hanging():
 
 # ---------------------------------------------------------------- pipelines
 def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject_step=2,
-                 incremental=False, in_place=False, specs=None, **kw):
+                 incremental=False, in_place=False, specs=None, k=1, **kw):
     d = dev.require_cuda()
     specs = specs or sh.load_shapes(model)
     master = sh.synth_master(specs, seed=0)
-    world = LocalWorld(gs.Topology(p, 1), d, peer_ctas=16)
+    world = LocalWorld(gs.Topology(p, k), d, peer_ctas=16)
     cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
     pipes = [gs.GradientPipeline(specs, cfg, threshold_bytes=theta, comm=c, init_master=master,
                                  loss_scale=gs.LossScale(1024.0), device=d, **kw)
@@ -165,8 +188,8 @@ def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject
             res = world.step(pipes, grads, step)
         out = rp.compose_step_fp16([split(w, specs) for w in wires], [s.name for s in specs],
                                    [s.numel for s in specs], order, groups,
-                                   rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1, oloss, theta, 0,
-                                   threads=rp.default_threads())
+                                   rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1, oloss, theta,
+                                   kw.get("eta_bytes", 0), threads=rp.default_threads())
         if pipes[0].sharded:
             world.gather_state(pipes)
         for r, (pipe, rr) in enumerate(zip(pipes, res)):
@@ -216,6 +239,50 @@ def test_ordered_allreduce_step_bit_exact(p, push):
     run_emulated(p, flat_variant="ordered", eta_bytes=0, ordered_push=push)
 
 
+@pytest.mark.parametrize("p,k", [(4, 2), (8, 4), (8, 2)])
+def test_hierarchical_step_bit_exact(p, k):
+    """Every bucket hierarchical (eta = inf, the reference's config 1 rule)
+    through the own two-level kernel, replicated update."""
+    pipes = run_emulated(p, k=k, eta_bytes=float("inf"), hier_variant="ordered_hier")
+    assert {b.algorithm for b in pipes[0].buckets} == {"ordered_hier"}
+
+
+def test_config1_emulated_hierarchy_matches_reference_hashes(golden):
+    """Config 1 (shufflenet shapes, p = 4 as Topology(4, 2),
+    theta = 256 KiB, eta = inf, an injected +Inf at step 2) with the four
+    ranks emulated on the device and the two-level own kernel: master,
+    velocity and working copy equal the SHA-256 the reference produced."""
+    import hashlib
+    doc = golden.json("step_golden.json")
+    d = dev.require_cuda()
+    specs = sh.load_shapes(doc["model"])
+    world = LocalWorld(gs.Topology(doc["p"], doc["k"]), d, peer_ctas=16)
+    cfg = gs.LarsConfig(gs.Schedule(base_lr=doc["lr"]), eta=doc["eta"], epsilon=doc["epsilon"],
+                        weight_decay=doc["weight_decay"], momentum=doc["momentum"])
+    pipes = [gs.GradientPipeline(specs, cfg, threshold_bytes=doc["theta"], comm=c,
+                                 eta_bytes=float("inf"), hier_variant="ordered_hier",
+                                 init_master=sh.synth_master(specs, seed=0),
+                                 loss_scale=gs.LossScale(doc["loss_scale"]), device=d)
+             for c in world.comms]
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for step, want in enumerate(doc["steps"]):
+        grads = []
+        for r in range(doc["p"]):
+            flat = sh.synth_wire_grads(specs, rank=r, seed=step,
+                                       loss_scale=pipes[0].loss_scale.scale)
+            inj = doc["inject"]
+            if step == inj["step"] and r == inj["rank"]:
+                flat[inj["index"]] = 0x7C00
+            grads.append(torch.from_numpy(flat).to(d))
+        res = world.step(pipes, grads, step)
+        for pipe, rr in zip(pipes, res):
+            assert rr.applied == want["applied"] and rr.scale == want["scale_used"]
+            assert pipe.loss_scale.scale == want["scale_after"]
+            assert sha(pipe.registration_view(pipe.master).cpu().numpy()) == want["master_sha"]
+            assert sha(pipe.registration_view(pipe.velocity).cpu().numpy()) == want["velocity_sha"]
+            assert sha(pipe.registration_view(pipe.working).cpu().numpy()) == want["working_sha"]
+
+
 @pytest.mark.parametrize("p", [4, 8])
 def test_incremental_sharded_step_bit_exact(p):
     """begin / submit (buckets in reverse) / end: per-bucket gs_rs_pass1 as
@@ -246,6 +313,9 @@ def test_pipeline_reports_peer_timeout():
                                  sharded_update=True, device=d) for c in world.comms]
     g = torch.from_numpy(sh.synth_wire_grads(specs, rank=0)).to(d)
     # drive rank 0 alone: its peer waits can never be satisfied
-    gs.GradientPipeline.enqueue(pipes[0], g, 0)
+    for op in pipes[0]._enqueue_gen(g, 0):
+        launch([op])
+    with pytest.raises(RuntimeError, match="driven by its LocalWorld"):
+        pipes[1].enqueue(g, 0)
     with pytest.raises(PeerTimeoutError, match="peer 1"):
         pipes[0].finish()

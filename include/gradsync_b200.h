@@ -227,6 +227,16 @@ int gs_ordered_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const 
                              const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
                              int nblocks, int push, void* stream);
 
+/* fp32 form for the reference's own fp32 wire (run_experiment fuses fp32
+ * gradients, experiment.py:282-301, 368-399): every element is the ascending
+ * left fold b0 + b1 + ... + b(p-1) in fp32 (fold_ascending,
+ * collectives.py:261-270; ring and hierarchical give this same fold, the
+ * mean's division by float32(p) is the consumer's: LARS pass 1).  n and
+ * offset in fp32 elements; otherwise the contract of the binary16 kernel. */
+int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
+                             int nblocks, int push, void* stream);
+
 /* The same all-reduce over Topology(p, k)'s two levels (
  * hierarchical_schedule, collectives.py:183-235): an intra-group
  * reduce-scatter (each member folds its slice over the group's k raw

@@ -108,6 +108,64 @@ __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint
   }
 }
 
+// fp32 form (fold_ascending, collectives.py:261-270): acc = b0; acc += b1;
+// ... in rank order, each add rounded to fp32 (the mean's division by
+// float32(p) is applied by the consumer, LARS pass 1, exactly as the
+// reference divides the folded sum).  Same slice discipline as fold_range.
+template <int P, bool PUSH = false>
+__device__ __forceinline__ void fold_range_f32(const float* const (&src)[P], float* mine,
+                                               int64_t lo, int64_t hi, uint32_t& bad) {
+  bool vec = gs::is_aligned16(mine + lo);
+#pragma unroll
+  for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q] + lo);
+  const int64_t nv = vec ? (hi - lo) / 4 : 0;
+  constexpr int kU = P <= 4 ? 4 : 2;
+  for (int64_t base = threadIdx.x; base < nv; base += kU * kThreads) {
+    float4 raw[kU][P];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * kThreads;
+      if (i < nv) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) raw[u][q] = __ldcv(reinterpret_cast<const float4*>(src[q] + lo) + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = base + u * kThreads;
+      if (i >= nv) break;
+      float4 o = raw[u][0];
+#pragma unroll
+      for (int q = 1; q < P; ++q) {
+        o.x = __fadd_rn(o.x, raw[u][q].x);
+        o.y = __fadd_rn(o.y, raw[u][q].y);
+        o.z = __fadd_rn(o.z, raw[u][q].z);
+        o.w = __fadd_rn(o.w, raw[u][q].w);
+      }
+      bad |= !(gs::is_finite_f32(o.x) && gs::is_finite_f32(o.y) && gs::is_finite_f32(o.z) &&
+               gs::is_finite_f32(o.w));
+      if (PUSH) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) reinterpret_cast<float4*>(const_cast<float*>(src[q]) + lo)[i] = o;
+      } else {
+        reinterpret_cast<float4*>(mine + lo)[i] = o;
+      }
+    }
+  }
+  for (int64_t i = lo + nv * 4 + threadIdx.x; i < hi; i += kThreads) {
+    float o = __ldcv(src[0] + i);
+#pragma unroll
+    for (int q = 1; q < P; ++q) o = __fadd_rn(o, __ldcv(src[q] + i));
+    bad |= !gs::is_finite_f32(o);
+    if (PUSH) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) const_cast<float*>(src[q])[i] = o;
+    } else {
+      mine[i] = o;
+    }
+  }
+}
+
 // copy bytes [lo, hi) of a peer buffer into mine
 __device__ __forceinline__ void copy_range(const uint8_t* src, uint8_t* mine, int64_t lo, int64_t hi) {
   const bool v2 = ((reinterpret_cast<uintptr_t>(src + lo) | reinterpret_cast<uintptr_t>(mine + lo)) & 15) == 0;
@@ -171,6 +229,45 @@ ordered_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
     const int r = (rank + d) % P;
     subrange(n, P, r, nb, c.lb, lo, hi);
     copy_range(reinterpret_cast<const uint8_t*>(src[r]), reinterpret_cast<uint8_t*>(mine), 2 * lo, 2 * hi);
+  }
+}
+
+// The fp32-wire bucket all-reduce (the reference's own run_experiment path
+// fuses fp32 gradients, experiment.py:282-301, 368-399): same structure as
+// the binary16 kernel, ascending left fold per element.  For fp32 the
+// reference's ring and hierarchical algorithms give the same left fold
+// (test_collectives.py:168-173), which does not factor over groups, so this
+// one kernel serves both.
+template <int P, bool PUSH>
+__global__ void __launch_bounds__(kThreads)
+ordered_allreduce_f32_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                             const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
+                             int64_t offset, int64_t n, uint32_t epoch) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
+  const float* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const float*>(bufs[q]) + offset;
+  float* mine = reinterpret_cast<float*>(bufs[rank]) + offset;
+  peer_barrier(sig, c, P, 0, epoch, kSiteOrderedAllreduce);
+  int64_t lo, hi;
+  subrange(n, P, rank, nb, c.lb, lo, hi);
+  uint32_t bad = 0;
+  fold_range_f32<P, PUSH>(src, mine, lo, hi, bad);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+  if (PUSH) {
+    __threadfence_system();
+    peer_barrier(sig, c, P, 1, epoch, kSiteOrderedAllreduce);
+    return;
+  }
+  peer_barrier(sig, c, P, 1, epoch, kSiteOrderedAllreduce);
+#pragma unroll 1
+  for (int d = 1; d < P; ++d) {
+    const int r = (rank + d) % P;
+    subrange(n, P, r, nb, c.lb, lo, hi);
+    copy_range(reinterpret_cast<const uint8_t*>(src[r]), reinterpret_cast<uint8_t*>(mine), 4 * lo, 4 * hi);
   }
 }
 
@@ -376,6 +473,40 @@ int gs_ordered_allgather(const gs_rank_ctx* ranks, int nranks, int p, const uint
   ordered_allgather_kernel<<<nb * nranks, kThreads, 0, (cudaStream_t)stream>>>(ranks, nb, p, bufs,
                                                                                sig, bounds, epoch);
   return gs_check_launch("gs_ordered_allgather");
+}
+
+int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* sig, int64_t offset, int64_t n, uint32_t epoch,
+                             int nblocks, int push, void* stream) {
+  GS_PEER_ARGS("gs_ordered_allreduce_f32");
+  GS_REQUIRE(n >= 0 && offset >= 0, "gs_ordered_allreduce_f32: negative size/offset");
+  if (p == 1 || n == 0) return GS_OK;
+  GS_REQUIRE(ranks && bufs && sig, "gs_ordered_allreduce_f32: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_OAR32(P)                                                                              \
+  case P: {                                                                                      \
+    if (push) {                                                                                  \
+      auto k = ordered_allreduce_f32_kernel<P, true>;                                            \
+      const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                    \
+      k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);                \
+    } else {                                                                                     \
+      auto k = ordered_allreduce_f32_kernel<P, false>;                                           \
+      const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                    \
+      k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);                \
+    }                                                                                            \
+    break;                                                                                       \
+  }
+  switch (p) {
+    GS_OAR32(2)
+    GS_OAR32(3)
+    GS_OAR32(4)
+    GS_OAR32(5)
+    GS_OAR32(6)
+    GS_OAR32(7)
+    GS_OAR32(8)
+  }
+#undef GS_OAR32
+  return gs_check_launch("gs_ordered_allreduce_f32");
 }
 
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,

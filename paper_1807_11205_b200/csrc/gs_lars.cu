@@ -135,10 +135,72 @@ __device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& 
 // in flight + the next chunk's table entries); the IEEE-division forms get
 // 128 registers so nothing spills
 #ifndef GS_P1_MINB
-#define GS_P1_MINB 3
+#define GS_P1_MINB 4
+#endif
+#ifndef GS_P1_CPC
+#define GS_P1_CPC 1   // chunks per CTA in the non-persistent form (loads of all issued at once)
+#endif
+#ifndef GS_P1_PERSISTENT
+#define GS_P1_PERSISTENT 0
 #endif
 template <bool F16, bool POW2>
 constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? GS_P1_MINB : 2;
+
+// one chunk's partials: the fixed block tree of gs::block_sum3 over
+// double-buffered scratch (one barrier per chunk)
+__device__ __forceinline__ void p1_finish(const P1Meta& m, bool cached, const Acc& a, int it,
+                                          double (*red)[3][kThreads / 32],
+                                          double* __restrict__ partials) {
+  double x = gs::warp_sum(a.sw), y = gs::warp_sum(a.se), z = gs::warp_sum(a.sg);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double(*rb)[kThreads / 32] = red[it & 1];
+  if (lane == 0) {
+    rb[0][warp] = x;
+    rb[1][warp] = y;
+    rb[2][warp] = z;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w8 = 1; w8 < kThreads / 32; ++w8) {
+      x += rb[0][w8];
+      y += rb[1][w8];
+      z += rb[2][w8];
+    }
+    partials[3 * (int64_t)m.c + 0] = cached ? m.wc : x;
+    partials[3 * (int64_t)m.c + 1] = y;
+    partials[3 * (int64_t)m.c + 2] = z;
+  }
+}
+
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM>
+__device__ __forceinline__ uint32_t p1_run(const P1Meta& cur, const P1Batch<F16>& bt,
+                                           const Ctx& cx, bool& cached_out, Acc& a) {
+  const bool lars = (cur.sflags & GS_SEG_LARS_ENABLED) != 0;
+  const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(cur.sflags & GS_SEG_DECAY_EXEMPT);
+  // the previous pass 2's sum w^2 stands in for this chunk's when it was
+  // formed in this very order (pass 2 stores NaN where it was not)
+  const bool cached = lars && !isnan(cur.wc) && p1_batched<F16>(cur);
+  if (lars && decay) {
+    if (cached)
+      p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, false>(cur, bt, cx, a);
+    else
+      p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, true>(cur, bt, cx, a);
+  } else if (lars) {
+    if (cached)
+      p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, false>(cur, bt, cx, a);
+    else
+      p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, true>(cur, bt, cx, a);
+  } else {
+    p1_consume<F16, POW2, RAWFLAG, GNORM, false, false, true>(cur, bt, cx, a);
+  }
+  if (lars && !decay) {
+    a.se = a.sg;  // eff == g exactly: same terms, same order
+    if (!GNORM) a.sg = 0.0;
+  }
+  cached_out = cached;
+  return a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
+}
 
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM>
 __global__ void __launch_bounds__(kThreads, (kP1MinBlocks<F16, POW2>))
@@ -152,6 +214,7 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   cx.wd = params.weight_decay;
   __shared__ double red[2][3][kThreads / 32];
   uint32_t flag_acc = 0;
+#if GS_P1_PERSISTENT
   int i = blockIdx.x;
   if (i >= nchunk) return;
   P1Meta cur = p1_meta<F16>(segs, chunks, chunk0 + i, wsq);
@@ -161,56 +224,35 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
     const int inext = i + gridDim.x;
     P1Meta nxt;
     if (inext < nchunk) nxt = p1_meta<F16>(segs, chunks, chunk0 + inext, wsq);
-    const bool lars = (cur.sflags & GS_SEG_LARS_ENABLED) != 0;
-    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(cur.sflags & GS_SEG_DECAY_EXEMPT);
-    // the previous pass 2's sum w^2 stands in for this chunk's when it was
-    // formed in this very order (pass 2 stores NaN where it was not)
-    const bool cached = lars && !isnan(cur.wc) && p1_batched<F16>(cur);
     Acc a;
-    if (lars && decay) {
-      if (cached)
-        p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, false>(cur, bt, cx, a);
-      else
-        p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, true>(cur, bt, cx, a);
-    } else if (lars) {
-      if (cached)
-        p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, false>(cur, bt, cx, a);
-      else
-        p1_consume<F16, POW2, RAWFLAG, GNORM, true, false, true>(cur, bt, cx, a);
-    } else {
-      p1_consume<F16, POW2, RAWFLAG, GNORM, false, false, true>(cur, bt, cx, a);
-    }
+    bool cached;
+    flag_acc |= p1_run<F16, POW2, RAWFLAG, GNORM>(cur, bt, cx, cached, a);
     if (inext < nchunk) p1_issue<F16>(nxt, bt);  // in flight during the reduction below
-    if (lars && !decay) {
-      a.se = a.sg;  // eff == g exactly: same terms, same order
-      if (!GNORM) a.sg = 0.0;
-    }
-    flag_acc |= a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
-    // the fixed block tree of gs::block_sum3, double-buffered scratch so one
-    // barrier per chunk suffices
-    double x = gs::warp_sum(a.sw), y = gs::warp_sum(a.se), z = gs::warp_sum(a.sg);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double(*rb)[kThreads / 32] = red[it & 1];
-    if (lane == 0) {
-      rb[0][warp] = x;
-      rb[1][warp] = y;
-      rb[2][warp] = z;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int w8 = 1; w8 < kThreads / 32; ++w8) {
-        x += rb[0][w8];
-        y += rb[1][w8];
-        z += rb[2][w8];
-      }
-      partials[3 * (int64_t)cur.c + 0] = cached ? cur.wc : x;
-      partials[3 * (int64_t)cur.c + 1] = y;
-      partials[3 * (int64_t)cur.c + 2] = z;
-    }
+    p1_finish(cur, cached, a, it, red, partials);
     cur = nxt;
     i = inext;
   }
+#else
+  // GS_P1_CPC consecutive chunks per CTA, every load issued before any
+  // arithmetic
+  const int i0 = blockIdx.x * GS_P1_CPC;
+  P1Meta m[GS_P1_CPC];
+  P1Batch<F16> bt[GS_P1_CPC];
+#pragma unroll
+  for (int k = 0; k < GS_P1_CPC; ++k)
+    if (i0 + k < nchunk) m[k] = p1_meta<F16>(segs, chunks, chunk0 + i0 + k, wsq);
+#pragma unroll
+  for (int k = 0; k < GS_P1_CPC; ++k)
+    if (i0 + k < nchunk) p1_issue<F16>(m[k], bt[k]);
+#pragma unroll
+  for (int k = 0; k < GS_P1_CPC; ++k) {
+    if (i0 + k >= nchunk) break;
+    Acc a;
+    bool cached;
+    flag_acc |= p1_run<F16, POW2, RAWFLAG, GNORM>(m[k], bt[k], cx, cached, a);
+    p1_finish(m[k], cached, a, k, red, partials);
+  }
+#endif
   flag_acc = __reduce_or_sync(0xFFFFFFFFu, flag_acc);
   if (flag_acc != 0u && (threadIdx.x & 31) == 0) atomicOr(&ctl->flags[parity], flag_acc);
 }
@@ -372,8 +414,10 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   }
 }
 
-// persistent pass 1: every resident CTA slot, at most one CTA per chunk
+// persistent pass 1: every resident CTA slot, at most one CTA per chunk;
+// otherwise one CTA per GS_P1_CPC chunks
 int p1_grid(const void* kernel, int nchunk) {
+  if (!GS_P1_PERSISTENT) return (nchunk + GS_P1_CPC - 1) / GS_P1_CPC;
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -170,8 +170,9 @@ class Communicator:
     def make_arena(self, regions: dict, device, sig_words: int) -> "SymmetricArena":
         return SymmetricArena(self, regions, device, sig_words)
 
-    def make_ordered_wire(self, total: int, device, push: bool = False) -> "OrderedWire":
-        return OrderedWire(self, total, device, push=push)
+    def make_ordered_wire(self, total: int, device, push: bool = False,
+                          itemsize: int = 2) -> "OrderedWire":
+        return OrderedWire(self, total, device, push=push, itemsize=itemsize)
 
 
 class OrderedWire:
@@ -185,11 +186,8 @@ class OrderedWire:
     form (fold, barrier, gather by remote loads); same result bit for bit."""
 
     def __init__(self, comm: "Communicator", total: int, device, nblocks: int | None = None,
-                 push: bool = False):
-        import numpy as np
+                 push: bool = False, itemsize: int = 2):
         import torch.distributed._symmetric_memory as symm
-
-        from . import _device as dev
 
         self.p = comm.topo.p
         self.rank = comm.rank
@@ -198,15 +196,20 @@ class OrderedWire:
         # 512-thread CTAs per SM fit next to anything else that is running
         self.nblocks = nblocks or comm.peer_ctas or 2 * sms
         self.total = (total + 255) // 256 * 256
-        sig_words = 3 * self.nblocks * self.p  # 3 barrier phases (hierarchical form)
-        sig_elems = (4 * sig_words + 1) // 2 + 256
-        self.buf = symm.empty(2 * self.total + sig_elems + 64, dtype=torch.uint16, device=device)
+        self.itemsize = itemsize
+        self.buf = symm.empty(self.nbytes_for(self.total, itemsize, self.nblocks, self.p),
+                              dtype=torch.uint8, device=device)
         self.buf.zero_()
         torch.cuda.synchronize(device)
         self.hdl = symm.rendezvous(self.buf, dist.group.WORLD.group_name)
         bases = [int(x) for x in self.hdl.buffer_ptrs]
         self._setup(bases, device, push, comm.timeout_s)
         dist.barrier()
+
+    @staticmethod
+    def nbytes_for(total: int, itemsize: int, nblocks: int, p: int) -> int:
+        """[wire A | wire B | signal area (3 barrier phases) | status]"""
+        return 2 * total * itemsize + 4 * 3 * nblocks * p + 512 + 128
 
     def _setup(self, bases, device, push: bool, timeout_s: float) -> None:
         """Tables and this rank's context from every rank's base address
@@ -216,16 +219,18 @@ class OrderedWire:
         from . import _device as dev
         from ._peer import rank_ctx
 
-        self.halves = (self.buf[: self.total], self.buf[self.total: 2 * self.total])
-        self.bufs_dev = [dev.upload(np.array([b + 2 * h * self.total for b in bases],
-                                             dtype=np.uint64), device) for h in range(2)]
-        self.sig_dev = dev.upload(np.array([b + 4 * self.total for b in bases], dtype=np.uint64),
+        z, t = self.itemsize, self.total
+        dt = torch.uint16 if z == 2 else torch.float32
+        self.halves = (self.buf[: z * t].view(dt), self.buf[z * t: 2 * z * t].view(dt))
+        self.bufs_dev = [dev.upload(np.array([b + h * z * t for b in bases], dtype=np.uint64),
+                                    device) for h in range(2)]
+        self.sig_dev = dev.upload(np.array([b + 2 * z * t for b in bases], dtype=np.uint64),
                                   device)
         # device-resident epoch base: every call of a step uses base + slot,
         # and advance() bumps the base once per step on the stream
         self.epoch_base = torch.zeros(1, dtype=torch.int32, device=device)
         # status word (a timed-out peer wait is reported here) at the tail
-        self.status = self.buf[-64:].view(torch.int32)
+        self.status = self.buf[-128:].view(torch.int32)
         self.ctx = rank_ctx(self.rank, timeout_s=timeout_s, status=dev.ptr(self.status),
                             epoch_base=dev.ptr(self.epoch_base))
         self.push = bool(push)
@@ -246,7 +251,8 @@ class OrderedWire:
         from . import _device as dev
         from ._peer import PeerOp
 
-        return PeerOp("gs_ordered_allreduce_f16", self.ctx,
+        return PeerOp("gs_ordered_allreduce_f16" if self.itemsize == 2 else
+                      "gs_ordered_allreduce_f32", self.ctx,
                       (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
                        slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
                       device=self.device)

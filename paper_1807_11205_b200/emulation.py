@@ -65,8 +65,9 @@ class LocalComm:
     def make_arena(self, regions: dict, device, sig_words: int) -> "LocalArena":
         return self.world._arena(self.rank, regions, device, sig_words)
 
-    def make_ordered_wire(self, total: int, device, push: bool = False) -> "LocalOrderedWire":
-        return self.world._ordered_wire(self.rank, total, device, push)
+    def make_ordered_wire(self, total: int, device, push: bool = False,
+                          itemsize: int = 2) -> "LocalOrderedWire":
+        return self.world._ordered_wire(self.rank, total, device, push, itemsize)
 
     def _no_nccl(self, *a, **k):
         raise NotImplementedError("NCCL collectives cannot be emulated on one device; use the "
@@ -96,6 +97,7 @@ class LocalOrderedWire:
 
     from .dist import OrderedWire as _OW
     MIN_ELEMS_PER_CTA = _OW.MIN_ELEMS_PER_CTA
+    nbytes_for = _OW.nbytes_for
     _setup = _OW._setup
     grid_for = _OW.grid_for
     allreduce_op = _OW.allreduce_op
@@ -104,8 +106,9 @@ class LocalOrderedWire:
     advance = _OW.advance
     status_word = _OW.status_word
 
-    def __init__(self, p, rank, total, buf, bases, nblocks, device, push, timeout_s):
+    def __init__(self, p, rank, total, itemsize, buf, bases, nblocks, device, push, timeout_s):
         self.p, self.rank, self.total, self.buf, self.nblocks = p, rank, total, buf, nblocks
+        self.itemsize = itemsize
         self._setup(bases, device, push, timeout_s)
 
 
@@ -144,22 +147,22 @@ class LocalWorld:
         self._arenas[1][rank] = None  # each rank takes its arena once
         return arena
 
-    def _ordered_wire(self, rank, total, device, push) -> LocalOrderedWire:
+    def _ordered_wire(self, rank, total, device, push, itemsize=2) -> LocalOrderedWire:
         p = self.topo.p
         total = (total + 255) // 256 * 256
-        if self._wires is None or self._wires[0] != total or self._wires[1][rank] is None:
+        key = (total, itemsize)
+        if self._wires is None or self._wires[0] != key or self._wires[1][rank] is None:
             nb = self.peer_ctas
-            sig_elems = (4 * 3 * nb * p + 1) // 2 + 256
-            bufs = [torch.zeros(2 * total + sig_elems + 64, dtype=torch.uint16, device=device)
-                    for _ in range(p)]
+            nbytes = LocalOrderedWire.nbytes_for(total, itemsize, nb, p)
+            bufs = [torch.zeros(nbytes, dtype=torch.uint8, device=device) for _ in range(p)]
             bases = [b.data_ptr() for b in bufs]
-            wires = [LocalOrderedWire(p, r, total, bufs[r], bases, nb, device, push,
+            wires = [LocalOrderedWire(p, r, total, itemsize, bufs[r], bases, nb, device, push,
                                       self.timeout_s) for r in range(p)]
             # one bufs/sig table for every rank: the batched launch passes
             # rank 0's, so all must be the same tensors
             for w in wires[1:]:
                 w.bufs_dev, w.sig_dev = wires[0].bufs_dev, wires[0].sig_dev
-            self._wires = (total, wires)
+            self._wires = (key, wires)
         w = self._wires[1][rank]
         self._wires[1][rank] = None
         return w

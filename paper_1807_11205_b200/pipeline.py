@@ -78,10 +78,11 @@ class Bucket:
     chunk0: int = 0
     nchunk: int = 0
     algorithm: str = "ring"
+    itemsize: int = 2          # wire element: binary16 (2) or fp32 (4)
 
     @property
     def nbytes(self) -> int:
-        return 2 * self.length
+        return self.itemsize * self.length
 
 
 @dataclass
@@ -97,15 +98,16 @@ def _roundup(n: int, a: int) -> int:
     return (n + a - 1) // a * a
 
 
-def plan_layout(specs, order, threshold_bytes: int):
+def plan_layout(specs, order, threshold_bytes: int, itemsize: int = 2):
     """Host-only wire layout: (wire offset per parameter, buckets, total).
 
     Bucket membership and per-bucket unpack maps are exactly what
-    FusionBuffer(threshold) emits for uint16 tensors enqueued in `order`
-    (fusion.py:58-94); bucket b starts at a BUCKET_ALIGN-aligned wire offset.
+    FusionBuffer(threshold) emits for tensors of `itemsize` bytes (uint16
+    binary16 or float32) enqueued in `order` (fusion.py:58-94); bucket b
+    starts at a BUCKET_ALIGN-aligned wire offset.
     """
     sizes = [s.numel for s in specs]
-    groups_pos = plan_buckets([sizes[i] for i in order], 2, threshold_bytes)
+    groups_pos = plan_buckets([sizes[i] for i in order], itemsize, threshold_bytes)
     wire_off = [0] * len(specs)
     buckets, off = [], 0
     for pos_list in groups_pos:
@@ -117,7 +119,7 @@ def plan_layout(specs, order, threshold_bytes: int):
             off += sizes[i]
         length = off - start
         off = start + max(BUCKET_ALIGN, _roundup(length, BUCKET_ALIGN))
-        buckets.append(Bucket(start, length, off - start, idxs, tuple(umap)))
+        buckets.append(Bucket(start, length, off - start, idxs, tuple(umap), itemsize=itemsize))
     return wire_off, buckets, max(off, BUCKET_ALIGN)
 
 
@@ -178,6 +180,11 @@ class GradientPipeline:
         from them on request (the gradients must then be unchanged since the
         step).  snapshot_wire=True packs the wire inside every step instead
         (2 B/element more HBM traffic).
+      wire_dtype: "f16" (the north star's binary16 wire) or "f32" — the
+        reference's own run_experiment path: fp32 gradients fused at 4 bytes
+        per element and all-reduced as the ascending fp32 left fold, mean
+        applied by pass 1 (experiment.py:282-301, 368-413).  Replicated
+        update only (no sharded_update).
     """
 
     def __init__(self, specs, cfg: LarsConfig, *, threshold_bytes: int = 4 << 20,
@@ -186,7 +193,7 @@ class GradientPipeline:
                  init_master=None, grad_norm: bool = True, device=None,
                  local_workers: int = 1, flat_variant: str = "ring", ordered_push: bool = False,
                  sharded_update: bool = False, fused_collective: bool = True,
-                 snapshot_wire: bool = False):
+                 snapshot_wire: bool = False, wire_dtype: str = "f16"):
         self.specs = [s if isinstance(s, ParamSpec) else ParamSpec(s[0], tuple(s[1]), s[2])
                       for s in specs]
         self.cfg = cfg
@@ -209,15 +216,24 @@ class GradientPipeline:
             raise ValueError("order must be a permutation of the parameter indices")
         sizes = [s.numel for s in self.specs]
         self.sizes = sizes
+        if wire_dtype not in ("f16", "f32"):
+            raise ValueError(f"wire_dtype must be 'f16' or 'f32', got {wire_dtype!r}")
+        self.wire_dtype = wire_dtype
+        self.f16 = wire_dtype == "f16"
+        #: bytes per wire element and the wire's torch dtype
+        self.isz = 2 if self.f16 else 4
+        self.wdt = torch.uint16 if self.f16 else torch.float32
 
         # ---- wire layout: FusionBuffer boundaries over the enqueue order
         self.wire_off, self.buckets, self.total = plan_layout(self.specs, self.order,
-                                                              threshold_bytes)
+                                                              threshold_bytes, self.isz)
 
         d = self.device
         self.sharded = bool(sharded_update)
         if self.sharded and (comm is None or comm.topo.p < 2):
             raise ValueError("sharded_update needs a Communicator with p >= 2")
+        if self.sharded and not self.f16:
+            raise ValueError("the sharded update runs on the binary16 wire (wire_dtype='f16')")
         self.fused_collective = bool(fused_collective) and self.sharded and \
             comm.topo.p in (2, 4, 8)
         for b in self.buckets:
@@ -241,10 +257,11 @@ class GradientPipeline:
                                       for b in self.buckets):
             # the ordered (bit-exact) collective reads peers' wires over
             # NVLink: the wire lives in a double-buffered symmetric window
-            self.ordered = comm.make_ordered_wire(self.total, d, push=ordered_push)
+            self.ordered = comm.make_ordered_wire(self.total, d, push=ordered_push,
+                                                  itemsize=self.isz)
             self.wire = self.ordered.halves[0]
         else:
-            self.wire = torch.zeros(self.total, dtype=torch.uint16, device=d)
+            self.wire = torch.zeros(self.total, dtype=self.wdt, device=d)
         self._last_wire = self.wire
         if not self.sharded:
             self.master = torch.zeros(self.total, dtype=torch.float32, device=d)
@@ -261,7 +278,7 @@ class GradientPipeline:
         # in wire order, so every bucket owns a contiguous chunk range
         gsrc = self.red if self.sharded else self.wire
         gb, mb, vb, hb = (t.data_ptr() for t in (gsrc, self.master, self.velocity, self.working))
-        segs = [SegmentSpec(gb + 2 * self.wire_off[i], mb + 4 * self.wire_off[i],
+        segs = [SegmentSpec(gb + self.isz * self.wire_off[i], mb + 4 * self.wire_off[i],
                             vb + 4 * self.wire_off[i], hb + 2 * self.wire_off[i], sizes[i],
                             segment_flags(self.groups[i])) for i in range(n)]
         if self.sharded:
@@ -285,7 +302,7 @@ class GradientPipeline:
         assert c == self.plan.nchunk
         if self.ordered is not None:
             self._half_segs = [self.plan.alt_segments(
-                [h.data_ptr() + 2 * o for o in self.wire_off]) for h in self.ordered.halves]
+                [h.data_ptr() + self.isz * o for o in self.wire_off]) for h in self.ordered.halves]
         if self.sharded:
             self._init_ownership(d)
 
@@ -300,7 +317,7 @@ class GradientPipeline:
         self._pack_stream = torch.cuda.Stream(device=d) if real_comm else None
         self._side_stream = torch.cuda.Stream(device=d) if real_comm else None
         if self.local:
-            self.rank_wire = [torch.zeros(self.total, dtype=torch.uint16, device=d)
+            self.rank_wire = [torch.zeros(self.total, dtype=self.wdt, device=d)
                               for _ in range(self.p)]
             self._slots = dev.upload(np.array([t.data_ptr() for t in self.rank_wire],
                                               dtype=np.uint64), d)
@@ -466,7 +483,7 @@ class GradientPipeline:
                 if timer:
                     timer(f"pass1_{b}")
                 if c1 > c0:
-                    plan.pass1(sh, g_is_f16=True, chunk0=c0, nchunk=c1 - c0)
+                    plan.pass1(sh, g_is_f16=self.f16, chunk0=c0, nchunk=c1 - c0)
             if timer:
                 timer("gather_partials")
             for b in range(nb):
@@ -480,7 +497,7 @@ class GradientPipeline:
             for b in range(nb):
                 c0, c1 = self._own_bucket[b]
                 if c1 > c0:
-                    plan.pass2(sh, g_is_f16=True, flag_mask=_MASK, chunk0=c0, nchunk=c1 - c0)
+                    plan.pass2(sh, g_is_f16=self.f16, flag_mask=_MASK, chunk0=c0, nchunk=c1 - c0)
             if timer:
                 timer("gather_w16")
             for b in range(nb):
@@ -543,10 +560,11 @@ class GradientPipeline:
 
     # ------------------------------------------------------------ packing
     def grad_arena(self) -> torch.Tensor:
-        """A device fp16 (uint16) gradient arena in registration order that a
-        backward pass (or a host copy) can write into; step() accepts it."""
+        """A device gradient arena (binary16 as uint16, or fp32) in
+        registration order that a backward pass (or a host copy) can write
+        into; step() accepts it."""
         if self._grad_arena is None:
-            self._grad_arena = torch.zeros(sum(self.sizes), dtype=torch.uint16, device=self.device)
+            self._grad_arena = torch.zeros(sum(self.sizes), dtype=self.wdt, device=self.device)
         return self._grad_arena
 
     def grad_views(self) -> list:
@@ -574,11 +592,14 @@ class GradientPipeline:
             raise ValueError(f"expected {len(self.sizes)} gradients, got {len(views)}")
         return views
 
+    def _dtype_ok(self, t) -> bool:
+        return t.dtype in ((torch.uint16, torch.float16) if self.f16 else (torch.float32,))
+
     def _check_grads(self, views) -> None:
         for t, n in zip(views, self.sizes):
-            if t.numel() != n or t.dtype not in (torch.uint16, torch.float16) or not t.is_cuda:
-                raise ValueError("gradients must be CUDA fp16/uint16 tensors of the "
-                                 "parameter sizes")
+            if t.numel() != n or not self._dtype_ok(t) or not t.is_cuda:
+                raise ValueError("gradients must be CUDA " + ("fp16/uint16" if self.f16 else "fp32")
+                                 + " tensors of the parameter sizes")
 
     def _tables_for(self, views, dst: torch.Tensor):
         """Per-bucket gs_copy tables packing `views` into `dst`, plus entry
@@ -590,7 +611,8 @@ class GradientPipeline:
             wb = dst.data_ptr()
             tabs, host = [], []
             for b in self.buckets:
-                t = copy_table((views[i].data_ptr(), wb + 2 * self.wire_off[i], 2 * self.sizes[i])
+                z = self.isz
+                t = copy_table((views[i].data_ptr(), wb + z * self.wire_off[i], z * self.sizes[i])
                                for i in b.params if self.sizes[i])
                 tabs.append((dev.upload(t, self.device), len(t)))
                 host.append(t)
@@ -618,7 +640,7 @@ class GradientPipeline:
 
     def prepare(self, step: int) -> None:
         """Host-only part of a step (schedule, loss scale, launch hint)."""
-        self.plan.set_params(self.params_for(step), g_is_f16=True)
+        self.plan.set_params(self.params_for(step), g_is_f16=self.f16)
         self._prepared = step
 
     def _sources(self, grads):
@@ -704,7 +726,7 @@ class GradientPipeline:
                 self._last_wire = self.wire
             if timer:
                 timer("pass1")
-            plan.pass1(sh, g_is_f16=True)
+            plan.pass1(sh, g_is_f16=self.f16)
         elif self.local:
             plan.use_segments(None)
             if timer:
@@ -716,13 +738,18 @@ class GradientPipeline:
                 timer("fold")
             wb = self.wire.data_ptr()
             for bk in self.buckets:
-                if bk.length:
+                if not bk.length:
+                    continue
+                if self.f16:
                     _native.call("gs_fold_f16_tree", dev.ptr(self._slots), self.p, bk.start,
                                  wb + 2 * bk.start, bk.length, None, sh)
+                else:  # ascending fp32 sum; pass 1 divides by float32(p)
+                    _native.call("gs_fold_f32", dev.ptr(self._slots), self.p, bk.start,
+                                 wb + 4 * bk.start, bk.length, 0, sh)
             self._last_wire = self.wire
             if timer:
                 timer("pass1")
-            plan.pass1(sh, g_is_f16=True)
+            plan.pass1(sh, g_is_f16=self.f16)
         else:
             # bucket b+1 is packed (pack stream) while bucket b's all-reduce is
             # in flight and bucket b-1 runs pass 1 (compute stream)
@@ -758,7 +785,7 @@ class GradientPipeline:
                     yield self._ordered_op(half, bk, sh, b)
                 if timer:
                     timer(f"pass1_{b}")
-                plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+                plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
             if ps is not s0:
                 s0.wait_stream(ps)
             if self.ordered is not None:
@@ -770,7 +797,7 @@ class GradientPipeline:
         plan.trust(sh)
         if timer:
             timer("pass2")
-        plan.pass2(sh, g_is_f16=True, flag_mask=_MASK)
+        plan.pass2(sh, g_is_f16=self.f16, flag_mask=_MASK)
         plan.use_segments(None)
         if timer:
             timer("end")
@@ -779,8 +806,10 @@ class GradientPipeline:
         """Own bit-exact all-reduce of one bucket: flat, or over
         Topology(p, k)'s two levels (hierarchical buckets, hier_variant =
         'ordered_hier'); identical results."""
-        if bk.algorithm == "ordered_hier":
+        if bk.algorithm == "ordered_hier" and self.f16:
             return self.ordered.hier_op(half, bk.start, bk.length, self.comm.topo.k, sh, slot=slot)
+        # fp32: the reference's left fold does not factor over groups, so the
+        # hierarchical buckets take the flat kernel (the same fold)
         return self.ordered.allreduce_op(half, bk.start, bk.length, sh, slot=slot)
 
     def _bucket_host_ranges(self):
@@ -838,8 +867,8 @@ class GradientPipeline:
         self._wire_src = views
         for bk, ev in zip(self.buckets, evs):
             s0.wait_event(ev)
-            plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
-        plan.finish(sh, True, _MASK)
+            plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
+        plan.finish(sh, self.f16, _MASK)
         plan.use_segments(None)
         plan.end_step()
         self._last_wire = self.wire
@@ -904,12 +933,13 @@ class GradientPipeline:
         wb = inc["wire"].data_ptr()
         pairs = []
         for i, t in zip(bk.params, grads):
-            if t.numel() != self.sizes[i] or t.dtype not in (torch.uint16, torch.float16) \
+            if t.numel() != self.sizes[i] or not self._dtype_ok(t) \
                     or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"gradient of {self.specs[i].name!r} must be a contiguous CUDA "
-                                 f"fp16 tensor of {self.sizes[i]} elements")
-            if self.sizes[i] and t.data_ptr() != wb + 2 * self.wire_off[i]:
-                pairs.append((t.data_ptr(), wb + 2 * self.wire_off[i], 2 * self.sizes[i]))
+                                 f"{self.wire_dtype} tensor of {self.sizes[i]} elements")
+            z = self.isz
+            if self.sizes[i] and t.data_ptr() != wb + z * self.wire_off[i]:
+                pairs.append((t.data_ptr(), wb + z * self.wire_off[i], z * self.sizes[i]))
         key = ("inc", b, wb) + tuple(p[0] for p in pairs)
         tab = self._pack_cache.get(key)
         if tab is None:
@@ -948,7 +978,7 @@ class GradientPipeline:
             elif bk.algorithm != "none":
                 self.comm.allreduce(inc["wire"][bk.start:bk.start + bk.padded], bk.algorithm)
             if bk.nchunk:
-                plan.pass1(sh, g_is_f16=True, chunk0=bk.chunk0, nchunk=bk.nchunk)
+                plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
 
     def end(self) -> None:
         """Close the step: every bucket must have been submitted; trust and
@@ -981,7 +1011,7 @@ class GradientPipeline:
             _native.call("gs_counter_add", dev.ptr(self.epoch_base), nb + 3, sh)
             self._last_wire = self.red
         else:
-            plan.finish(sh, True, _MASK)
+            plan.finish(sh, self.f16, _MASK)
             if self.ordered is not None:
                 self.ordered.advance(nb + 1, sh)
                 self._half ^= 1

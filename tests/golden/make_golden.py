@@ -19,6 +19,10 @@ Fixtures:
                         working after each step, per-group fp32 scales, flags
   netsim_golden.json    simulate() reports and crossover sweeps of the α-β model
                         (`python tests/golden/make_golden.py make_netsim` alone)
+  step32_golden.json    the reference's OWN fp32-wire step body (run_experiment,
+                        experiment.py:368-413, with its _fused_allreduce
+                        op="mean", experiment.py:282-301) on config-1 shapes
+                        with fp32 gradients: hashes per step (`make_step32`)
   checkpoint_golden.lars  a LARS v1 checkpoint written by the reference's
                         save_checkpoint (lars.py:197-207) after two lars_step
                         calls on the first 14 shufflenet tensors, and
@@ -352,6 +356,91 @@ def make_netsim(ref):
                                                          "sweeps": sweeps}))
 
 
+def make_step32(ref):
+    """run_experiment's step body verbatim in structure, minus the toy
+    model: per-worker FusionBuffer over fp32 gradients in registration order
+    (experiment.py:369-379), experiment._fused_allreduce per bucket (hybrid
+    choice, op="mean"), unpack, LossScale.update on the scaled mean,
+    unscale_gradients, grad norm, lars_step (experiment.py:395-412)."""
+    sys.path.insert(0, str(ROOT))
+    from paper_1807_11205_b200 import shapes as sh
+    fusion = importlib.import_module("gradsync_ref.fusion")
+    col = importlib.import_module("gradsync_ref.collectives")
+    hp = importlib.import_module("gradsync_ref.halfprec")
+    lars = importlib.import_module("gradsync_ref.lars")
+    exp = importlib.import_module("gradsync_ref.experiment")
+    netsim = importlib.import_module("gradsync_ref.netsim")
+    model, p, k, theta, eta = "shufflenet_v2_x0_5", 4, 2, 256 << 10, 1 << 40
+    specs_obj = sh.load_shapes(model)
+    master = sh.synth_master(specs_obj, seed=0)
+    groups, o = [], 0
+    for s in specs_obj:
+        groups.append(lars.make_param_group(s.name, s.kind, master[o:o + s.numel]))
+        o += s.numel
+    cfg = lars.LarsConfig(schedule=lars.Schedule(base_lr=0.1), eta=0.001, epsilon=0.0,
+                          weight_decay=5e-4, momentum=0.9)
+    scale = hp.LossScale(scale=1024.0)
+    topo = col.Topology(p, k)
+    link = netsim.LinkModel()
+    steps = []
+    for step in range(3):
+        step_scale = scale.scale
+        worker_grads = []
+        for r in range(p):
+            flat = sh.synth_grads_f32(specs_obj, rank=r, seed=step) * np.float32(step_scale)
+            if step == 2 and r == 1:
+                flat[12345] = np.inf
+            d, o = {}, 0
+            for s in specs_obj:
+                d[s.name] = flat[o:o + s.numel]
+                o += s.numel
+            worker_grads.append(d)
+        buffers = [fusion.FusionBuffer(theta) for _ in range(p)]
+        step_batches = [[] for _ in range(p)]
+        for g in groups:
+            for w in range(p):
+                emitted = buffers[w].enqueue(g.name, worker_grads[w][g.name])
+                if emitted is not None:
+                    step_batches[w].append(emitted)
+        for w in range(p):
+            tail = buffers[w].flush()
+            if tail is not None:
+                step_batches[w].append(tail)
+        merged, algos, maps = {}, [], []
+        for b_idx in range(len(step_batches[0])):
+            aligned = [step_batches[w][b_idx] for w in range(p)]
+            mean_payload, algorithm, _, _ = exp._fused_allreduce(aligned, topo, link, eta, None)
+            algos.append(algorithm)
+            maps.append([list(m) for m in aligned[0].unpack_map])
+            for name, tensor in fusion.unpack(fusion.FusedBatch(mean_payload,
+                                                                aligned[0].unpack_map)):
+                merged[name] = tensor
+        for g in groups:
+            g.grad[:] = merged[g.name]
+        with np.errstate(over="ignore", invalid="ignore"):
+            applied = scale.update([g.grad for g in groups])
+            grad_norm = 0.0
+            if applied:
+                for g in groups:
+                    g.grad[:] = hp.unscale_gradients(g.grad, step_scale)
+                grad_norm = float(np.sqrt(sum(float(np.dot(g.grad.astype(np.float64),
+                                                           g.grad.astype(np.float64)))
+                                              for g in groups)))
+                applied = lars.lars_step(groups, cfg, step)
+        steps.append({"applied": bool(applied), "scale_used": step_scale,
+                      "scale_after": scale.scale, "grad_norm": grad_norm, "maps": maps,
+                      "algorithms": algos,
+                      "master_sha": sha(np.concatenate([g.master_w for g in groups])),
+                      "velocity_sha": sha(np.concatenate([g.velocity for g in groups])),
+                      "working_sha": sha(np.concatenate([g.working_w16 for g in groups]))})
+    doc = {"model": model, "p": p, "k": k, "theta": theta, "eta_bytes": eta, "lr": 0.1,
+           "eta": 0.001, "epsilon": 0.0, "weight_decay": 5e-4, "momentum": 0.9,
+           "loss_scale": 1024.0, "inject": {"step": 2, "rank": 1, "index": 12345},
+           "grads": "shapes.synth_grads_f32(rank, seed=step) * scale (fp32)",
+           "order": "registration (experiment.py:371)", "steps": steps}
+    (HERE / "step32_golden.json").write_text(json.dumps(doc))
+
+
 def make_checkpoint(ref):
     lars = importlib.import_module("gradsync_ref.lars")
     spec = json.loads((ROOT / "paper_1807_11205_b200" / "shapes.json").read_text())
@@ -379,7 +468,7 @@ def make_checkpoint(ref):
 def main():
     ref = load_reference()
     fns = (make_halfprec, make_fusion, make_schedules, make_folds, make_lars, make_step,
-           make_netsim, make_checkpoint)
+           make_netsim, make_checkpoint, make_step32)
     only = set(sys.argv[1:])
     for fn in fns:
         if only and fn.__name__ not in only:

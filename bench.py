@@ -537,7 +537,8 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
     variants = [("ring", 1)]
     for k in (4, 2):
         if world % k == 0 and k < world:
-            variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k)]
+            variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k),
+                         (f"ordered_hier_{world // k}x{k}", k)]
     comms = {}
     s0 = torch.cuda.current_stream(dev)
     variants += [("ordered", 1), ("ordered_push", 1)]
@@ -547,6 +548,7 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             comms[k] = Communicator(gs.Topology(world, k))
         comm = comms[k]
         algo = "ordered" if name.startswith("ordered") else name.split("_")[0]
+        hier_k = k if name.startswith("ordered_hier") else 0
         n = buf.numel() - buf.numel() % (k * 8)
         t = buf[:n]
         if algo == "ordered":
@@ -554,9 +556,13 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             ow = ow or OrderedWire(comm, pipe.total, dev)
             half = [0]
 
-            def run_ordered(_t=None, _push=name == "ordered_push"):
+            def run_ordered(_t=None, _push=name == "ordered_push", _k=hier_k):
+                from paper_1807_11205_b200._peer import launch
                 ow.push = _push
-                ow.allreduce(half[0], 0, n, int(s0.cuda_stream))
+                if _k:  # the bit-exact two-level kernel over Topology(p, k)
+                    launch([ow.hier_op(half[0], 0, n, _k, int(s0.cuda_stream))])
+                else:
+                    ow.allreduce(half[0], 0, n, int(s0.cuda_stream))
                 ow.advance(1, int(s0.cuda_stream))
                 half[0] ^= 1
             comm_allreduce = run_ordered

@@ -55,12 +55,14 @@ def _fingerprint() -> str:
 
 
 def build(force: bool = False, verbose: bool = False, variant: str | None = None,
-          defines: tuple = ()) -> Path:
+          defines: tuple = (), only: tuple = ()) -> Path:
     """Compile every csrc/*.cu for sm_100a and link the shared library.
 
     variant/defines: a tuning build (extra -D flags) linked to
     _lib/variants/libgradsync_b200_<variant>.so for A/B measurements (load
-    it with GRADSYNC_B200_LIB); the product library is untouched."""
+    it with GRADSYNC_B200_LIB); the product library is untouched.  only:
+    translation units (stems) a variant recompiles; the others are the
+    product build's objects."""
     libdir = LIBDIR / "variants" if variant else LIBDIR
     libpath = libdir / (f"libgradsync_b200_{variant}.so" if variant else LIBNAME)
     flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
@@ -74,6 +76,9 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
     nvcc = _nvcc()
     objs, cmds = [], []
     for src in _sources():
+        if variant and only and src.stem not in only:
+            objs.append(str(LIBDIR / "obj" / (src.stem + ".o")))  # the product build's
+            continue
         obj = objdir / (src.stem + ".o")
         cmds.append([nvcc, *flags, "-c", str(src), "-o", str(obj)])
         objs.append(str(obj))
@@ -100,4 +105,7 @@ if __name__ == "__main__":
     args = sys.argv[1:]
     var = args[args.index("--variant") + 1] if "--variant" in args else None
     defs = tuple(a[2:] for a in args if a.startswith("-D"))
-    print(build(force="--force" in args, verbose=True, variant=var, defines=defs))
+    only = tuple(args[args.index("--only") + 1].split(",")) if "--only" in args else ()
+    if var and only:
+        build()  # the product objects the variant links against
+    print(build(force="--force" in args, verbose=True, variant=var, defines=defs, only=only))

@@ -41,6 +41,7 @@ import torch
 
 from . import _device as dev
 from . import _native
+from . import _trace
 from ._peer import PeerOp, PeerTimeoutError, decode_status, launch, rank_ctx
 from ._plan import LarsPlan, SegmentSpec, build_chunks, step_params
 from .fusion import copy_table, plan_buckets
@@ -703,10 +704,13 @@ class GradientPipeline:
         s0 = torch.cuda.current_stream(self.device)
         self._pending = True
         self._wire_src = None
+        timer = _trace.hook(timer)
         if self.sharded:
             yield from self._gen_sharded(tabs, s0, timer)
         else:
             yield from self._gen_replicated(tabs, s0, timer)
+        if isinstance(timer, _trace.PhaseRanges):
+            timer.close()
         self.plan.end_step()
 
     def _gen_replicated(self, tabs, s0, timer):
@@ -964,21 +968,28 @@ class GradientPipeline:
         bk, plan, ss = self.buckets[b], self.plan, inc["stream"]
         ss.wait_event(ev)
         sh = int(ss.cuda_stream)
+        rng = _trace.hook(None, f"gs.bucket{b}")
         with torch.cuda.stream(ss):
-            if tab[1]:
-                _native.call("gs_batched_copy", dev.ptr(tab[0]), tab[1], sh)
-            if self.sharded:
-                a, p = self.arena, self.comm.topo.p
-                yield self._op("gs_rs_pass1", p, dev.ptr(a.peers("wire")), dev.ptr(a.peers("sig")),
-                               dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")), b, b + 1,
-                               plan.sp, plan.hint, plan.parity, b + 1, self._nblocks, sh)
-                return
-            if bk.algorithm in ("ordered", "ordered_hier"):
-                yield self._ordered_op(inc["half"], bk, sh, b)
-            elif bk.algorithm != "none":
-                self.comm.allreduce(inc["wire"][bk.start:bk.start + bk.padded], bk.algorithm)
-            if bk.nchunk:
-                plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
+            yield from self._bucket_ops(b, tab, inc, bk, plan, sh)
+        if isinstance(rng, _trace.PhaseRanges):
+            rng.close()
+
+    def _bucket_ops(self, b, tab, inc, bk, plan, sh):
+        """Bucket b on the side stream: pack, reduce, pass 1."""
+        if tab[1]:
+            _native.call("gs_batched_copy", dev.ptr(tab[0]), tab[1], sh)
+        if self.sharded:
+            a, p = self.arena, self.comm.topo.p
+            yield self._op("gs_rs_pass1", p, dev.ptr(a.peers("wire")), dev.ptr(a.peers("sig")),
+                           dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")), b, b + 1,
+                           plan.sp, plan.hint, plan.parity, b + 1, self._nblocks, sh)
+            return
+        if bk.algorithm in ("ordered", "ordered_hier"):
+            yield self._ordered_op(inc["half"], bk, sh, b)
+        elif bk.algorithm != "none":
+            self.comm.allreduce(inc["wire"][bk.start:bk.start + bk.padded], bk.algorithm)
+        if bk.nchunk:
+            plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
 
     def end(self) -> None:
         """Close the step: every bucket must have been submitted; trust and

@@ -49,9 +49,11 @@ def main():
     master = sh.synth_master(specs)
     order = list(reversed(range(len(specs))))
     results = {}
-    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ring,hierarchical,sharded,zero_inc,ordered_inc,ring_inc,"
-                           "zero_host,ordered_host").split(",")
-    for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ring", 1),
+    algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ordered_push,ordered_hier,ring,"
+                           "hierarchical,sharded,zero_inc,ordered_inc,ring_inc,zero_host,"
+                           "ordered_host").split(",")
+    for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ordered_push", 1),
+                         ("ordered_hier", 2), ("ring", 1),
                          ("hierarchical", 2), ("sharded", 2), ("zero_inc", 1), ("ordered_inc", 1),
                          ("ring_inc", 1), ("zero_host", 1), ("ordered_host", 1)):
         if algo_name not in algos:
@@ -64,6 +66,9 @@ def main():
         # per-bucket H2D overlapped with the incremental submission)
         host = algo_name.endswith("_host")
         algo = algo_name[:-4] if inc else algo_name[:-5] if host else algo_name
+        push = algo == "ordered_push"
+        if push:
+            algo = "ordered"
         if world % k or (algo != "ring" and world == 1):
             continue
         comm = Communicator(gs.Topology(world, k))
@@ -72,6 +77,7 @@ def main():
                                    eta_bytes=0 if algo in ("ring", "ordered") else 1 << 62,
                                    hier_variant=algo if algo not in ("ring", "ordered") else "hierarchical",
                                    flat_variant="ordered" if algo == "ordered" else "ring",
+                                   ordered_push=push,
                                    sharded_update=algo.startswith("zero"),
                                    fused_collective=algo == "zero",
                                    init_master=master, loss_scale=gs.LossScale(1024.0), device=dev)
@@ -105,7 +111,7 @@ def main():
                 torch.cuda.synchronize(dev)
             if rank == 0:
                 parts = [split(w, specs) for w in wires]
-                exact = world == 2 or algo in ("ordered", "zero", "zero_unfused")
+                exact = world == 2 or algo in ("ordered", "ordered_hier", "zero", "zero_unfused")
                 out = rp.compose_step_fp16(parts, [s.name for s in specs], [s.numel for s in specs],
                                            order, groups, rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1,
                                            oloss, theta, 0,

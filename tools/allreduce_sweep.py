@@ -42,7 +42,8 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--min-log2", type=int, default=10)
     ap.add_argument("--max-log2", type=int, default=30)
-    ap.add_argument("--variants", default="ring,hierarchical,sharded,ordered,ordered_push")
+    ap.add_argument("--variants",
+                    default="ring,hierarchical,sharded,ordered,ordered_push,ordered_hier")
     ap.add_argument("--out", default=None, help="also write the lines to this file (rank 0)")
     args = ap.parse_args()
 
@@ -51,7 +52,7 @@ def main() -> None:
 
     import paper_1807_11205_b200 as gs
     from paper_1807_11205_b200 import _device as dv
-    from paper_1807_11205_b200 import _native
+    from paper_1807_11205_b200._peer import launch
     from paper_1807_11205_b200.dist import Communicator, OrderedWire, init_from_env
 
     rank, world, local = init_from_env("nccl")
@@ -74,6 +75,10 @@ def main() -> None:
         variants.append(("ordered", 1))
     if "ordered_push" in want:
         variants.append(("ordered_push", 1))
+    if "ordered_hier" in want:
+        for k in (4, 2):
+            if 1 < k < world and world % k == 0:
+                variants.append((f"ordered_hier_{world // k}x{k}", k))
     comms = {k: Communicator(gs.Topology(world, k)) for k in sorted({k for _, k in variants})}
     # bookkeeping reductions on CPU (gloo): NCCL_ALGO=NVLS runs have no fp64/int path
     host = dist.new_group(backend="gloo")
@@ -85,6 +90,8 @@ def main() -> None:
     ow = OrderedWire(comms[1], max_elems, dev) if any(v[0].startswith("ordered") for v in variants) \
         else None
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    if ow is not None:
+        ow.ctx["nonfinite"] = dv.ptr(flag)  # the kernels OR 1 here on a non-finite sum
     tok = torch.zeros(1, dtype=torch.float32, device=dev)
     sleep_cycles = 1.0e7  # ~5 ms at 2 GHz, longer than queueing 50 eager calls
     half = [0]
@@ -95,8 +102,6 @@ def main() -> None:
         for name, k in variants:
             comm = comms[k]
             algo = "ordered" if name.startswith("ordered") else name.split("_")[0]
-            fn = "gs_ordered_allreduce_push_f16" if name == "ordered_push" else \
-                "gs_ordered_allreduce_f16"
             nn = n - n % k if algo == "sharded" else n
             if nn == 0:
                 continue
@@ -107,12 +112,14 @@ def main() -> None:
                     if rank == 0:
                         h[:1].view(torch.int16).fill_(0x7C00)
 
-                def run(_fn=fn):
-                    _native.call(_fn, dv.ptr(ow.bufs_dev[half[0]]),
-                                 dv.ptr(ow.sig_dev), ow.rank, ow.p, 0, nn, 1,
-                                 dv.ptr(ow.epoch_base), ow.grid_for(nn), dv.ptr(flag),
-                                 int(s0.cuda_stream))
-                    ow.advance(1, int(s0.cuda_stream))
+                def run(_push=name == "ordered_push",
+                        _k=k if name.startswith("ordered_hier") else 0):
+                    ow.push = _push
+                    sh = int(s0.cuda_stream)
+                    op = ow.hier_op(half[0], 0, nn, _k, sh) if _k else \
+                        ow.allreduce_op(half[0], 0, nn, sh)
+                    launch([op])
+                    ow.advance(1, sh)
                     half[0] ^= 1
 
                 def result():

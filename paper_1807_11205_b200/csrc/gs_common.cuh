@@ -136,13 +136,6 @@ int gs_check_launch(const char* what);
 // kernel was launched normally), griddep_launch_dependents() lets the next
 // PDL kernel in the stream start launching.
 namespace gs {
-// bulk (TMA) prefetch of [p, p + bytes) into L2; p 16-byte aligned, bytes a
-// multiple of 16 (rounded down here), fire and forget
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  bytes &= ~15u;
-  if (bytes)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

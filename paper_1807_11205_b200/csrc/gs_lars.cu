@@ -41,10 +41,12 @@ namespace {
 // thread, every load issued before any arithmetic).  Per-thread vector order
 // t, t+256, t+512, t+768, then the scalar tail: the summation order of every
 // other pass-1 form (rs_pass1, p1_chunk), so the partials are bit-identical.
-// Measured alternatives (profiles/r02e): a persistent software-pipelined
-// form (3 CTAs/SM: 39.3 us), two chunks per CTA (2 CTAs/SM: 42.9 us) and
-// 3 CTAs/SM (37.4 us) all lost to 4 CTAs/SM x one chunk (34.4 us): pass 1 is
-// bound by memory-level parallelism, i.e. resident warps.
+// Measured alternatives on ResNet-50 (profiles/r02_pass1_variants.md): a
+// persistent software-pipelined form (3 CTAs/SM: 39.3 us), two chunks per
+// CTA (2 CTAs/SM: 42.9 us), 3 CTAs/SM (37.4 us), a TMA bulk L2 prefetch of
+// the chunk one wave ahead (35.8 us) and a persistent cp.async-staged 4-stage
+// ring (45.6 us: latency hidden, but twice the instructions) all lost to 4
+// CTAs/SM x one chunk (34.3 us).
 struct P1Meta {
   const void* g;
   const float* w;
@@ -135,9 +137,6 @@ __device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& 
 #ifndef GS_P1_MINB
 #define GS_P1_MINB 4
 #endif
-#ifndef GS_P1_ASYNC
-#define GS_P1_ASYNC 1  // binary16 pass 1: the cp.async-staged persistent kernel
-#endif
 template <bool F16, bool POW2>
 constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? GS_P1_MINB : 2;
 
@@ -219,189 +218,6 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   p1_finish(m, cached, a, 0, red, partials);
   flag_acc = __reduce_or_sync(0xFFFFFFFFu, flag_acc);
   if (flag_acc != 0u && (threadIdx.x & 31) == 0) atomicOr(&ctl->flags[parity], flag_acc);
-}
-
-// ------------------------------------------ pass 1, cp.async-staged form
-// The one-chunk-per-CTA kernel holds its whole 48 KB batch in registers, so
-// bytes are in flight only between a CTA's table lookups and its compute
-// (ncu r02c: 46 % warps active, long-scoreboard bound, DRAM 59 %).  Here each
-// CTA is persistent (4 per SM, chunks b, b + grid, ...) and streams its
-// chunks through a 4-stage ring in shared memory: a unit = one 2048-element
-// slice of a chunk (thread t's vector k of the register form), every thread
-// copies ITS OWN vectors with cp.async (LDGSTS, L2 -> smem, no register
-// held while in flight) three units ahead of the unit it computes, and waits
-// on its own copy groups only — no barrier between copy and compute.  The
-// table lookups of the chunk after next are issued a whole chunk early.
-// Thread t still visits vectors t, t+256, t+512, t+768 then the scalar tail
-// in that order: the same partials bit for bit.
-constexpr int kSt = 4;  // ring stages (units in flight per thread, incl. the one computed)
-
-struct P1A {
-  const uint16_t* g;
-  const float* w;
-  double wc;
-  int len, c, nsl;     // nsl = units of this chunk (0: no chunk)
-  uint32_t sflags;
-  bool batched;
-};
-
-__device__ __forceinline__ P1A p1a_meta(const gs_segment* __restrict__ segs,
-                                        const gs_chunk* __restrict__ chunks, int c, int cend,
-                                        const double* __restrict__ wsq) {
-  P1A m;
-  m.nsl = 0;
-  if (c >= cend) return m;
-  const P1Meta b = p1_meta<true>(segs, chunks, c, wsq);
-  m.g = static_cast<const uint16_t*>(b.g);
-  m.w = b.w;
-  m.wc = b.wc;
-  m.len = b.len;
-  m.c = b.c;
-  m.sflags = b.sflags;
-  m.batched = p1_batched<true>(b);
-  const int nv = b.len / 8;
-  m.nsl = m.batched ? max(1, (nv + kThreads - 1) / kThreads) : 1;
-  return m;
-}
-
-__device__ __forceinline__ void cp_async16(uint4* smem, const void* gmem) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait(int pending) {
-  switch (pending) {  // at most `pending` of this thread's newest groups still in flight
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-  }
-}
-
-template <bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2>
-__device__ __forceinline__ void p1a_unit(const P1A& m, int k, const uint4* st, const Ctx& cx,
-                                         Acc& a) {
-  const int t = threadIdx.x;
-  if (!m.batched) {  // misaligned / oversized chunk: the generic loop, one unit
-    p1_chunk<true, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(m.g, m.w, m.len, cx, a);
-    return;
-  }
-  const int nv = m.len / 8;
-  if (t + k * kThreads < nv) {
-    F8 wv{};
-    if (LARS) {
-      const uint4 lo = st[kThreads + t], hi = st[2 * kThreads + t];
-      wv.a = make_float4(__uint_as_float(lo.x), __uint_as_float(lo.y), __uint_as_float(lo.z),
-                         __uint_as_float(lo.w));
-      wv.b = make_float4(__uint_as_float(hi.x), __uint_as_float(hi.y), __uint_as_float(hi.z),
-                         __uint_as_float(hi.w));
-    }
-    p1_vec<true, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(st[t], wv, cx, a);
-  }
-  if (k == m.nsl - 1) {  // scalar tail, exactly as p1_chunk's
-    for (int i = nv * 8 + t; i < m.len; i += kThreads) {
-      if (RAWFLAG) a.raw |= raw_nonfinite_bits(m.g[i]);
-      Acc b;
-      p1_pair<POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(make_float2(gs::widen(m.g[i]), 0.0f),
-                                                     make_float2(LARS ? m.w[i] : 0.0f, 0.0f), cx,
-                                                     b);
-      a.sw += b.sw;
-      a.se += b.se;
-      a.sg += b.sg;
-      a.fl |= b.fl;
-    }
-  }
-}
-
-template <bool POW2, bool RAWFLAG, bool GNORM>
-__global__ void __launch_bounds__(kThreads, POW2 ? 4 : 2)
-lars_pass1_async_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
-                        int chunk0, int nchunk, const gs_step_params params,
-                        double* __restrict__ partials, gs_ctl* __restrict__ ctl, uint32_t parity,
-                        const double* __restrict__ wsq) {
-  extern __shared__ uint4 ring[];  // [kSt][3][kThreads]: g, w lo, w hi
-  __shared__ double red[2][3][kThreads / 32];
-  Ctx cx;
-  cx.u.load(&params);
-  cx.mul = params.mul;
-  cx.wd = params.weight_decay;
-  const int t = threadIdx.x, G = gridDim.x, cend = chunk0 + nchunk;
-  int c = chunk0 + blockIdx.x;
-  if (c >= cend) return;
-  // A = chunk being computed, B = next, C = the one after (lookups in flight)
-  P1A A = p1a_meta(segs, chunks, c, cend, wsq);
-  P1A B = p1a_meta(segs, chunks, c + G, cend, wsq);
-  P1A C = p1a_meta(segs, chunks, c + 2 * G, cend, wsq);
-  int ib = 0, ki = 0;  // issue position: chunk (0 = A, 1 = B), unit
-  int iu = 0, cu = 0;  // units issued / computed
-  auto issue = [&]() {
-    if (ib == 0 && ki == A.nsl) { ib = 1; ki = 0; }
-    // fields selected by value (a reference to A or B would put both in
-    // local memory)
-    const bool inb = ib != 0;
-    const int nsl = inb ? B.nsl : A.nsl;
-    if (ki >= nsl || iu - cu >= kSt) return;  // never past B, never > kSt in flight
-    if (inb ? B.batched : A.batched) {
-      const int v = t + ki * kThreads;
-      if (v < (inb ? B.len : A.len) / 8) {
-        uint4* st = ring + (iu % kSt) * 3 * kThreads;
-        cp_async16(st + t, (inb ? B.g : A.g) + 8 * v);
-        if ((inb ? B.sflags : A.sflags) & GS_SEG_LARS_ENABLED) {
-          const float* w = (inb ? B.w : A.w) + 8 * v;
-          cp_async16(st + kThreads + t, w);
-          cp_async16(st + 2 * kThreads + t, w + 4);
-        }
-      }
-    }
-    cp_async_commit();  // one group per unit (possibly empty)
-    ++ki;
-    ++iu;
-  };
-  for (int q = 0; q < kSt - 1; ++q) issue();
-  uint32_t flag_acc = 0;
-  for (int it = 0; A.nsl > 0; ++it) {
-    const bool lars = (A.sflags & GS_SEG_LARS_ENABLED) != 0;
-    const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(A.sflags & GS_SEG_DECAY_EXEMPT);
-    const bool cached = lars && !isnan(A.wc) && A.batched;
-    Acc a;
-    for (int k = 0; k < A.nsl; ++k) {
-      issue();
-      cp_async_wait(iu - cu - 1);  // this unit's copies (and all older ones) landed
-      const uint4* st = ring + (cu % kSt) * 3 * kThreads;
-      if (lars && decay) {
-        if (cached)
-          p1a_unit<POW2, RAWFLAG, GNORM, true, true, false>(A, k, st, cx, a);
-        else
-          p1a_unit<POW2, RAWFLAG, GNORM, true, true, true>(A, k, st, cx, a);
-      } else if (lars) {
-        if (cached)
-          p1a_unit<POW2, RAWFLAG, GNORM, true, false, false>(A, k, st, cx, a);
-        else
-          p1a_unit<POW2, RAWFLAG, GNORM, true, false, true>(A, k, st, cx, a);
-      } else {
-        p1a_unit<POW2, RAWFLAG, GNORM, false, false, true>(A, k, st, cx, a);
-      }
-      ++cu;
-    }
-    if (lars && !decay) {
-      a.se = a.sg;  // eff == g exactly: same terms, same order
-      if (!GNORM) a.sg = 0.0;
-    }
-    flag_acc |= a.fl | ((a.raw & 0x80008000u) ? kBoth : 0u);
-    P1Meta fm;
-    fm.c = A.c;
-    fm.wc = A.wc;
-    p1_finish(fm, cached, a, it, red, partials);
-    // shift the chunk window; the issuer's position moves with it
-    if (ib == 0) { ib = 1; ki = 0; }  // (A fully issued: it was just computed)
-    ib -= 1;
-    c += G;
-    A = B;
-    B = C;
-    C = p1a_meta(segs, chunks, c + 2 * G, cend, wsq);
-  }
-  flag_acc = __reduce_or_sync(0xFFFFFFFFu, flag_acc);
-  if (flag_acc != 0u && (t & 31) == 0) atomicOr(&ctl->flags[parity], flag_acc);
 }
 
 // ----------------------------------------------------------------- trust
@@ -561,33 +377,6 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   }
 }
 
-constexpr size_t kRingBytes = sizeof(uint4) * kSt * 3 * kThreads;  // 48 KB
-
-// the staged pass 1 is persistent: every resident CTA slot, at most one CTA
-// per chunk
-template <bool P, bool R, bool N>
-int launch_p1_async(const gs_segment* segs, const gs_chunk* chunks, int chunk0, int nchunk,
-                    const gs_step_params& params, double* partials, gs_ctl* ctl, uint32_t parity,
-                    const double* wsq, cudaStream_t s) {
-  auto k = lars_pass1_async_kernel<P, R, N>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes) !=
-        cudaSuccess)
-      return gs_check_launch("gs_lars_pass1 (smem attribute)");
-    attr = true;
-  }
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, kRingBytes);
-  int grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
-  if (grid > nchunk) grid = nchunk;
-  k<<<grid, kThreads, kRingBytes, s>>>(segs, chunks, chunk0, nchunk, params, partials, ctl, parity,
-                                       wsq);
-  return gs_check_launch("gs_lars_pass1");
-}
-
 }  // namespace
 
 extern "C" {
@@ -603,9 +392,6 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
              gnorm = hint & GS_HINT_GRADNORM;
 #define GS_P1(F, P, R, N)                                                                       \
   do {                                                                                          \
-    if (F && GS_P1_ASYNC)                                                                       \
-      return launch_p1_async<P, R, N>(segs, chunks, chunk0, nchunk, params, partials, ctl,      \
-                                      parity, wsq, s);                                          \
     lars_pass1_kernel<F, P, R, N><<<nchunk, kThreads, 0, s>>>(segs, chunks, chunk0, nchunk,     \
                                                                params, partials, ctl, parity,   \
                                                                wsq);                            \

@@ -197,6 +197,8 @@ class LocalWorld:
     def gather_state(self, pipes) -> None:
         """Sharded masters / velocities made whole on every rank."""
         self.drive(pipe._gather_gen() for pipe in pipes)
+        for pipe in pipes:
+            pipe._gathered = True
 
     # the incremental API, lockstep over ranks
     def begin(self, pipes, step: int) -> None:

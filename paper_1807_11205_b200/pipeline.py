@@ -423,6 +423,16 @@ class GradientPipeline:
     def gather_state(self) -> None:
         """Make the sharded masters and velocities whole on every rank."""
         self._drive(self._gather_gen())
+        self._gathered = True
+
+    def state_groups(self) -> list:
+        """The ParamGroups with current masters / velocities on this rank: a
+        sharded pipeline keeps only its own chunks of them current between
+        steps, so this gathers first when a step ran since the last gather
+        (collective: every rank calls it).  Replicated pipelines: `groups`."""
+        if self.sharded and not getattr(self, "_gathered", True):
+            self.gather_state()
+        return self.groups
 
     def _drive(self, gen) -> None:
         """Launch this rank's peer ops as they come (one rank per launch)."""
@@ -704,6 +714,7 @@ class GradientPipeline:
         s0 = torch.cuda.current_stream(self.device)
         self._pending = True
         self._wire_src = None
+        self._gathered = False
         timer = _trace.hook(timer)
         if self.sharded:
             yield from self._gen_sharded(tabs, s0, timer)
@@ -912,6 +923,7 @@ class GradientPipeline:
         if ss is not s0:
             ss.wait_stream(s0)
         self._pending = True
+        self._gathered = False
         self._inc = {"step": step, "half": half, "wire": wire, "next": 0, "stream": ss,
                      "ready": [None] * len(self.buckets)}
         return
@@ -1068,9 +1080,7 @@ class GradientPipeline:
         Sharded: gathers the masters / velocities first (collective: every
         rank calls it; each may write its own file)."""
         from .lars import save_checkpoint
-        if self.sharded:
-            self.gather_state()
-        save_checkpoint(path, self.groups, step)
+        save_checkpoint(path, self.state_groups(), step)
 
     def load_checkpoint(self, path) -> int:
         """Restore masters, velocities and working copies from a LARS v1 file

@@ -74,12 +74,12 @@ def test_fusion_plan_matches_reference_golden(golden):
                 off += s.numel
             maps.append(m)
         assert maps == case["maps"]
-        if itemsize == 2:
-            wire_off, buckets, total = plan_layout(specs, order, case["theta"])
-            assert [[list(x) for x in b.unpack_map] for b in buckets] == case["maps"]
-            assert [b.nbytes for b in buckets] == case["bytes"]
-            for b in buckets:
-                assert b.start % BUCKET_ALIGN == 0 and b.padded >= b.length
+        # the pipeline's wire layout: binary16 and the fp32 wire alike
+        wire_off, buckets, total = plan_layout(specs, order, case["theta"], itemsize)
+        assert [[list(x) for x in b.unpack_map] for b in buckets] == case["maps"]
+        assert [b.nbytes for b in buckets] == case["bytes"]
+        for b in buckets:
+            assert b.start % BUCKET_ALIGN == 0 and b.padded >= b.length
     for case in doc["fuzz"]:
         itemsize = 2 if case["dtype"] == "uint16" else 4
         plan = gs.plan_buckets(case["sizes"], itemsize, case["theta"])

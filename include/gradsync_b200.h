@@ -141,6 +141,25 @@ typedef struct gs_rank_ctx {
                                    raw wires the fold reads) */
 } gs_rank_ctx; /* 96 bytes */
 
+/* One rank's buffers for the native step executor (gs_step_*): a HOST
+ * struct (the executor reads it on the host and launches from it). */
+typedef struct gs_step_rank {
+  const gs_copy* pack;          /* optional pack table run before the step (device), or NULL */
+  int32_t npack;
+  int32_t nseg;
+  const gs_segment* segs;       /* device segment / chunk tables */
+  const gs_chunk* chunks;
+  int32_t nchunk;
+  int32_t reserved;
+  double* partials;             /* device scratch of the LARS passes */
+  float* seg_scale;
+  double* seg_out;
+  gs_ctl* ctl;
+  const double* wsq_in;         /* replicated step: w^2 carried into pass 1 (or NULL) */
+  double* wsq_out;              /* replicated step: pass 2's w^2 for the next step (or NULL) */
+  uint32_t* epoch_base;         /* sharded step: the rank's device epoch base */
+} gs_step_rank; /* 96 bytes */
+
 /* Host-side launch hints: which specialised pass-1/pass-2 kernel may be used.
  * A hint is a promise about the params of the launch; 0 is always correct
  * (generic kernel, per-element IEEE division). */
@@ -302,6 +321,26 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
  * stream are visible to every peer, and every peer's to this rank. */
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
                   void* stream);
+
+/* ---- native step executor (gs_step.cu) ---------------------------------
+ * One call launches a whole step — the same kernels, in the same order, as
+ * the pipeline's per-kernel path, without per-kernel host work. */
+
+/* p = 1 / replicated update: [pack] -> gs_lars_pass1 -> gs_lars_trust ->
+ * gs_lars_pass2 (experiment.py:403-412 after the all-reduce). */
+int gs_step_replicated(const gs_step_rank* rank, int g_is_f16, gs_step_params params,
+                       uint32_t hint, uint32_t parity, uint32_t flag_mask, void* stream);
+
+/* The sharded (ZeRO-1) step in fused kernels for `nranks` ranks (1 on a box,
+ * p when emulated; ranks = host array, ctx = device gs_rank_ctx table):
+ * [pack per rank] -> gs_rs_pass1 -> gs_peer_fence -> gs_lars_trust per rank
+ * -> gs_pass2_push -> gs_peer_fence -> epoch base += 4 per rank.  Epochs
+ * 1, 2, 3 of the step; max_own >= every rank's owned chunk count. */
+int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, int p,
+                 const uint64_t* wires, const uint64_t* sig, const uint64_t* peer_partials,
+                 const uint64_t* peer_ctl, const uint64_t* peer_working, int nbuckets,
+                 int max_own, gs_step_params params, uint32_t hint, uint32_t parity,
+                 uint32_t flag_mask, int nblocks, void* stream);
 
 /* ---- LARS (lars.py:142-181) fused over a segment table ---------------- */
 

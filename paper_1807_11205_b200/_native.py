@@ -59,6 +59,13 @@ RANK_CTX_DTYPE = np.dtype([
     ("own_off", "<u8"), ("ctl", "<u8"), ("seg_scale", "<u8"), ("nonfinite", "<u8"),
     ("red", "<u8"),
 ])
+STEP_RANK_DTYPE = np.dtype([
+    ("pack", "<u8"), ("npack", "<i4"), ("nseg", "<i4"), ("segs", "<u8"), ("chunks", "<u8"),
+    ("nchunk", "<i4"), ("reserved", "<i4"), ("partials", "<u8"), ("seg_scale", "<u8"),
+    ("seg_out", "<u8"), ("ctl", "<u8"), ("wsq_in", "<u8"), ("wsq_out", "<u8"),
+    ("epoch_base", "<u8"),
+])
+assert STEP_RANK_DTYPE.itemsize == 96
 assert SEGMENT_DTYPE.itemsize == 64
 assert CTL_DTYPE.itemsize == 48
 assert RANK_CTX_DTYPE.itemsize == 96
@@ -120,6 +127,11 @@ SIGNATURES = {
     "gs_pass2_push": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, StepParams,
                               c_uint32, c_uint32, c_uint32, c_void_p]),
     "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_void_p]),
+    "gs_step_replicated": (c_int, [c_void_p, c_int, StepParams, c_uint32, c_uint32, c_uint32,
+                                   c_void_p]),
+    "gs_step_zero": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                             c_void_p, c_void_p, c_int, c_int, StepParams, c_uint32, c_uint32,
+                             c_uint32, c_int, c_void_p]),
 }
 
 ABI_VERSION = 2

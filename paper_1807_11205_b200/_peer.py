@@ -77,6 +77,19 @@ def _key(a):
     return a
 
 
+def batched_table(ctxs, device=None) -> torch.Tensor:
+    """The device gs_rank_ctx table of several ranks (uploaded once per
+    distinct content and cached)."""
+    raw = b"".join(c.tobytes() for c in ctxs)
+    tab = _CACHE.get(raw)
+    if tab is None:
+        if len(_CACHE) >= _CACHE_MAX:
+            _CACHE.pop(next(iter(_CACHE)))
+        tab = _CACHE[raw] = dev.upload(np.frombuffer(raw, dtype=np.uint8).copy(),
+                                       device or torch.device("cuda", torch.cuda.current_device()))
+    return tab
+
+
 def launch(ops: list[PeerOp]) -> None:
     """Launch one op per rank (ranks in order) as ONE kernel call."""
     if not ops:
@@ -87,14 +100,7 @@ def launch(ops: list[PeerOp]) -> None:
         if op.fn != first.fn or tuple(_key(a) for a in op.args) != key0:
             raise RuntimeError(f"ranks diverged at a peer launch: {first.fn} vs {op.fn} "
                                "(every rank must issue the same collective sequence)")
-    raw = b"".join(op.ctx.tobytes() for op in ops)
-    tab = _CACHE.get(raw)
-    if tab is None:
-        if len(_CACHE) >= _CACHE_MAX:
-            _CACHE.pop(next(iter(_CACHE)))
-        tab = _CACHE[raw] = dev.upload(np.frombuffer(raw, dtype=np.uint8).copy(),
-                                       first.device or torch.device("cuda",
-                                                                    torch.cuda.current_device()))
+    tab = batched_table([op.ctx for op in ops], first.device)
     args = first.args
     if first.count is not None:
         m = max(op.count for op in ops)

@@ -121,6 +121,11 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c) {
 void gs_set_error(const char* fmt, ...);
 int gs_check_launch(const char* what);
 
+// CTAs of `kernel` that fit on the current device at once (occupancy x SMs),
+// cached per (kernel, block, smem, device): the launch path of the peer
+// kernels asks on every call and the driver queries cost microseconds
+int gs_resident_ctas(const void* kernel, int threads, size_t smem);
+
 #define GS_REQUIRE(cond, ...)      \
   do {                             \
     if (!(cond)) {                 \

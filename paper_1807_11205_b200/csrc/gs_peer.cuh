@@ -127,11 +127,7 @@ __device__ __forceinline__ float tree(float (&v)[P]) {
 // The clamp depends only on the kernel and the device, so every rank of a
 // homogeneous box derives the same nb and the signal slots pair up.
 inline int peer_grid(const void* kernel, int threads, size_t smem, int want, int nranks) {
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-  const int cap = per_sm > 0 ? (per_sm * sms) / (nranks > 0 ? nranks : 1) : 1;
+  const int cap = gs_resident_ctas(kernel, threads, smem) / (nranks > 0 ? nranks : 1);
   int nb = want < cap ? want : cap;
   return nb < 1 ? 1 : nb;
 }

@@ -1,6 +1,7 @@
 // gs_runtime.cu — error reporting, version and device queries for the C ABI.
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 
 #include "gs_common.cuh"
 
@@ -11,6 +12,7 @@ static_assert(sizeof(gs_copy) == 24, "gs_copy layout");
 static_assert(sizeof(gs_step_params) == 56, "gs_step_params layout");
 static_assert(sizeof(gs_ctl) == 48, "gs_ctl layout");
 static_assert(sizeof(gs_rank_ctx) == 96, "gs_rank_ctx layout");
+static_assert(sizeof(gs_step_rank) == 96, "gs_step_rank layout");
 
 static thread_local char g_err[512] = "";
 
@@ -28,6 +30,34 @@ int gs_check_launch(const char* what) {
     return GS_ECUDA;
   }
   return GS_OK;
+}
+
+int gs_resident_ctas(const void* kernel, int threads, size_t smem) {
+  struct Entry {
+    const void* k;
+    int threads, dev;
+    size_t smem;
+    int ctas;
+  };
+  static Entry cache[256];
+  static int n = 0;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < n; ++i)
+      if (cache[i].k == kernel && cache[i].threads == threads && cache[i].smem == smem &&
+          cache[i].dev == dev)
+        return cache[i].ctas;
+  }
+  int per_sm = 0, sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  const int ctas = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  std::lock_guard<std::mutex> lock(mu);
+  if (n < 256) cache[n++] = Entry{kernel, threads, dev, smem, ctas};
+  return ctas;
 }
 
 namespace {

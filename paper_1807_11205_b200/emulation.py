@@ -185,13 +185,31 @@ class LocalWorld:
             launch(ops)
             n += 1
 
-    def enqueue(self, pipes, grads, step: int) -> None:
+    def enqueue(self, pipes, grads, step: int, executor: bool = True) -> None:
         """One step of every rank (grads[r] = rank r's gradients), launched on
-        the current stream; finish() each pipe afterwards."""
+        the current stream; finish() each pipe afterwards.  The fused sharded
+        step goes through the native executor (gs_step_zero over all p ranks
+        in one call) unless executor=False, which drives the per-kernel
+        generators in lockstep instead (same kernels, same order)."""
+        if executor and all(pp.sharded and pp.fused_collective for pp in pipes):
+            import numpy as np_
+            from . import _native
+            from ._peer import batched_table
+            tabs = [pp._open_step(g, step) for pp, g in zip(pipes, grads)]
+            recs = np_.concatenate([pp._zero_record(t) for pp, t in zip(pipes, tabs)])
+            ctx = batched_table([pp._ctx for pp in pipes], self.device)
+            sh = int(torch.cuda.current_stream(self.device).cuda_stream)
+            max_own = max(pp._n_own for pp in pipes)
+            _native.call("gs_step_zero", recs.ctypes.data, len(pipes), dev.ptr(ctx),
+                         *pipes[0]._zero_args(max_own, sh))
+            for pp in pipes:
+                pp._last_wire = pp.red
+                pp.plan.end_step()
+            return
         self.drive(pipe._enqueue_gen(g, step) for pipe, g in zip(pipes, grads))
 
-    def step(self, pipes, grads, step: int):
-        self.enqueue(pipes, grads, step)
+    def step(self, pipes, grads, step: int, executor: bool = True):
+        self.enqueue(pipes, grads, step, executor)
         return [pipe.finish() for pipe in pipes]
 
     def gather_state(self, pipes) -> None:

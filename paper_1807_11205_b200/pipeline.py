@@ -402,6 +402,8 @@ class GradientPipeline:
                              chunks=dev.ptr(plan.d_chunks), own_list=dev.ptr(self._own_list),
                              own_off=dev.ptr(self._own_off), ctl=dev.ptr(plan.ctl),
                              seg_scale=dev.ptr(plan.seg_scale), red=dev.ptr(self.red))
+        # this rank's one-entry context table for the native executor
+        self._ctx_dev = dev.upload(self._ctx, d)
 
     def _op(self, fn: str, *args, count: int | None = None) -> PeerOp:
         return PeerOp(fn, self._ctx, args, count=count, device=self.device)
@@ -700,10 +702,90 @@ class GradientPipeline:
         `timer`, if given, is called with a phase name before each phase
         (the bench records CUDA events there).  finish() must be called
         before the next step is enqueued: the LossScale update needs this
-        step's flags (experiment.py:403-413)."""
+        step's flags (experiment.py:403-413).
+
+        The two hot steps (p = 1 and the fused sharded step) go through the
+        native executor (one C call, gs_step_replicated / gs_step_zero) unless
+        a timer or NVTX ranges ask for the per-kernel path; both launch the
+        same kernels in the same order."""
+        if timer is None and not _trace.enabled() and self._fast_ok():
+            tabs = self._open_step(grads, step)
+            sh = int(torch.cuda.current_stream(self.device).cuda_stream)
+            if self.sharded:
+                rec = self._zero_record(tabs)
+                _native.call("gs_step_zero", rec.ctypes.data, 1, dev.ptr(self._ctx_dev),
+                             *self._zero_args(self._n_own, sh))
+                self._last_wire = self.red
+            else:
+                _, seg_tab, views, snap = tabs
+                rec = self._replicated_record(seg_tab, snap)
+                plan = self.plan
+                _native.call("gs_step_replicated", rec.ctypes.data, 1 if self.f16 else 0,
+                             plan.sp, plan.hint, plan.parity, _MASK, sh)
+                self._wire_src = views if snap is None else None
+                self._last_wire = self.wire
+            self.plan.end_step()
+            return
         self._drive(self._enqueue_gen(grads, step, timer))
 
-    def _enqueue_gen(self, grads, step: int, timer=None):
+    # ---- the native executor's records (host structs, rebuilt only when a
+    # pointer changes)
+    def _fast_ok(self) -> bool:
+        if self.emulated:
+            return False
+        if self.sharded:
+            return self.fused_collective
+        return self.comm is None and not self.local
+
+    def _replicated_record(self, seg_tab, snap) -> np.ndarray:
+        plan = self.plan
+        key = (dev.ptr(seg_tab), id(snap))
+        rec = getattr(self, "_rep_rec", None)
+        if rec is None or self._rep_key != key:
+            rec = np.zeros(1, dtype=_native.STEP_RANK_DTYPE)
+            nb = len(self.buckets)
+            if snap is not None and snap[nb][1]:
+                rec["pack"], rec["npack"] = dev.ptr(snap[nb][0]), snap[nb][1]
+            rec["segs"], rec["chunks"] = dev.ptr(seg_tab), dev.ptr(plan.d_chunks)
+            rec["nseg"], rec["nchunk"] = plan.nseg, plan.nchunk
+            rec["partials"], rec["seg_scale"] = dev.ptr(plan.partials), dev.ptr(plan.seg_scale)
+            rec["seg_out"], rec["ctl"] = dev.ptr(plan.seg_out), dev.ptr(plan.ctl)
+            self._rep_rec, self._rep_key = rec, key
+            self._rep_refs = (seg_tab, snap)  # keep the tables alive with the record
+        wsq = plan.wsq
+        rec["wsq_out"] = dev.ptr(wsq) if wsq is not None else 0
+        rec["wsq_in"] = dev.ptr(wsq) if wsq is not None and plan.wsq_valid else 0
+        return rec
+
+    def _zero_record(self, tabs) -> np.ndarray:
+        """gs_step_zero's rank record (pack table = the all-bucket table, or
+        none when the gradients already lie in the raw wire)."""
+        key = id(tabs)
+        rec = getattr(self, "_zero_rec", None)
+        if rec is None or self._zero_key != key:
+            plan, nb = self.plan, len(self.buckets)
+            rec = np.zeros(1, dtype=_native.STEP_RANK_DTYPE)
+            if tabs is not None and tabs[nb][1]:
+                rec["pack"], rec["npack"] = dev.ptr(tabs[nb][0]), tabs[nb][1]
+            rec["segs"], rec["chunks"] = dev.ptr(plan.base_segs), dev.ptr(plan.d_chunks)
+            rec["nseg"], rec["nchunk"] = plan.nseg, plan.nchunk
+            rec["partials"], rec["seg_scale"] = dev.ptr(plan.partials), dev.ptr(plan.seg_scale)
+            rec["seg_out"], rec["ctl"] = dev.ptr(plan.seg_out), dev.ptr(plan.ctl)
+            rec["epoch_base"] = dev.ptr(self.epoch_base)
+            self._zero_rec, self._zero_key, self._zero_refs = rec, key, tabs
+        return rec
+
+    def _zero_args(self, max_own: int, sh: int) -> tuple:
+        """The arguments of gs_step_zero after (ranks, nranks, ctx)."""
+        a, plan = self.arena, self.plan
+        return (self.comm.topo.p, dev.ptr(a.peers("wire")), dev.ptr(a.peers("sig")),
+                dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")),
+                dev.ptr(a.peers("working")), len(self.buckets), max_own, plan.sp, plan.hint,
+                plan.parity, _MASK, self._nblocks, sh)
+
+    def _open_step(self, grads, step: int):
+        """Host prologue of every step: the previous step finished, scalars
+        staged, launch tables for these gradients."""
         if self._pending:
             raise RuntimeError("the previous step was not finished: call finish() before "
                                "enqueueing the next step (its flags drive the loss scale)")
@@ -711,10 +793,14 @@ class GradientPipeline:
             self.prepare(step)
         self._prepared = None
         tabs = self._sources(grads)
-        s0 = torch.cuda.current_stream(self.device)
         self._pending = True
         self._wire_src = None
         self._gathered = False
+        return tabs
+
+    def _enqueue_gen(self, grads, step: int, timer=None):
+        tabs = self._open_step(grads, step)
+        s0 = torch.cuda.current_stream(self.device)
         timer = _trace.hook(timer)
         if self.sharded:
             yield from self._gen_sharded(tabs, s0, timer)

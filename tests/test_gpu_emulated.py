@@ -149,7 +149,7 @@ def test_missing_peer_times_out_without_hanging():
 
 # ---------------------------------------------------------------- pipelines
 def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject_step=2,
-                 incremental=False, in_place=False, specs=None, k=1, **kw):
+                 incremental=False, in_place=False, specs=None, k=1, executor=True, **kw):
     d = dev.require_cuda()
     specs = specs or sh.load_shapes(model)
     master = sh.synth_master(specs, seed=0)
@@ -185,7 +185,7 @@ def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject
             world.end(pipes)
             res = [pipe.finish() for pipe in pipes]
         else:
-            res = world.step(pipes, grads, step)
+            res = world.step(pipes, grads, step, executor=executor)
         out = rp.compose_step_fp16([split(w, specs) for w in wires], [s.name for s in specs],
                                    [s.numel for s in specs], order, groups,
                                    rp.LarsHyper(0.001, 0.0, 5e-4, 0.9), 0.1, oloss, theta,
@@ -209,12 +209,14 @@ def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject
     return pipes
 
 
-@pytest.mark.parametrize("p", [2, 4, 8])
-def test_sharded_fused_step_bit_exact(p):
+@pytest.mark.parametrize("p,executor", [(2, True), (4, True), (8, True), (2, False), (8, False)])
+def test_sharded_fused_step_bit_exact(p, executor):
     """gs_rs_pass1 + trust + gs_pass2_push + gs_peer_fence (ZeRO-1 step),
     shufflenet shapes, theta = 256 KiB, 3 steps, +Inf on the last rank at
-    step 2 (skipped everywhere, loss scale halved)."""
-    pipes = run_emulated(p, sharded_update=True)
+    step 2 (skipped everywhere, loss scale halved) — through the native
+    executor (gs_step_zero, all ranks in one call) and through the
+    per-kernel generators in lockstep."""
+    pipes = run_emulated(p, sharded_update=True, executor=executor)
     assert pipes[0].fused_collective
     assert pipes[0].loss_scale.scale == 512.0
 

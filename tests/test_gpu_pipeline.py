@@ -225,3 +225,24 @@ def test_host_gradient_path_matches_device_path():
         assert ra.applied == rb.applied and ra.grad_norm == rb.grad_norm
         assert torch.equal(a.master, b.master) and torch.equal(a.working, b.working)
         assert torch.equal(a.velocity, b.velocity)
+
+
+def test_per_kernel_path_equals_executor():
+    """The per-kernel launch path (taken when a timer or NVTX asks for
+    phases) and the native executor (gs_step_replicated) give the same
+    state bit for bit, step after step."""
+    specs = sh.load_shapes("shufflenet_v2_x0_5")
+    master = sh.synth_master(specs, seed=0)
+    cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
+    a = gs.GradientPipeline(specs, cfg, threshold_bytes=256 << 10, init_master=master)
+    b = gs.GradientPipeline(specs, cfg, threshold_bytes=256 << 10, init_master=master)
+    phases = []
+    for step in range(3):
+        g = torch.from_numpy(sh.synth_wire_grads(specs, rank=0, seed=step)).cuda()
+        ra = a.step(g, step)
+        b.enqueue(g, step, timer=phases.append)
+        rb = b.finish()
+        assert (ra.applied, ra.grad_norm, ra.flags) == (rb.applied, rb.grad_norm, rb.flags)
+        for name in ("master", "velocity", "working"):
+            assert torch.equal(getattr(a, name), getattr(b, name)), (step, name)
+    assert phases[:4] == ["pass1", "trust", "pass2", "end"]

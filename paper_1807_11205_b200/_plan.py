@@ -20,7 +20,9 @@ import torch
 from . import _device as dev
 from . import _native
 
-#: elements per chunk: 256 threads x 8 elements x 4 unrolled rounds
+#: elements per chunk: 256 threads x 8 elements x 4 unrolled rounds (the
+#: pass-1 batch).  4096-element chunks with 6 CTAs/SM measured no better
+#: (profiles/r02/pass1_variants.md)
 CHUNK_ELEMS = 8192
 
 

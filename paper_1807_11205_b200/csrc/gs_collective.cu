@@ -40,6 +40,7 @@ __device__ __forceinline__ void subrange(int64_t n, int p, int r, int nb, int b,
   const int64_t sub = ((s1 - s0 + nb - 1) / nb + 7) / 8 * 8;
   lo = min(s1, s0 + (int64_t)b * sub);
   hi = min(s1, lo + sub);
+  GS_DCHECK(0 <= lo && lo <= hi && hi <= n, "collective sub-range");
 }
 
 // fold [lo, hi) of every peer's buffer into mine (pairwise tree, P <= 8);

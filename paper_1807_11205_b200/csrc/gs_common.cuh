@@ -14,8 +14,24 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/gradsync_b200.h"
+
+// ---- device-side checks (a GS_CHECKS=1 build; compute-sanitizer is not
+// available on the GPU pool): table indices, ranges and launch invariants are
+// asserted in the kernels, and a failed check prints its site and traps
+#ifndef GS_CHECKS
+#define GS_CHECKS 0
+#endif
+#define GS_DCHECK(cond, what)                                                             \
+  do {                                                                                    \
+    if (GS_CHECKS && !(cond)) {                                                           \
+      printf("gs check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
 
 namespace gs {
 

@@ -102,6 +102,7 @@ constexpr int kRsMinBlocks = !POW2 ? 2 : P <= 4 ? 4 : 3;
 __device__ __forceinline__ void own_range(const gs_rank_ctx& R, int b0, int b1, int& i0, int& i1) {
   i0 = R.own_off[b0];
   i1 = R.own_off[b1];
+  GS_DCHECK(0 <= i0 && i0 <= i1, "owned chunk list range");
 }
 
 template <int P, bool POW2, bool RAWFLAG, bool GNORM>
@@ -130,6 +131,7 @@ rs_pass1_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t* _
     const int c = R.own_list[ci];
     const gs_chunk ch = R.chunks[c];
     const gs_segment* sp = R.segs + ch.seg;
+    GS_DCHECK(c >= 0 && ch.len >= 0 && ch.start + ch.len <= sp->n, "rs_pass1: owned chunk");
     const uint32_t sflags = sp->flags;
     uint16_t* mine = const_cast<uint16_t*>(static_cast<const uint16_t*>(sp->g)) + ch.start;
     const size_t off = reinterpret_cast<const uint8_t*>(mine) - mybase;

@@ -64,6 +64,8 @@ __device__ __forceinline__ P1Meta p1_meta(const gs_segment* __restrict__ segs,
   m.c = c;
   m.wc = wsq != nullptr ? wsq[c] : __longlong_as_double(0x7FF8000000000000ll);
   const gs_chunk ch = chunks[c];
+  GS_DCHECK(ch.seg >= 0 && ch.len >= 0 && ch.start >= 0, "pass 1: chunk table entry");
+  GS_DCHECK(ch.start + ch.len <= segs[ch.seg].n, "pass 1: chunk inside its segment");
   const gs_segment* sp = segs + ch.seg;
   m.g = static_cast<const T*>(sp->g) + ch.start;
   m.w = sp->w + ch.start;
@@ -263,6 +265,7 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, int nchunk,
     return;
   }
   const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
+  GS_DCHECK(cb >= 0 && cn >= 0 && cb + cn <= nchunk, "trust: segment's chunk range");
   double x = 0.0, y = 0.0, z = 0.0;
 #pragma unroll 2
   for (int i = threadIdx.x; i < cn; i += kThreads) {
@@ -349,7 +352,9 @@ lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   using T = typename G<F16>::T;
   const int c = chunk0 + (int)(gridDim.x - 1 - blockIdx.x);
   const gs_chunk ch = chunks[c];
+  GS_DCHECK(ch.seg >= 0 && ch.len >= 0 && ch.start >= 0, "pass 2: chunk table entry");
   const gs_segment* sgp = segs + ch.seg;
+  GS_DCHECK(ch.start + ch.len <= sgp->n, "pass 2: chunk inside its segment");
   const uint32_t sflags = sgp->flags;
   const T* g = static_cast<const T*>(sgp->g) + ch.start;
   Ctx cx;

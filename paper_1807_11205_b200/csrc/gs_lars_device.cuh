@@ -9,12 +9,10 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRounds = 4;                      // 8-element vectors per thread
 #ifndef GS_P1_ROUNDS
 #define GS_P1_ROUNDS 4   // pass-1 load batch (vectors per thread)
 #endif
 constexpr int kP1Rounds = GS_P1_ROUNDS;
-constexpr int kFullChunk = kThreads * 8 * kRounds;  // 8192
 constexpr int kTrustThreads = 1024;
 constexpr uint32_t kBoth = GS_FLAG_SCALED_NONFINITE | GS_FLAG_GRAD_NONFINITE;
 
@@ -171,7 +169,7 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
   const bool vec = p1_vec_path<LARS>(g, w);
   const int nv = vec ? len / 8 : 0;
   const int t = threadIdx.x;
-  // full batches of kRounds vectors per thread: issue every load of the
+  // full batches of kP1Rounds vectors per thread: issue every load of the
   // batch (4 x 16 B of g, 4 x 32 B of w) before any arithmetic; each thread
   // still visits its vectors t, t+256, t+512, ... in increasing order, so
   // the batching never changes the summation order

@@ -68,6 +68,7 @@ __device__ __forceinline__ PeerCta peer_cta(const gs_rank_ctx* __restrict__ rank
 __device__ __forceinline__ void peer_barrier(const uint64_t* __restrict__ sig, const PeerCta& c,
                                              int p, int phase, uint32_t epoch, uint32_t site) {
   __syncthreads();
+  GS_DCHECK(c.R->rank >= 0 && c.R->rank < p && c.lb < c.nb && phase < 3, "peer barrier geometry");
   if (threadIdx.x < p) {
     const int q = threadIdx.x;
     const int rank = c.R->rank;

@@ -316,7 +316,9 @@ class GradientPipeline:
         self._inc = None
         real_comm = comm is not None and not self.emulated
         self._pack_stream = torch.cuda.Stream(device=d) if real_comm else None
-        self._side_stream = torch.cuda.Stream(device=d) if real_comm else None
+        # the incremental API's side stream (bucket work under backward);
+        # emulated ranks keep one stream so their peer launches batch
+        self._side_stream = torch.cuda.Stream(device=d) if not self.emulated else None
         if self.local:
             self.rank_wire = [torch.zeros(self.total, dtype=self.wdt, device=d)
                               for _ in range(self.p)]

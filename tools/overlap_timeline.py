@@ -55,15 +55,19 @@ class Net(torch.nn.Module):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/overlap")
-    ap.add_argument("--theta", type=int, default=256 << 10)
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--theta", type=int, default=1 << 20)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--res", type=int, default=64)
+    ap.add_argument("--width", type=int, default=256)
     args = ap.parse_args()
     torch.manual_seed(0)
-    net = Net().cuda()
+    # GPU-bound backward (each conv's backward takes longer than the host
+    # needs to launch it), so a side-stream kernel CAN run beside it
+    net = Net(width=args.width).cuda()
     cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
     drv = gs.BackwardOverlap.for_module(net, cfg, threshold_bytes=args.theta,
                                         loss_scale=gs.LossScale(1024.0))
-    x = torch.randn(args.batch, 3, 32, 32, device="cuda").half()
+    x = torch.randn(args.batch, 3, args.res, args.res, device="cuda").half()
     y = torch.randint(0, 100, (args.batch,), device="cuda")
 
     def one(step):
@@ -107,15 +111,25 @@ def main():
 
     side_time = sum(e["dur"] for e in side)
     side_under = sum(overlap(e["ts"], e["ts"] + e["dur"]) for e in side)
+    # per step: the compute stream's last non-optimizer kernel (end of
+    # backward) to the end of pass 2 = what the optimizer step adds
+    p2 = sorted(e["ts"] + e["dur"] for e in ours if "lars_pass2" in e["name"])
+    tails = []
+    for end in p2:
+        before = [t for s_, t in comp if t <= end]
+        if before:
+            tails.append(end - max(before))
     ranges = [e for e in ev if e.get("cat") == "user_annotation" and e["name"].startswith("gs.")]
     summary = {
         "trace": trace, "theta": args.theta, "buckets": len(drv.pipe.buckets),
         "params": sum(drv.pipe.sizes), "compute_stream": comp_stream,
-        "our_kernels_by_stream": {str(k): sorted({e["name"].split("(")[0][-40:] for e in v})
-                                  for k, v in by_stream.items()},
+        "our_kernels_by_stream": {str(k): sorted({next(o for o in OURS if o in e["name"])
+                                                  for e in v}) for k, v in by_stream.items()},
         "side_stream_kernel_us": round(side_time, 1),
         "side_stream_us_under_backward": round(side_under, 1),
         "side_overlap_fraction": round(side_under / side_time, 3) if side_time else None,
+        "exposed_tail_us_per_step": [round(t, 1) for t in tails],
+        "config": {"batch": args.batch, "res": args.res, "width": args.width, "depth": 10},
         "nvtx_ranges": sorted({e["name"] for e in ranges}),
         "steps_profiled": 3,
     }

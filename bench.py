@@ -59,6 +59,8 @@ def parse():
                     help="forced overflow: rank 0's gradient carries +Inf, every step takes "
                          "the skip path (fixed loss-scale policy so the scale stays put)")
     ap.add_argument("--no-soak", action="store_true", help="skip the clock soak (profiling runs)")
+    ap.add_argument("--no-grad-norm", action="store_true",
+                    help="A/B only: do not compute the grad-norm metric (experiment.py:408-411)")
     return ap.parse_args()
 
 
@@ -306,7 +308,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                                fused_collective=args.algorithm == "zero",
                                init_master=sh.synth_master(specs, seed=0),
                                loss_scale=gs.LossScale(1024.0, policy="fixed" if args.overflow
-                                                       else "dynamic"), device=dev)
+                                                       else "dynamic"), device=dev,
+                               grad_norm=not args.no_grad_norm)
     wire_np = sh.synth_wire_grads(specs, rank=rank, seed=0)
     if args.overflow and rank == 0:
         wire_np[len(wire_np) // 2] = 0x7C00  # +Inf: every step is skipped
@@ -365,11 +368,16 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # ---- timed region: K steps, each alone between an L2 flush and its flag
     # read; device time by CUDA events on the launching stream
     barrier()
-    launches0 = _native.launch_count
+    launches0 = _native.kernel_launches()
     step_ms = []
     for i in range(args.steps):
         flush_l2()
         pipe.prepare(args.warmup + i)  # host-only: schedule, loss scale, hint
+        # the stream sleeps while the host enqueues the step (as in training,
+        # where the host runs ahead of the device): the events time the
+        # device, not the host prologue; at N > 1 the barrier after the sleep
+        # starts every rank's step together
+        torch.cuda._sleep(1_000_000)
         device_barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -378,7 +386,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         b.record(s0)
         res = pipe.finish()
         step_ms.append(a.elapsed_time(b))
-    launches = _native.launch_count - launches0 - args.steps  # minus the L2 flushes
+    launches = _native.kernel_launches() - launches0 - args.steps  # minus the L2 flushes
     barrier()
     clk = clocks.stop()
 

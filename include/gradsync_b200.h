@@ -173,6 +173,9 @@ typedef struct gs_step_rank {
 int gs_abi_version(void);
 const char* gs_last_error(void);
 int gs_device_sm_count(int device);
+/* Number of kernels this library has launched so far in the process (every
+ * launch site counts once per kernel; bench.py's gpu_launches evidence). */
+int64_t gs_kernel_launches(void);
 
 /* ---- halfprec (halfprec.py) -------------------------------------------- */
 

@@ -91,6 +91,7 @@ assert ctypes.sizeof(StepParams) == STEP_PARAMS_DTYPE.itemsize
 #: every symbol include/gradsync_b200.h declares, with its ctypes signature
 SIGNATURES = {
     "gs_abi_version": (c_int, []),
+    "gs_kernel_launches": (c_int64, []),
     "gs_last_error": (ctypes.c_char_p, []),
     "gs_device_sm_count": (c_int, [c_int]),
     "gs_f32_to_f16": (c_int, [c_void_p, c_void_p, c_int64, c_float, c_void_p, c_void_p]),
@@ -183,7 +184,7 @@ def check(status: int, what: str) -> None:
 
 #: entry points that launch a kernel (everything but the queries)
 _LAUNCHING = {n for n in SIGNATURES if n not in ("gs_abi_version", "gs_last_error",
-                                                 "gs_device_sm_count")}
+                                                 "gs_device_sm_count", "gs_kernel_launches")}
 #: running count of kernel-launching calls (bench.py's gpu_launches evidence)
 launch_count = 0
 
@@ -193,6 +194,12 @@ def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args), name)
     if name in _LAUNCHING:
         launch_count += 1
+
+
+def kernel_launches() -> int:
+    """Kernels the library has launched in this process (counted in C at
+    every launch site, so one gs_step_* call counts each of its kernels)."""
+    return int(lib().gs_kernel_launches())
 
 
 def stream_handle(stream=None) -> int:

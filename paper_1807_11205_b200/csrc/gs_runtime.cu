@@ -1,4 +1,5 @@
 // gs_runtime.cu — error reporting, version and device queries for the C ABI.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -15,6 +16,7 @@ static_assert(sizeof(gs_rank_ctx) == 96, "gs_rank_ctx layout");
 static_assert(sizeof(gs_step_rank) == 96, "gs_step_rank layout");
 
 static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
 
 void gs_set_error(const char* fmt, ...) {
   va_list ap;
@@ -24,6 +26,7 @@ void gs_set_error(const char* fmt, ...) {
 }
 
 int gs_check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     gs_set_error("%s: %s", what, cudaGetErrorString(e));
@@ -78,6 +81,8 @@ extern "C" {
 int gs_abi_version(void) { return GS_ABI_VERSION; }
 
 const char* gs_last_error(void) { return g_err; }
+
+int64_t gs_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int gs_device_sm_count(int device) {
   int v = 0;

@@ -95,23 +95,6 @@ __device__ __forceinline__ void p1_issue(const P1Meta& m, P1Batch<F16>& bt) {
   const int nv = m.len / 8, t = threadIdx.x;
   const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
   const typename Gt::T* g = static_cast<const typename Gt::T*>(m.g);
-#if GS_L2HINT
-  const uint64_t pol = pol_keep();
-#pragma unroll
-  for (int k = 0; k < kP1Rounds; ++k)
-    if (t + k * kThreads < nv) bt.gv[k] = ldg_pol<F16>(g + 8 * (t + k * kThreads), pol);
-  if (lars) {
-#if GS_L2HINT == 3
-#pragma unroll
-    for (int k = 0; k < kP1Rounds; ++k)
-      if (t + k * kThreads < nv) bt.wv[k] = ldw(m.w + 8 * (t + k * kThreads));
-#else
-#pragma unroll
-    for (int k = 0; k < kP1Rounds; ++k)
-      if (t + k * kThreads < nv) bt.wv[k] = ldw_pol(m.w + 8 * (t + k * kThreads), pol);
-#endif
-  }
-#else
 #pragma unroll
   for (int k = 0; k < kP1Rounds; ++k)
     if (t + k * kThreads < nv) bt.gv[k] = Gt::ld(g + 8 * (t + k * kThreads));
@@ -120,7 +103,6 @@ __device__ __forceinline__ void p1_issue(const P1Meta& m, P1Batch<F16>& bt) {
     for (int k = 0; k < kP1Rounds; ++k)
       if (t + k * kThreads < nv) bt.wv[k] = ldw(m.w + 8 * (t + k * kThreads));
   }
-#endif
 }
 
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2>
@@ -327,19 +309,10 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
   // the arithmetic and stores (stores cannot alias the next batch's loads,
   // but the compiler cannot prove it through the casts)
   int done = 0;
-#if GS_L2HINT
-  const uint64_t pol = pol_drop();
-#endif
   for (; done + 2 * kThreads <= nv; done += 2 * kThreads) {
     const int i0 = done + t, i1 = i0 + kThreads;
-#if GS_L2HINT
-    const typename Gt::V g0 = ldg_pol<F16>(g + 8 * i0, pol), g1 = ldg_pol<F16>(g + 8 * i1, pol);
-    const F8 w0 = ld8_pol(w, i0, pol), w1 = ld8_pol(w, i1, pol), v0 = ld8_pol(v, i0, pol),
-             v1 = ld8_pol(v, i1, pol);
-#else
     const typename Gt::V g0 = Gt::ld(g + 8 * i0), g1 = Gt::ld(g + 8 * i1);
     const F8 w0 = ld8(w, i0), w1 = ld8(w, i1), v0 = ld8(v, i0), v1 = ld8(v, i1);
-#endif
     if (!have_s) {  // uniform: every thread runs the first batch
       if (!scale_of()) return;
       have_s = true;
@@ -420,18 +393,6 @@ int gs_lars_pass1(const gs_segment* segs, const gs_chunk* chunks, int chunk0, in
   if (nchunk == 0) return GS_OK;
   GS_REQUIRE(segs && chunks && partials && ctl, "gs_lars_pass1: null pointer");
   cudaStream_t s = (cudaStream_t)stream;
-#if GS_L2SETASIDE
-  static bool set_aside = false;
-  if (!set_aside) {
-    // evict_last lines live in the persisting set-aside (0 B by default)
-    int dev = 0, mx = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx);
-    fprintf(stderr, "gs: persisting L2 set-aside %d bytes\n", mx);
-    set_aside = true;
-  }
-#endif
   const bool pow2 = hint & GS_HINT_POW2, raw = g_is_f16 && pow2 && (hint & GS_HINT_RAWFLAG),
              gnorm = hint & GS_HINT_GRADNORM;
 #define GS_P1(F, P, R, N)                                                                       \

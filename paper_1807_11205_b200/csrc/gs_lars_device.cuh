@@ -134,65 +134,6 @@ struct G<false> {
 __device__ __forceinline__ F8 ldw(const float* p) {
   return F8{__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
 }
-
-// ---- L2 eviction priorities (createpolicy + ld ... L2::cache_hint).  Pass 1
-// reads g and w once more than pass 2 needs them again; tagging pass 1's
-// reads evict_last and pass 2's last reads evict_first keeps the re-read set
-// in the 126 MB L2 instead of letting pass 2's streams evict it.
-#ifndef GS_L2HINT
-#define GS_L2HINT 0
-#endif
-#ifndef GS_L2SETASIDE
-#define GS_L2SETASIDE 0
-#endif
-#ifndef GS_L2FRAC
-#define GS_L2FRAC 1.0
-#endif
-#define GS_STR2(x) #x
-#define GS_STR(x) GS_STR2(x)
-__device__ __forceinline__ uint64_t pol_keep() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, " GS_STR(GS_L2FRAC) ";"
-               : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_drop() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint4 ldnc_u4(const void* p, uint64_t pol) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float4 ldnc_f4(const void* p, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float4 ld_f4(const void* p, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-template <bool F16>
-__device__ __forceinline__ typename G<F16>::V ldg_pol(const typename G<F16>::T* p, uint64_t pol) {
-  if constexpr (F16) {
-    return ldnc_u4(p, pol);
-  } else {
-    return F8{ldnc_f4(p, pol), ldnc_f4(p + 4, pol)};
-  }
-}
-__device__ __forceinline__ F8 ldw_pol(const float* p, uint64_t pol) {
-  return F8{ldnc_f4(p, pol), ldnc_f4(p + 4, pol)};
-}
-__device__ __forceinline__ F8 ld8_pol(const float* p, int i, uint64_t pol) {
-  return F8{ld_f4(p + 8 * i, pol), ld_f4(p + 8 * i + 4, pol)};
-}
 __device__ __forceinline__ float2 wpair(const F8& v, int q) {
   return q == 0 ? make_float2(v.a.x, v.a.y) : q == 1 ? make_float2(v.a.z, v.a.w)
        : q == 2 ? make_float2(v.b.x, v.b.y) : make_float2(v.b.z, v.b.w);

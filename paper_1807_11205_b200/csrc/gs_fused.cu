@@ -95,8 +95,10 @@ __device__ __forceinline__ void rs_p1_chunk(const uint16_t* const (&src)[P], uin
 
 // residency: every CTA waits for its peers at entry, so the whole launch
 // must fit at once (peer_grid clamps nb with the occupancy calculator)
-template <int P, bool POW2>
-constexpr int kRsMinBlocks = !POW2 ? 2 : P <= 4 ? 4 : 3;
+// (the power-of-two form with per-element finite tests needs more than 64
+// registers at P = 4: 3 CTAs / SM so it does not spill)
+template <int P, bool POW2, bool RAWFLAG>
+constexpr int kRsMinBlocks = !POW2 ? 2 : (P <= 4 && RAWFLAG) ? 4 : 3;
 
 // owned chunks [own_off[b0], own_off[b1]) of the rank's chunk list
 __device__ __forceinline__ void own_range(const gs_rank_ctx& R, int b0, int b1, int& i0, int& i1) {
@@ -106,7 +108,7 @@ __device__ __forceinline__ void own_range(const gs_rank_ctx& R, int b0, int b1, 
 }
 
 template <int P, bool POW2, bool RAWFLAG, bool GNORM>
-__global__ void __launch_bounds__(kThreads, (kRsMinBlocks<P, POW2>))
+__global__ void __launch_bounds__(kThreads, (kRsMinBlocks<P, POW2, RAWFLAG>))
 rs_pass1_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t* __restrict__ wires,
                 const uint64_t* __restrict__ sig, const uint64_t* __restrict__ peer_partials,
                 const uint64_t* __restrict__ peer_ctl, int b0, int b1, const gs_step_params params,

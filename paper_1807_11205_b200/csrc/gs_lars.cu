@@ -139,8 +139,10 @@ __device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& 
 #ifndef GS_P1_MINB
 #define GS_P1_MINB 4
 #endif
-template <bool F16, bool POW2>
-constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? GS_P1_MINB : 2;
+// (the power-of-two form with per-element finite tests, mul > 1, needs a few
+// more registers than 64: 3 CTAs / SM so it does not spill)
+template <bool F16, bool POW2, bool RAWFLAG>
+constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? (RAWFLAG ? GS_P1_MINB : 3) : 2;
 
 // one chunk's partials: the fixed block tree of gs::block_sum3 over
 // double-buffered scratch (one barrier per chunk)
@@ -199,7 +201,7 @@ __device__ __forceinline__ uint32_t p1_run(const P1Meta& cur, const P1Batch<F16>
 }
 
 template <bool F16, bool POW2, bool RAWFLAG, bool GNORM>
-__global__ void __launch_bounds__(kThreads, (kP1MinBlocks<F16, POW2>))
+__global__ void __launch_bounds__(kThreads, (kP1MinBlocks<F16, POW2, RAWFLAG>))
 lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
                   int chunk0, int nchunk, const gs_step_params params,
                   double* __restrict__ partials, gs_ctl* __restrict__ ctl, uint32_t parity,
@@ -245,7 +247,6 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, int nchunk,
       // the next step's flag word and counter (the host read them after the
       // previous step; nobody touches them before this step ends)
       ctl->flags[parity ^ 1u] = 0u;
-      ctl->counter[parity ^ 1u] = 0u;
       if (npeers > 0) {
         // sharded update with separate collectives: the step is rejected if
         // any rank saw a non-finite value
@@ -344,7 +345,7 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
 // forward, so the first chunks pass 2 needs are the ones still in L2
 // (ResNet-50: 84.0 -> 81.2 us, profiles/r02a)
 template <bool F16, bool POW2>
-__global__ void __launch_bounds__(kThreads, POW2 ? 4 : 2)
+__global__ void __launch_bounds__(kThreads, F16 && POW2 ? 4 : POW2 ? 3 : 2)
 lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
                   int chunk0, const gs_step_params params, const float* __restrict__ seg_scale,
                   const gs_ctl* __restrict__ ctl, uint32_t parity, uint32_t flag_mask,

@@ -51,21 +51,28 @@ def main():
     results = {}
     algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ordered_push,ordered_hier,ring,"
                            "hierarchical,sharded,zero_inc,ordered_inc,ring_inc,zero_host,"
-                           "ordered_host").split(",")
+                           "ordered_host,zero_busy,ordered_busy").split(",")
     for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ordered_push", 1),
                          ("ordered_hier", 2), ("ring", 1),
                          ("hierarchical", 2), ("sharded", 2), ("zero_inc", 1), ("ordered_inc", 1),
-                         ("ring_inc", 1), ("zero_host", 1), ("ordered_host", 1)):
+                         ("ring_inc", 1), ("zero_host", 1), ("ordered_host", 1),
+                         ("zero_busy", 1), ("ordered_busy", 1)):
         if algo_name not in algos:
             continue
         # *_inc: the same step driven through the incremental API the
         # backward-overlap driver uses (begin / submit per bucket / end),
         # buckets submitted in REVERSE order to exercise the in-order gating
-        inc = algo_name.endswith("_inc")
+        # *_busy: the incremental path while another stream keeps every SM
+        # busy with GEMMs of a rank-dependent length (the backward pass the
+        # overlap driver runs against): the spin-waiting peer kernels must
+        # still make progress and give the same bits
+        busy = algo_name.endswith("_busy")
+        inc = algo_name.endswith("_inc") or busy
         # *_host: the same step from a pinned HOST gradient (enqueue_host:
         # per-bucket H2D overlapped with the incremental submission)
         host = algo_name.endswith("_host")
-        algo = algo_name[:-4] if inc else algo_name[:-5] if host else algo_name
+        algo = algo_name[:-5] if busy else algo_name[:-4] if inc else \
+            algo_name[:-5] if host else algo_name
         push = algo == "ordered_push"
         if push:
             algo = "ordered"
@@ -98,11 +105,20 @@ def main():
                 res = pipe.finish()
             elif inc:
                 views = split(flat, specs)
+                if busy:
+                    hog = torch.cuda.Stream(dev)
+                    hog.wait_stream(torch.cuda.current_stream(dev))
+                    a = torch.randn(4096, 4096, device=dev, dtype=torch.bfloat16)
+                    with torch.cuda.stream(hog):
+                        for _ in range(8 + 8 * rank):
+                            a = (a @ a).clamp_(-1, 1)
                 pipe.begin(step)
                 for b in reversed(range(len(pipe.buckets))):
                     pipe.submit(b, [views[i] for i in pipe.buckets[b].params])
                 pipe.end()
                 res = pipe.finish()
+                if busy:
+                    torch.cuda.current_stream(dev).wait_stream(hog)
             else:
                 res = pipe.step(flat, step)
             reduced = [pipe.bucket_payload(b).cpu().numpy() for b in range(len(pipe.buckets))]

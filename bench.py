@@ -59,6 +59,9 @@ def parse():
                     help="forced overflow: rank 0's gradient carries +Inf, every step takes "
                          "the skip path (fixed loss-scale policy so the scale stays put)")
     ap.add_argument("--no-soak", action="store_true", help="skip the clock soak (profiling runs)")
+    ap.add_argument("--loss-scale", type=float, default=1024.0,
+                    help="initial loss scale (a non-power-of-two value takes the IEEE-division "
+                         "kernels)")
     ap.add_argument("--no-grad-norm", action="store_true",
                     help="A/B only: do not compute the grad-norm metric (experiment.py:408-411)")
     return ap.parse_args()
@@ -143,7 +146,8 @@ def workload_config(args, world: int) -> dict:
     algo = args.algorithm if world > 1 else "none"
     k = args.group_size if algo in ("hierarchical", "sharded") and world % args.group_size == 0 \
         else 1
-    return {"workload": f"{args.model} fused MP-LARS step, fp16 wire, p={world}",
+    extra = {} if getattr(args, "loss_scale", 1024.0) == 1024.0 else {"loss_scale": args.loss_scale}
+    return {**extra, "workload": f"{args.model} fused MP-LARS step, fp16 wire, p={world}",
             "model": args.model, "params": sum(sizes), "tensors": len(specs),
             "theta": args.theta, "buckets": nb, "algorithm": algo,
             "topology": f"Topology({world},{k})" if world > 1 else "1 GPU",
@@ -307,7 +311,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
                                sharded_update=args.algorithm.startswith("zero") and world > 1,
                                fused_collective=args.algorithm == "zero",
                                init_master=sh.synth_master(specs, seed=0),
-                               loss_scale=gs.LossScale(1024.0, policy="fixed" if args.overflow
+                               loss_scale=gs.LossScale(args.loss_scale, policy="fixed" if args.overflow
                                                        else "dynamic"), device=dev,
                                grad_norm=not args.no_grad_norm)
     wire_np = sh.synth_wire_grads(specs, rank=rank, seed=0)

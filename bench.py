@@ -550,7 +550,8 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
     for k in (4, 2):
         if world % k == 0 and k < world:
             variants += [(f"hierarchical_{world // k}x{k}", k), (f"sharded_{world // k}x{k}", k),
-                         (f"ordered_hier_{world // k}x{k}", k)]
+                         (f"ordered_hier_{world // k}x{k}", k),
+                         (f"ordered_hier_push_{world // k}x{k}", k)]
     comms = {}
     s0 = torch.cuda.current_stream(dev)
     variants += [("ordered", 1), ("ordered_push", 1)]
@@ -568,7 +569,7 @@ def allreduce_busbw(pipe, world, local, dev) -> dict:
             ow = ow or OrderedWire(comm, pipe.total, dev)
             half = [0]
 
-            def run_ordered(_t=None, _push=name == "ordered_push", _k=hier_k):
+            def run_ordered(_t=None, _push="push" in name, _k=hier_k):
                 from paper_1807_11205_b200._peer import launch
                 ow.push = _push
                 if _k:  # the bit-exact two-level kernel over Topology(p, k)

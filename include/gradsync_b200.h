@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 2
+#define GS_ABI_VERSION 3
 
 #define GS_OK 0
 #define GS_EINVAL (-1)
@@ -265,11 +265,13 @@ int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const 
  * copies), an inter-group fold of each sub-slice over the p/k same-offset
  * group partials, then the all-gather.  For power-of-two k the reference's
  * rank tree factors exactly this way, so the result equals
- * gs_ordered_allreduce_f16's bit for bit.  Signal areas need >= 3 * nblocks
- * * p words.  k in {2, 4, 8}, p <= 8. */
+ * gs_ordered_allreduce_f16's bit for bit.  push != 0: the rank that folds a
+ * final sub-slice stores it into every rank and one exit barrier replaces
+ * the gather (same bits).  Signal areas need >= 3 * nblocks * p words.
+ * k in {2, 4, 8}, p <= 8. */
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
                           const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
-                          uint32_t epoch, int nblocks, void* stream);
+                          uint32_t epoch, int nblocks, int push, void* stream);
 
 /* Reduce-scatter half of the above with explicit slices: rank r folds
  * elements [bounds[r], bounds[r+1]) (device int64 array of p + 1 offsets)

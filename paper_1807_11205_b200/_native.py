@@ -116,7 +116,7 @@ SIGNATURES = {
     "gs_ordered_allreduce_f32": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int64,
                                          c_int64, c_uint32, c_int, c_int, c_void_p]),
     "gs_hier_allreduce_f16": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int64,
-                                      c_int64, c_uint32, c_int, c_void_p]),
+                                      c_int64, c_uint32, c_int, c_int, c_void_p]),
     "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p,
                                               c_void_p, c_uint32, c_int, c_void_p]),
     "gs_ordered_allgather": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
@@ -135,7 +135,7 @@ SIGNATURES = {
                              c_uint32, c_int, c_void_p]),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lib = None
 _lock = threading.Lock()

@@ -47,9 +47,9 @@ __device__ __forceinline__ void subrange(int64_t n, int p, int r, int nb, int b,
 // PUSH: also store every folded vector into every peer's buffer at the same
 // offset (only the slice's owner ever reads or writes those positions, and
 // each thread reads its element from all peers before it overwrites it)
-template <int P, bool PUSH = false>
-__device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint16_t* mine, int64_t lo,
-                                           int64_t hi, uint32_t& bad) {
+template <int P, int Q, bool PUSH>
+__device__ __forceinline__ void fold_range_to(const uint16_t* const (&src)[P], uint16_t* const (&dst)[Q],
+                                              uint16_t* mine, int64_t lo, int64_t hi, uint32_t& bad) {
   bool vec = gs::is_aligned16(mine + lo);
 #pragma unroll
   for (int q = 0; q < P; ++q) vec = vec && gs::is_aligned16(src[q] + lo);
@@ -87,8 +87,7 @@ __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint
       const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
       if (PUSH) {
 #pragma unroll
-        for (int q = 0; q < P; ++q)
-          reinterpret_cast<uint4*>(const_cast<uint16_t*>(src[q]) + lo)[i] = ov;
+        for (int q = 0; q < Q; ++q) reinterpret_cast<uint4*>(dst[q] + lo)[i] = ov;
       } else {
         reinterpret_cast<uint4*>(mine + lo)[i] = ov;
       }
@@ -102,11 +101,22 @@ __device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint
     bad |= (o & 0x7C00u) == 0x7C00u;
     if (PUSH) {
 #pragma unroll
-      for (int q = 0; q < P; ++q) const_cast<uint16_t*>(src[q])[i] = o;
+      for (int q = 0; q < Q; ++q) dst[q][i] = o;
     } else {
       mine[i] = o;
     }
   }
+}
+
+// the folded values stored into `mine` (pull) or into every source buffer
+// (PUSH: the slice's final value lands in every peer as it is produced)
+template <int P, bool PUSH = false>
+__device__ __forceinline__ void fold_range(const uint16_t* const (&src)[P], uint16_t* mine, int64_t lo,
+                                           int64_t hi, uint32_t& bad) {
+  uint16_t* dst[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) dst[q] = const_cast<uint16_t*>(src[q]);
+  fold_range_to<P, P, PUSH>(src, dst, mine, lo, hi, bad);
 }
 
 // fp32 form (fold_ascending, collectives.py:261-270): acc = b0; acc += b1;
@@ -337,7 +347,7 @@ ordered_allgather_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, int p,
 // what CTA lb of its peers wrote and the per-CTA barriers suffice.  Same
 // inbound volume as the flat ring, 2(p-1)/p * S; no exit barrier (the wire
 // is double-buffered across calls, as for the flat kernel).
-template <int K, int G>
+template <int K, int G, bool PUSH>
 __global__ void __launch_bounds__(kThreads)
 hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
                       const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ sig,
@@ -355,10 +365,21 @@ hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
 #pragma unroll
     for (int m = 0; m < K; ++m) grp[m] = reinterpret_cast<const uint16_t*>(bufs[g * K + m]) + offset;
 #pragma unroll 1
-    for (int gp = 0; gp < G; ++gp) {
+    if (PUSH && G == 1) {
+      // one group: the group fold is final -- store it into every member
+      uint16_t* all[K];
+#pragma unroll
+      for (int m = 0; m < K; ++m) all[m] = const_cast<uint16_t*>(grp[m]);
       int64_t lo, hi;
-      subrange(n, P, j * G + gp, nb, c.lb, lo, hi);
-      fold_range<K>(grp, mine, lo, hi, bad);
+      subrange(n, P, j, nb, c.lb, lo, hi);
+      fold_range_to<K, K, true>(grp, all, mine, lo, hi, bad);
+    } else {
+#pragma unroll 1
+      for (int gp = 0; gp < G; ++gp) {
+        int64_t lo, hi;
+        subrange(n, P, j * G + gp, nb, c.lb, lo, hi);
+        fold_range<K>(grp, mine, lo, hi, bad);
+      }
     }
   }
   if (G > 1) {
@@ -369,8 +390,16 @@ hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
     for (int q = 0; q < G; ++q) crs[q] = reinterpret_cast<const uint16_t*>(bufs[q * K + j]) + offset;
     int64_t lo, hi;
     subrange(n, P, j * G + g, nb, c.lb, lo, hi);
-    fold_range<G>(crs, mine, lo, hi, bad);
-  } else {
+    if (PUSH) {
+      // the final sub-slice goes straight into every rank (no gather phase)
+      uint16_t* all[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) all[q] = reinterpret_cast<uint16_t*>(bufs[q]) + offset;
+      fold_range_to<G, P, true>(crs, all, mine, lo, hi, bad);
+    } else {
+      fold_range<G>(crs, mine, lo, hi, bad);
+    }
+  } else if (!PUSH) {
     // one group: the group partial of sub-slice j is the final value
     int64_t lo, hi;
     subrange(n, P, j, nb, c.lb, lo, hi);
@@ -379,6 +408,12 @@ hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
   }
   bad = __reduce_or_sync(0xFFFFFFFFu, bad);
   if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+  if (PUSH) {
+    // every final sub-slice was stored into every rank: one exit barrier
+    __threadfence_system();
+    peer_barrier(sig, c, P, 2, epoch, kSiteHierarchical);
+    return;
+  }
   peer_barrier(sig, c, P, 2, epoch, kSiteHierarchical);  // D
 #pragma unroll 1
   for (int d = 1; d < P; ++d) {
@@ -512,7 +547,7 @@ int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const 
 
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
                           const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
-                          uint32_t epoch, int nblocks, void* stream) {
+                          uint32_t epoch, int nblocks, int push, void* stream) {
   GS_PEER_ARGS("gs_hier_allreduce_f16");
   GS_REQUIRE(k == 2 || k == 4 || k == 8, "gs_hier_allreduce_f16: group size k must be 2, 4 or 8 "
              "(the reference tree factors over groups only for power-of-two k; got %d)", k);
@@ -524,7 +559,7 @@ int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
   bool done = false;
 #define GS_HAR(K, G)                                                                             \
   if (!done && k == K && p == K * G) {                                                           \
-    auto kern = hier_allreduce_kernel<K, G>;                                                     \
+    auto kern = push ? hier_allreduce_kernel<K, G, true> : hier_allreduce_kernel<K, G, false>;    \
     const int nb = peer_grid((const void*)kern, kThreads, 0, nblocks, nranks);                   \
     kern<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, sig, offset, n, epoch);               \
     done = true;                                                                                 \

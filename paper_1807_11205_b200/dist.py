@@ -265,7 +265,8 @@ class OrderedWire:
 
         return PeerOp("gs_hier_allreduce_f16", self.ctx,
                       (self.p, k, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
-                       slot + 1, self.grid_for(n), stream_h), device=self.device)
+                       slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
+                      device=self.device)
 
     def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
         from ._peer import launch

@@ -51,12 +51,12 @@ def main():
     results = {}
     algos = os.environ.get("MGPU_ALGOS", "zero,zero_unfused,ordered,ordered_push,ordered_hier,ring,"
                            "hierarchical,sharded,zero_inc,ordered_inc,ring_inc,zero_host,"
-                           "ordered_host,zero_busy,ordered_busy").split(",")
+                           "ordered_host,zero_busy,ordered_busy,ordered_hier_push").split(",")
     for algo_name, k in (("zero", 1), ("zero_unfused", 1), ("ordered", 1), ("ordered_push", 1),
                          ("ordered_hier", 2), ("ring", 1),
                          ("hierarchical", 2), ("sharded", 2), ("zero_inc", 1), ("ordered_inc", 1),
                          ("ring_inc", 1), ("zero_host", 1), ("ordered_host", 1),
-                         ("zero_busy", 1), ("ordered_busy", 1)):
+                         ("zero_busy", 1), ("ordered_busy", 1), ("ordered_hier_push", 2)):
         if algo_name not in algos:
             continue
         # *_inc: the same step driven through the incremental API the
@@ -73,9 +73,9 @@ def main():
         host = algo_name.endswith("_host")
         algo = algo_name[:-5] if busy else algo_name[:-4] if inc else \
             algo_name[:-5] if host else algo_name
-        push = algo == "ordered_push"
+        push = algo in ("ordered_push", "ordered_hier_push")
         if push:
-            algo = "ordered"
+            algo = "ordered" if algo == "ordered_push" else "ordered_hier"
         if world % k or (algo != "ring" and world == 1):
             continue
         comm = Communicator(gs.Topology(world, k))

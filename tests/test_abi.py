@@ -37,7 +37,7 @@ def test_every_declared_symbol_is_exported_and_bound():
 
 def test_abi_version_and_errors_without_gpu():
     lib = _native.load()
-    assert lib.gs_abi_version() == _native.ABI_VERSION == 2
+    assert lib.gs_abi_version() == _native.ABI_VERSION == 3
     # argument validation happens before any launch
     assert lib.gs_f32_to_f16(None, None, -1, 1.0, None, None) == -1
     assert b"negative" in lib.gs_last_error()

@@ -73,14 +73,16 @@ def test_ordered_allreduce_bit_exact(p, push):
             assert w.status_word() == 0
 
 
+@pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("p,k", [(2, 2), (4, 2), (4, 4), (6, 2), (8, 2), (8, 4), (8, 8)])
-def test_hierarchical_allreduce_bit_exact(p, k):
+def test_hierarchical_allreduce_bit_exact(p, k, push):
     """gs_hier_allreduce_f16 over Topology(p, k): intra-group reduce-scatter,
-    inter-group fold of the group partials, all-gather — the reference's
-    rank tree (fold_f16_tree) bit for bit."""
+    inter-group fold of the group partials, all-gather (or, push form, the
+    final sub-slices stored into every rank) — the reference's rank tree
+    (fold_f16_tree) bit for bit."""
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
-    wires = [c.make_ordered_wire(1 << 16, d) for c in world.comms]
+    wires = [c.make_ordered_wire(1 << 16, d, push=push) for c in world.comms]
     rng = np.random.default_rng(300 + 10 * p + k)
     sh_ = torch.cuda.current_stream().cuda_stream
     for slot, (off, n) in enumerate([(0, 50001), (24, 7), (1000, 8 * p * 16 + 3)]):

@@ -43,7 +43,8 @@ def main() -> None:
     ap.add_argument("--min-log2", type=int, default=10)
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--variants",
-                    default="ring,hierarchical,sharded,ordered,ordered_push,ordered_hier")
+                    default="ring,hierarchical,sharded,ordered,ordered_push,ordered_hier,"
+                            "ordered_hier_push")
     ap.add_argument("--out", default=None, help="also write the lines to this file (rank 0)")
     args = ap.parse_args()
 
@@ -75,10 +76,11 @@ def main() -> None:
         variants.append(("ordered", 1))
     if "ordered_push" in want:
         variants.append(("ordered_push", 1))
-    if "ordered_hier" in want:
-        for k in (4, 2):
-            if 1 < k < world and world % k == 0:
-                variants.append((f"ordered_hier_{world // k}x{k}", k))
+    for form in ("ordered_hier", "ordered_hier_push"):
+        if form in want:
+            for k in (4, 2):
+                if 1 < k < world and world % k == 0:
+                    variants.append((f"{form}_{world // k}x{k}", k))
     comms = {k: Communicator(gs.Topology(world, k)) for k in sorted({k for _, k in variants})}
     # bookkeeping reductions on CPU (gloo): NCCL_ALGO=NVLS runs have no fp64/int path
     host = dist.new_group(backend="gloo")
@@ -112,7 +114,7 @@ def main() -> None:
                     if rank == 0:
                         h[:1].view(torch.int16).fill_(0x7C00)
 
-                def run(_push=name == "ordered_push",
+                def run(_push="push" in name,
                         _k=k if name.startswith("ordered_hier") else 0):
                     ow.push = _push
                     sh = int(s0.cuda_stream)

@@ -34,7 +34,7 @@ METRIC = "fused MP-LARS step time (ms) + allreduce bus GB/s, ResNet-50 grads, 1/
 PIECE = "pass2"   # dominant kernel for the roofline line
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -64,7 +64,7 @@ def parse():
                          "kernels)")
     ap.add_argument("--no-grad-norm", action="store_true",
                     help="A/B only: do not compute the grad-norm metric (experiment.py:408-411)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def load_peaks():

@@ -417,6 +417,18 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
             phase_ms.setdefault(x, []).append(ev[x].elapsed_time(ev[y]))
 
     mean_ms = statistics.mean(step_ms)
+    # every rank's mean phase times (rank skew shows up as a fence / wait
+    # phase that is long on the early ranks only)
+    phase_spread = None
+    if world > 1:
+        names = list(phase_ms)
+        loc = torch.tensor([statistics.mean(phase_ms[k]) for k in names], dtype=torch.float64,
+                           device=dev)
+        lo, hi = loc.clone(), loc.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        phase_spread = {k: [round(float(a), 4), round(float(b), 4)]
+                        for k, a, b in zip(names, lo.tolist(), hi.tolist())}
     # the dominant kernel: pass 2 (gs_pass2_push in the fused sharded step,
     # over this rank's owned elements only); its achieved bandwidth is taken
     # per rank and the slowest rank reported
@@ -523,6 +535,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "l2": "flushed before every step (256 MiB write, then read: no step data resident, "
               "L2 clean)",
         "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phase_ms.items() if v},
+        "phases_ms_min_max_over_ranks": phase_spread,
         "update_roofline_ms": round(update_bytes / (peak * 1e9) * 1e3, 4),
         "roofline": roofline,
         "clocks": clk,

@@ -269,6 +269,18 @@ int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const 
  * final sub-slice stores it into every rank and one exit barrier replaces
  * the gather (same bits).  Signal areas need >= 3 * nblocks * p words.
  * k in {2, 4, 8}, p <= 8. */
+/* One-shot form of gs_ordered_allreduce_f16 for small buckets (same bits):
+ * every rank stores its raw bucket into slot [parity][rank] (cap elements
+ * each) of every rank's `inbox` (device table of p inbox base addresses),
+ * one barrier, then folds its own p slots in the reference's tree order into
+ * its buffer.  One barrier instead of two; (p-1) x S bytes out per rank.
+ * Consecutive one-shot calls on the same inboxes must alternate parity.
+ * n <= cap. */
+int gs_oneshot_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* inbox, const uint64_t* sig, int64_t offset, int64_t n,
+                             int64_t cap, uint32_t epoch, int nblocks, uint32_t parity,
+                             void* stream);
+
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
                           const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
                           uint32_t epoch, int nblocks, int push, void* stream);

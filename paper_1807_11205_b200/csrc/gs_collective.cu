@@ -425,6 +425,59 @@ hier_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
   }
 }
 
+// One-shot form for small buckets (one barrier instead of two): every rank
+// pushes its raw binary16 piece into slot [parity][rank] of every peer's
+// inbox, fences and signals; after the barrier it folds the p slots of its
+// OWN inbox (local memory) in the reference's tree order into its wire.
+// (p-1) x S NVLink bytes out per rank instead of 2(p-1)/p x S, so it pays
+// only while latency dominates.  CTA lb pushes and folds piece lb, so the
+// per-CTA barrier suffices.  Slot reuse: consecutive one-shot calls
+// alternate `parity`; a peer can push call c+2 only after this rank arrived
+// at call c+1's barrier, i.e. after it folded call c.
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+oneshot_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                         const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ inbox,
+                         const uint64_t* __restrict__ sig, int64_t offset, int64_t n,
+                         int64_t cap, uint32_t epoch, uint32_t parity) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+  int64_t lo, hi;
+  split_range(0, n, nb, c.lb, 8, lo, hi);
+  const size_t slot = ((size_t)parity * P + rank) * (size_t)cap;
+  {  // push my raw piece into every rank's inbox (own included)
+    uint8_t* dst[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) dst[q] = reinterpret_cast<uint8_t*>(inbox[q]) + 2 * slot;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(mine);
+    const int64_t b0 = 2 * lo, b1 = 2 * hi;
+    const bool vec = gs::is_aligned16(src + b0) && gs::is_aligned16(dst[0] + b0);
+    const int64_t nv = vec ? (b1 - b0) / 16 : 0;
+    for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+      const uint4 v = __ldcv(reinterpret_cast<const uint4*>(src + b0) + i);
+#pragma unroll
+      for (int q = 0; q < P; ++q) reinterpret_cast<uint4*>(dst[q] + b0)[i] = v;
+    }
+    for (int64_t i = b0 + 16 * nv + threadIdx.x; i < b1; i += kThreads) {
+      const uint8_t v = src[i];
+#pragma unroll
+      for (int q = 0; q < P; ++q) dst[q][i] = v;
+    }
+  }
+  __threadfence_system();
+  peer_barrier(sig, c, P, 0, epoch, kSiteOrderedAllreduce);
+  const uint16_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+    src[q] = reinterpret_cast<const uint16_t*>(inbox[rank]) + ((size_t)parity * P + q) * cap;
+  uint32_t bad = 0;
+  fold_range<P>(src, mine, lo, hi, bad);
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+}
+
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
 
 }  // namespace
@@ -543,6 +596,38 @@ int gs_ordered_allreduce_f32(const gs_rank_ctx* ranks, int nranks, int p, const 
   }
 #undef GS_OAR32
   return gs_check_launch("gs_ordered_allreduce_f32");
+}
+
+int gs_oneshot_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                             const uint64_t* inbox, const uint64_t* sig, int64_t offset, int64_t n,
+                             int64_t cap, uint32_t epoch, int nblocks, uint32_t parity,
+                             void* stream) {
+  GS_PEER_ARGS("gs_oneshot_allreduce_f16");
+  GS_REQUIRE(n >= 0 && offset >= 0 && n <= cap && parity <= 1,
+             "gs_oneshot_allreduce_f16: need 0 <= n <= cap (n=%lld, cap=%lld) and parity 0/1",
+             (long long)n, (long long)cap);
+  if (p == 1 || n == 0) return GS_OK;
+  GS_REQUIRE(ranks && bufs && inbox && sig, "gs_oneshot_allreduce_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_OS(P)                                                                                 \
+  case P: {                                                                                      \
+    auto k = oneshot_allreduce_kernel<P>;                                                        \
+    const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                      \
+    k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, inbox, sig, offset, n, cap, epoch,       \
+                                       parity);                                                  \
+    break;                                                                                       \
+  }
+  switch (p) {
+    GS_OS(2)
+    GS_OS(3)
+    GS_OS(4)
+    GS_OS(5)
+    GS_OS(6)
+    GS_OS(7)
+    GS_OS(8)
+  }
+#undef GS_OS
+  return gs_check_launch("gs_oneshot_allreduce_f16");
 }
 
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,

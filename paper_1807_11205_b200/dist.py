@@ -206,10 +206,30 @@ class OrderedWire:
         self._setup(bases, device, push, comm.timeout_s)
         dist.barrier()
 
+    #: buckets of at most this many binary16 elements take the one-shot
+    #: kernel (gs_oneshot_allreduce_f16: one barrier, (p-1) x S bytes out).
+    #: Measured at p = 4 (profiles/r02/y_n4): 14.5-16.0 µs up to 16 KB vs
+    #: 20-21.5 (pull) / 16.7-17.3 (push) and NCCL's 15.3-16.2; from 32 KB on
+    #: the (p-1) x S bytes make it lose to the push form.
+    ONESHOT_MAX_ELEMS = 8192
+
+    @staticmethod
+    def oneshot_cap(total: int, itemsize: int) -> int:
+        """Elements per inbox slot (0: no one-shot form, e.g. the fp32 wire)."""
+        if itemsize != 2:
+            return 0
+        return (min(total, OrderedWire.ONESHOT_MAX_ELEMS) + 255) // 256 * 256
+
+    @staticmethod
+    def sig_bytes(nblocks: int, p: int) -> int:
+        return (4 * 3 * nblocks * p + 512 + 255) // 256 * 256
+
     @staticmethod
     def nbytes_for(total: int, itemsize: int, nblocks: int, p: int) -> int:
-        """[wire A | wire B | signal area (3 barrier phases) | status]"""
-        return 2 * total * itemsize + 4 * 3 * nblocks * p + 512 + 128
+        """[wire A | wire B | signal area (3 barrier phases) | inbox (2 parities
+        x p slots of oneshot_cap elements) | status]"""
+        cap = OrderedWire.oneshot_cap(total, itemsize)
+        return 2 * total * itemsize + OrderedWire.sig_bytes(nblocks, p) + 2 * p * cap * 2 + 128
 
     def _setup(self, bases, device, push: bool, timeout_s: float) -> None:
         """Tables and this rank's context from every rank's base address
@@ -226,6 +246,12 @@ class OrderedWire:
                                     device) for h in range(2)]
         self.sig_dev = dev.upload(np.array([b + 2 * z * t for b in bases], dtype=np.uint64),
                                   device)
+        # one-shot inboxes (small buckets): after the signal area
+        self.cap = self.oneshot_cap(t, z)
+        ib = 2 * z * t + self.sig_bytes(self.nblocks, self.p)
+        self.inbox_dev = dev.upload(np.array([b + ib for b in bases], dtype=np.uint64), device) \
+            if self.cap else None
+        self._oneshot_calls = 0
         # device-resident epoch base: every call of a step uses base + slot,
         # and advance() bumps the base once per step on the stream
         self.epoch_base = torch.zeros(1, dtype=torch.int32, device=device)
@@ -245,12 +271,24 @@ class OrderedWire:
     def grid_for(self, n: int) -> int:
         return max(1, min(self.nblocks, -(-int(n) // self.MIN_ELEMS_PER_CTA)))
 
-    def allreduce_op(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0):
+    def allreduce_op(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0,
+                     oneshot: bool | None = None):
         """The bucket all-reduce as a peer op; `slot` (0-based within the
-        step, < per_step) makes the epoch unique among the step's calls."""
+        step, < per_step) makes the epoch unique among the step's calls.
+        oneshot: None = the one-shot kernel for buckets up to
+        ONESHOT_MAX_ELEMS (bit-identical either way)."""
         from . import _device as dev
         from ._peer import PeerOp
 
+        if oneshot is None:
+            oneshot = 0 < n <= self.cap
+        if oneshot and self.cap and 0 < n <= self.cap:
+            parity = self._oneshot_calls & 1
+            self._oneshot_calls += 1
+            return PeerOp("gs_oneshot_allreduce_f16", self.ctx,
+                          (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.inbox_dev),
+                           dev.ptr(self.sig_dev), offset, n, self.cap, slot + 1, self.grid_for(n),
+                           parity, stream_h), device=self.device)
         return PeerOp("gs_ordered_allreduce_f16" if self.itemsize == 2 else
                       "gs_ordered_allreduce_f32", self.ctx,
                       (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
@@ -268,9 +306,10 @@ class OrderedWire:
                        slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
                       device=self.device)
 
-    def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0) -> None:
+    def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0,
+                  oneshot: bool | None = None) -> None:
         from ._peer import launch
-        launch([self.allreduce_op(half, offset, n, stream_h, slot)])
+        launch([self.allreduce_op(half, offset, n, stream_h, slot, oneshot)])
 
     def advance(self, per_step: int, stream_h: int) -> None:
         from . import _device as dev

@@ -98,6 +98,8 @@ class LocalOrderedWire:
     from .dist import OrderedWire as _OW
     MIN_ELEMS_PER_CTA = _OW.MIN_ELEMS_PER_CTA
     nbytes_for = _OW.nbytes_for
+    oneshot_cap = staticmethod(_OW.oneshot_cap)
+    sig_bytes = staticmethod(_OW.sig_bytes)
     _setup = _OW._setup
     grid_for = _OW.grid_for
     allreduce_op = _OW.allreduce_op
@@ -162,6 +164,7 @@ class LocalWorld:
             # rank 0's, so all must be the same tensors
             for w in wires[1:]:
                 w.bufs_dev, w.sig_dev = wires[0].bufs_dev, wires[0].sig_dev
+                w.inbox_dev = wires[0].inbox_dev
             self._wires = (key, wires)
         w = self._wires[1][rank]
         self._wires[1][rank] = None

@@ -49,22 +49,28 @@ def random_f16(rng, n, special=True):
 
 # ---------------------------------------------------------------- collectives
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
-@pytest.mark.parametrize("push", [0, 1])
-def test_ordered_allreduce_bit_exact(p, push):
-    """gs_ordered_allreduce_f16 (pull and push forms) == fold_f16_tree on
-    every rank, incl. ragged lengths, an unaligned bucket offset, Inf/NaN
-    and pairwise overflow."""
+@pytest.mark.parametrize("form", ["pull", "push", "oneshot"])
+def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
+    """gs_ordered_allreduce_f16 (pull and push forms) and
+    gs_oneshot_allreduce_f16 == fold_f16_tree on every rank, incl. ragged
+    lengths, an unaligned bucket offset, Inf/NaN and pairwise overflow; the
+    one-shot calls alternate their inbox parity."""
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, 1), d, peer_ctas=8, timeout_s=20.0)
     total = 1 << 16
-    wires = [c.make_ordered_wire(total, d, push=bool(push)) for c in world.comms]
+    push = form == "push"
+    if form == "oneshot":  # inboxes large enough for every bucket below
+        from paper_1807_11205_b200.dist import OrderedWire
+        monkeypatch.setattr(OrderedWire, "ONESHOT_MAX_ELEMS", total)
+    wires = [c.make_ordered_wire(total, d, push=push) for c in world.comms]
     rng = np.random.default_rng(100 + p)
     sh_ = torch.cuda.current_stream().cuda_stream
     for slot, (off, n) in enumerate([(0, 40000), (8, 1), (1003, 12345), (4096, 0)]):
         data = [random_f16(rng, n) for _ in range(p)]
         for w, x in zip(wires, data):
             w.halves[0][off:off + n].copy_(torch.from_numpy(x))
-        launch([w.allreduce_op(0, off, n, sh_, slot=slot) for w in wires])
+        launch([w.allreduce_op(0, off, n, sh_, slot=slot, oneshot=form == "oneshot")
+                for w in wires])
         torch.cuda.synchronize()
         want = rp.fold_f16_tree([x for x in data]) if n else np.zeros(0, np.uint16)
         for r, w in enumerate(wires):

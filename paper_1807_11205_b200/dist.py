@@ -208,10 +208,10 @@ class OrderedWire:
 
     #: buckets of at most this many binary16 elements take the one-shot
     #: kernel (gs_oneshot_allreduce_f16: one barrier, (p-1) x S bytes out).
-    #: Measured at p = 4 (profiles/r02/y_n4): 14.5-16.0 µs up to 16 KB vs
-    #: 20-21.5 (pull) / 16.7-17.3 (push) and NCCL's 15.3-16.2; from 32 KB on
-    #: the (p-1) x S bytes make it lose to the push form.
-    ONESHOT_MAX_ELEMS = 8192
+    #: Measured at p = 4 (profiles/r02/y_n4, aa_n4): 13.1-14.3 µs up to 8 KB
+    #: vs 19-20 (pull) / 15.3-16.1 (push) and NCCL's 14.6-15.0; from 16 KB
+    #: on the (p-1) x S bytes make it tie or lose to the push form.
+    ONESHOT_MAX_ELEMS = 4096
 
     @staticmethod
     def oneshot_cap(total: int, itemsize: int) -> int:

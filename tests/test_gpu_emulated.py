@@ -52,9 +52,9 @@ def random_f16(rng, n, special=True):
 @pytest.mark.parametrize("form", ["pull", "push", "oneshot"])
 def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
     """gs_ordered_allreduce_f16 (pull and push forms) and
-    gs_oneshot_allreduce_f16 == fold_f16_tree on every rank, incl. ragged
-    lengths, an unaligned bucket offset, Inf/NaN and pairwise overflow; the
-    one-shot calls alternate their inbox parity."""
+    the small-bucket gs_oneshot_allreduce_f16 == fold_f16_tree on every
+    rank, incl. ragged lengths, an unaligned bucket offset, Inf/NaN and
+    pairwise overflow; the one-shot calls alternate their inbox parity."""
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, 1), d, peer_ctas=8, timeout_s=20.0)
     total = 1 << 16

@@ -34,7 +34,7 @@ import torch  # noqa: E402
 import paper_1807_11205_b200 as gs  # noqa: E402
 
 OURS = ("lars_pass1", "lars_trust", "lars_pass2", "batched_copy", "ordered_allreduce",
-        "rs_pass1", "pass2_push", "fold_")
+        "oneshot_allreduce", "rs_pass1", "pass2_push", "peer_fence", "fold_")
 
 
 class Net(torch.nn.Module):
@@ -59,14 +59,27 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--res", type=int, default=64)
     ap.add_argument("--width", type=int, default=256)
+    ap.add_argument("--algorithm", default="zero", choices=["zero", "ordered"],
+                    help="multi-GPU (torchrun): the sharded fused step or the ordered all-reduce")
     args = ap.parse_args()
     torch.manual_seed(0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = 0
+    kw = {}
+    if world > 1:
+        from paper_1807_11205_b200.dist import Communicator, init_from_env
+        rank, world, local = init_from_env("nccl")
+        torch.cuda.set_device(local)
+        comm = Communicator(gs.Topology(world, 1))
+        kw = dict(comm=comm, sharded_update=args.algorithm == "zero",
+                  flat_variant="ordered", eta_bytes=0)
+        args.out = f"{args.out}_rank{rank}"
     # GPU-bound backward (each conv's backward takes longer than the host
     # needs to launch it), so a side-stream kernel CAN run beside it
     net = Net(width=args.width).cuda()
     cfg = gs.LarsConfig(gs.Schedule(0.1), eta=0.001, weight_decay=5e-4, momentum=0.9)
     drv = gs.BackwardOverlap.for_module(net, cfg, threshold_bytes=args.theta,
-                                        loss_scale=gs.LossScale(1024.0))
+                                        loss_scale=gs.LossScale(1024.0), **kw)
     x = torch.randn(args.batch, 3, args.res, args.res, device="cuda").half()
     y = torch.randint(0, 100, (args.batch,), device="cuda")
 
@@ -113,7 +126,8 @@ def main():
     side_under = sum(overlap(e["ts"], e["ts"] + e["dur"]) for e in side)
     # per step: the compute stream's last non-optimizer kernel (end of
     # backward) to the end of pass 2 = what the optimizer step adds
-    p2 = sorted(e["ts"] + e["dur"] for e in ours if "lars_pass2" in e["name"])
+    p2 = sorted(e["ts"] + e["dur"] for e in ours
+                if "lars_pass2" in e["name"] or "pass2_push" in e["name"])
     tails = []
     for end in p2:
         before = [t for s_, t in comp if t <= end]
@@ -129,11 +143,17 @@ def main():
         "side_stream_us_under_backward": round(side_under, 1),
         "side_overlap_fraction": round(side_under / side_time, 3) if side_time else None,
         "exposed_tail_us_per_step": [round(t, 1) for t in tails],
-        "config": {"batch": args.batch, "res": args.res, "width": args.width, "depth": 10},
+        "config": {"batch": args.batch, "res": args.res, "width": args.width, "depth": 10,
+                   "world": world, "rank": rank,
+                   "algorithm": args.algorithm if world > 1 else "none"},
         "nvtx_ranges": sorted({e["name"] for e in ranges}),
         "steps_profiled": 3,
     }
     print(json.dumps(summary, indent=1))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -297,9 +297,15 @@ class OrderedWire:
 
     def hier_op(self, half: int, offset: int, n: int, k: int, stream_h: int, slot: int = 0):
         """The bucket all-reduce over Topology(p, k)'s two levels
-        (gs_hier_allreduce_f16; bit-identical to allreduce_op)."""
+        (gs_hier_allreduce_f16; bit-identical to allreduce_op).  Buckets the
+        one-shot kernel takes (n <= ONESHOT_MAX_ELEMS) use it here too: the
+        reference's rank tree factors over the groups, so the flat one-shot
+        fold gives the hierarchy's bits with one barrier instead of three."""
         from . import _device as dev
         from ._peer import PeerOp
+
+        if 0 < n <= self.cap:
+            return self.allreduce_op(half, offset, n, stream_h, slot, oneshot=True)
 
         return PeerOp("gs_hier_allreduce_f16", self.ctx,
                       (self.p, k, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,

@@ -81,11 +81,15 @@ def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
 
 @pytest.mark.parametrize("push", [False, True])
 @pytest.mark.parametrize("p,k", [(2, 2), (4, 2), (4, 4), (6, 2), (8, 2), (8, 4), (8, 8)])
-def test_hierarchical_allreduce_bit_exact(p, k, push):
+def test_hierarchical_allreduce_bit_exact(p, k, push, monkeypatch):
     """gs_hier_allreduce_f16 over Topology(p, k): intra-group reduce-scatter,
     inter-group fold of the group partials, all-gather (or, push form, the
     final sub-slices stored into every rank) — the reference's rank tree
     (fold_f16_tree) bit for bit."""
+    from paper_1807_11205_b200.dist import OrderedWire
+    # no one-shot inbox: every bucket below runs the two-level kernel (small
+    # buckets take the one-shot kernel by default: test_hier_op_small_buckets)
+    monkeypatch.setattr(OrderedWire, "ONESHOT_MAX_ELEMS", 0)
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
     wires = [c.make_ordered_wire(1 << 16, d, push=push) for c in world.comms]
@@ -101,6 +105,30 @@ def test_hierarchical_allreduce_bit_exact(p, k, push):
         for r, w in enumerate(wires):
             assert np.array_equal(w.halves[0][off:off + n].cpu().numpy(), want), \
                 f"Topology({p},{k}) rank {r} bucket {slot}"
+            assert w.status_word() == 0
+
+
+@pytest.mark.parametrize("p,k", [(4, 2), (8, 4)])
+def test_hier_op_small_buckets(p, k):
+    """hier_op sends buckets up to ONESHOT_MAX_ELEMS to the one-shot kernel
+    (the reference's tree factors over the groups, so the bits are the
+    hierarchy's); alternating parities over consecutive calls."""
+    d = dev.require_cuda()
+    world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
+    wires = [c.make_ordered_wire(1 << 16, d) for c in world.comms]
+    rng = np.random.default_rng(900 + p)
+    sh_ = torch.cuda.current_stream().cuda_stream
+    for slot, (off, n) in enumerate([(0, 4096), (24, 7), (512, 3001), (8, 1)]):
+        data = [random_f16(rng, n) for _ in range(p)]
+        for w, x in zip(wires, data):
+            w.halves[0][off:off + n].copy_(torch.from_numpy(x))
+        ops = [w.hier_op(0, off, n, k, sh_, slot=slot) for w in wires]
+        assert ops[0].fn == "gs_oneshot_allreduce_f16"
+        launch(ops)
+        torch.cuda.synchronize()
+        want = rp.fold_f16_tree(data)
+        for r, w in enumerate(wires):
+            assert np.array_equal(w.halves[0][off:off + n].cpu().numpy(), want), (p, k, r, slot)
             assert w.status_word() == 0
 
 

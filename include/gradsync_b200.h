@@ -335,9 +335,11 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
                   uint32_t parity, uint32_t flag_mask, void* stream);
 
 /* One CTA per rank: this rank's remote stores from earlier kernels on the
- * stream are visible to every peer, and every peer's to this rank. */
+ * stream are visible to every peer, and every peer's to this rank.
+ * epoch_inc != 0: afterwards add it to the rank's device epoch base (the
+ * step's last kernel advances the base for the next step). */
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
-                  void* stream);
+                  uint32_t epoch_inc, void* stream);
 
 /* ---- native step executor (gs_step.cu) ---------------------------------
  * One call launches a whole step — the same kernels, in the same order, as
@@ -351,7 +353,8 @@ int gs_step_replicated(const gs_step_rank* rank, int g_is_f16, gs_step_params pa
 /* The sharded (ZeRO-1) step in fused kernels for `nranks` ranks (1 on a box,
  * p when emulated; ranks = host array, ctx = device gs_rank_ctx table):
  * [pack per rank] -> gs_rs_pass1 -> gs_peer_fence -> gs_lars_trust per rank
- * -> gs_pass2_push -> gs_peer_fence -> epoch base += 4 per rank.  Epochs
+ * -> gs_pass2_push -> gs_peer_fence (which adds 4 to every rank's epoch
+ * base).  Epochs
  * 1, 2, 3 of the step; max_own >= every rank's owned chunk count. */
 int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, int p,
                  const uint64_t* wires, const uint64_t* sig, const uint64_t* peer_partials,

@@ -130,7 +130,7 @@ SIGNATURES = {
                             c_void_p]),
     "gs_pass2_push": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, StepParams,
                               c_uint32, c_uint32, c_uint32, c_void_p]),
-    "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_void_p]),
+    "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_uint32, c_void_p]),
     "gs_step_replicated": (c_int, [c_void_p, c_int, StepParams, c_uint32, c_uint32, c_uint32,
                                    c_void_p]),
     "gs_step_zero": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p,

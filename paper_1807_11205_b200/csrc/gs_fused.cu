@@ -274,11 +274,15 @@ pass2_push_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t*
 }
 
 __global__ void peer_fence_kernel(const gs_rank_ctx* __restrict__ ranks, const uint64_t* __restrict__ sig,
-                                  int p, uint32_t epoch) {
+                                  int p, uint32_t epoch, uint32_t epoch_inc) {
   const PeerCta pc = peer_cta(ranks, 1);
   if (pc.R->epoch_base != nullptr) epoch += *pc.R->epoch_base;
   if (threadIdx.x < p) __threadfence_system();  // this GPU's earlier remote stores
   peer_barrier(sig, pc, p, 1, epoch, kSiteFence);
+  // the step's last kernel: advance the rank's epoch base for the next step
+  // (every kernel of this step read it at its start; saves a launch)
+  if (epoch_inc != 0u && threadIdx.x == 0 && pc.R->epoch_base != nullptr)
+    *const_cast<uint32_t*>(pc.R->epoch_base) += epoch_inc;
 }
 
 }  // namespace
@@ -348,12 +352,12 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
 }
 
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
-                  void* stream) {
+                  uint32_t epoch_inc, void* stream) {
   GS_REQUIRE(p >= 1 && p <= 32 && nranks >= 1 && nranks <= p, "gs_peer_fence: bad arguments");
   if (p == 1) return GS_OK;
   GS_REQUIRE(ranks && sig, "gs_peer_fence: null pointer");
   GS_REQUIRE(epoch != 0, "gs_peer_fence: epoch 0 is the reset value");
-  peer_fence_kernel<<<nranks, 32, 0, (cudaStream_t)stream>>>(ranks, sig, p, epoch);
+  peer_fence_kernel<<<nranks, 32, 0, (cudaStream_t)stream>>>(ranks, sig, p, epoch, epoch_inc);
   return gs_check_launch("gs_peer_fence");
 }
 

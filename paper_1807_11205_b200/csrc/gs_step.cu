@@ -33,7 +33,7 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
                   int b0, int b1, int max_chunks, gs_step_params params, uint32_t hint,
                   uint32_t parity, uint32_t flag_mask, void* stream);
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
-                  void* stream);
+                  uint32_t epoch_inc, void* stream);
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 
 #define GS_TRY(call)          \
@@ -66,7 +66,7 @@ int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, 
     if (ranks[i].npack > 0) GS_TRY(gs_batched_copy(ranks[i].pack, ranks[i].npack, stream));
   GS_TRY(gs_rs_pass1(ctx, nranks, p, wires, sig, peer_partials, peer_ctl, 0, nbuckets, params,
                      hint, parity, 1, nblocks, stream));
-  GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 2, stream));
+  GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 2, 0, stream));
   for (int i = 0; i < nranks; ++i) {
     const gs_step_rank& r = ranks[i];
     GS_TRY(gs_lars_trust(r.segs, r.nseg, r.nchunk, r.partials, params, r.seg_scale, r.seg_out,
@@ -74,8 +74,8 @@ int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, 
   }
   GS_TRY(gs_pass2_push(ctx, nranks, p, peer_working, 0, nbuckets, max_own, params, hint, parity,
                        flag_mask, stream));
-  GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 3, stream));
-  for (int i = 0; i < nranks; ++i) GS_TRY(gs_counter_add(ranks[i].epoch_base, 4, stream));
+  // the closing fence also advances every rank's epoch base by the step's 4
+  GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 3, 4, stream));
   return GS_OK;
 }
 

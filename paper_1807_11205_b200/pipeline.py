@@ -472,7 +472,7 @@ class GradientPipeline:
                            plan.sp, plan.hint, plan.parity, 1, self._nblocks, sh)
             if timer:
                 timer("fence")
-            yield self._op("gs_peer_fence", p, sig, 2, sh)
+            yield self._op("gs_peer_fence", p, sig, 2, 0, sh)
             if timer:
                 timer("trust")
             plan.trust(sh)
@@ -482,8 +482,8 @@ class GradientPipeline:
                            plan.hint, plan.parity, _MASK, sh, count=self._n_own)
             if timer:
                 timer("fence_end")
-            yield self._op("gs_peer_fence", p, sig, 3, sh)
-            _native.call("gs_counter_add", ebase, 4, sh)
+            # the closing fence also advances the epoch base for the next step
+            yield self._op("gs_peer_fence", p, sig, 3, 4, sh)
         else:
             # the reduce-scatter folds in place in the reduced wire
             if timer:
@@ -1114,12 +1114,11 @@ class GradientPipeline:
         if self.sharded:
             p, a = self.comm.topo.p, self.arena
             sig = dev.ptr(a.peers("sig"))
-            yield self._op("gs_peer_fence", p, sig, nb + 1, sh)
+            yield self._op("gs_peer_fence", p, sig, nb + 1, 0, sh)
             plan.trust(sh)
             yield self._op("gs_pass2_push", p, dev.ptr(a.peers("working")), 0, nb, None, plan.sp,
                            plan.hint, plan.parity, _MASK, sh, count=self._n_own)
-            yield self._op("gs_peer_fence", p, sig, nb + 2, sh)
-            _native.call("gs_counter_add", dev.ptr(self.epoch_base), nb + 3, sh)
+            yield self._op("gs_peer_fence", p, sig, nb + 2, nb + 3, sh)
             self._last_wire = self.red
         else:
             plan.finish(sh, self.f16, _MASK)

@@ -50,7 +50,7 @@ def test_abi_version_and_errors_without_gpu():
     assert b"p must be 2, 4 or 8" in lib.gs_last_error()
     assert lib.gs_ordered_allreduce_f16(None, 1, 2, None, None, 0, 16, 0, 8, 0, None) == -1
     assert b"epoch 0" in lib.gs_last_error()
-    assert lib.gs_peer_fence(None, 3, 2, None, 1, None) == -1
+    assert lib.gs_peer_fence(None, 3, 2, None, 1, 0, None) == -1
 
 
 def test_struct_layouts_match_header():

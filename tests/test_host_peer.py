@@ -39,8 +39,8 @@ def test_lockstep_driver_batches_one_op_per_rank(monkeypatch):
     launched, log = [], []
     monkeypatch.setattr(emulation, "launch", lambda ops: launched.append([o.ctx for o in ops]))
     ctx = [rank_ctx(r) for r in range(3)]
-    gens = [_gen([PeerOp("gs_peer_fence", ctx[r], (3, 0, 1, 0)),
-                  PeerOp("gs_peer_fence", ctx[r], (3, 0, 2, 0))], log, r) for r in range(3)]
+    gens = [_gen([PeerOp("gs_peer_fence", ctx[r], (3, 0, 1, 0, 0)),
+                  PeerOp("gs_peer_fence", ctx[r], (3, 0, 2, 0, 0))], log, r) for r in range(3)]
     assert emulation.LocalWorld.drive(gens) == 2
     assert len(launched) == 2 and all(len(x) == 3 for x in launched)
     assert [int(c["rank"][0]) for c in launched[0]] == [0, 1, 2]
@@ -51,7 +51,7 @@ def test_lockstep_driver_batches_one_op_per_rank(monkeypatch):
 def test_lockstep_driver_refuses_divergent_ranks(monkeypatch):
     monkeypatch.setattr(emulation, "launch", lambda ops: None)
     ctx = [rank_ctx(r) for r in range(2)]
-    gens = [_gen([PeerOp("gs_peer_fence", ctx[0], (2, 0, 1, 0))], [], 0),
+    gens = [_gen([PeerOp("gs_peer_fence", ctx[0], (2, 0, 1, 0, 0))], [], 0),
             _gen([], [], 1)]
     with pytest.raises(RuntimeError, match="diverged"):
         emulation.LocalWorld.drive(gens)
@@ -59,7 +59,7 @@ def test_lockstep_driver_refuses_divergent_ranks(monkeypatch):
 
 def test_batched_launch_requires_identical_arguments(monkeypatch):
     monkeypatch.setattr(_peer.dev, "upload", lambda *a, **k: None)
-    ops = [PeerOp("gs_peer_fence", rank_ctx(0), (2, 0, 1, 0)),
-           PeerOp("gs_peer_fence", rank_ctx(1), (2, 0, 2, 0))]
+    ops = [PeerOp("gs_peer_fence", rank_ctx(0), (2, 0, 1, 0, 0)),
+           PeerOp("gs_peer_fence", rank_ctx(1), (2, 0, 2, 0, 0))]
     with pytest.raises(RuntimeError, match="ranks diverged"):
         _peer.launch(ops)

@@ -139,7 +139,9 @@ typedef struct gs_rank_ctx {
   void* red;                    /* gs_rs_pass1: base of this rank's reduced wire (the
                                    segments' g pointers lie in it; same layout as the
                                    raw wires the fold reads) */
-} gs_rank_ctx; /* 96 bytes */
+  const double* partials;       /* gs_trust_fence: this rank's chunk partials */
+  double* seg_out;              /* gs_trust_fence: per-segment norms / rates */
+} gs_rank_ctx; /* 112 bytes */
 
 /* One rank's buffers for the native step executor (gs_step_*): a HOST
  * struct (the executor reads it on the host and launches from it). */
@@ -341,6 +343,17 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
                   uint32_t epoch_inc, void* stream);
 
+/* gs_peer_fence(epoch) followed by gs_lars_trust in ONE launch (the
+ * sharded step's middle): the first nranks CTAs fence and run the peer
+ * barrier (one per rank, as gs_peer_fence), then publish `epoch` in
+ * ctl->counter[0]; the other nranks x (nseg + 1) CTAs wait for their rank's
+ * word and run the trust kernel's CTAs over the rank's segs / partials /
+ * seg_scale / seg_out / ctl from the gs_rank_ctx table (same order, same
+ * bits).  pass 2 may be PDL-launched behind it. */
+int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   uint32_t epoch, int nseg, int nchunk, gs_step_params params, uint32_t parity,
+                   void* stream);
+
 /* ---- native step executor (gs_step.cu) ---------------------------------
  * One call launches a whole step — the same kernels, in the same order, as
  * the pipeline's per-kernel path, without per-kernel host work. */
@@ -352,8 +365,8 @@ int gs_step_replicated(const gs_step_rank* rank, int g_is_f16, gs_step_params pa
 
 /* The sharded (ZeRO-1) step in fused kernels for `nranks` ranks (1 on a box,
  * p when emulated; ranks = host array, ctx = device gs_rank_ctx table):
- * [pack per rank] -> gs_rs_pass1 -> gs_peer_fence -> gs_lars_trust per rank
- * -> gs_pass2_push -> gs_peer_fence (which adds 4 to every rank's epoch
+ * [pack per rank] -> gs_rs_pass1 -> gs_trust_fence (fence + trust) ->
+ * gs_pass2_push -> gs_peer_fence (which adds 4 to every rank's epoch
  * base).  Epochs
  * 1, 2, 3 of the step; max_own >= every rank's owned chunk count. */
 int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, int p,

@@ -273,6 +273,55 @@ pass2_push_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t*
                                peer_working, p, woff);
 }
 
+// gs_peer_fence + gs_lars_trust in one launch.  Blocks [0, nranks): one
+// fence CTA per rank (fence.sys, the peer barrier of gs_peer_fence, then
+// `epoch` published in ctl->counter[0]); blocks nranks + r * (nseg + 1) + s:
+// trust CTA s of rank r, which waits for its rank's word.  The fence CTAs
+// come first in the grid, so they are dispatched before any waiting trust
+// CTA and the launch cannot deadlock even when it does not fit at once.
+__global__ void __launch_bounds__(kThreads)
+trust_fence_kernel(const gs_rank_ctx* __restrict__ ranks, int nranks, const uint64_t* __restrict__ sig,
+                   int p, uint32_t epoch, int nseg, int nchunk, const gs_step_params params,
+                   uint32_t parity) {
+  gs::griddep_launch_dependents();  // pass 2 (PDL) may start issuing its loads
+  if ((int)blockIdx.x < nranks) {
+    PeerCta pc;
+    pc.R = ranks + blockIdx.x;
+    pc.lb = 0;
+    pc.nb = 1;
+    if (pc.R->epoch_base != nullptr) epoch += *pc.R->epoch_base;
+    if (threadIdx.x < p) __threadfence_system();  // this GPU's earlier remote stores
+    peer_barrier(sig, pc, p, 1, epoch, kSiteFence);
+    if (threadIdx.x == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&pc.R->ctl->counter[0]), "r"(epoch)
+                   : "memory");
+    return;
+  }
+  const int b = blockIdx.x - nranks;
+  const gs_rank_ctx& R = ranks[b / (nseg + 1)];
+  const int s = b % (nseg + 1);
+  if (R.epoch_base != nullptr) epoch += *R.epoch_base;
+  if (threadIdx.x == 0) {
+    const uint32_t* w = &R.ctl->counter[0];
+    uint32_t v;
+    uint32_t spins = 0;
+    const uint64_t t0 = globaltimer_ns();
+    const uint64_t limit = R.timeout_ns ? R.timeout_ns : kPeerTimeoutNs;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+      if (v == epoch) break;
+      if ((++spins & 63u) == 0) {
+        // the fence CTA gave up (its wait timed out and recorded a status)
+        if (R.status != nullptr && *reinterpret_cast<volatile uint32_t*>(R.status) != 0u) break;
+        if (globaltimer_ns() - t0 > limit) break;
+      }
+    }
+  }
+  __syncthreads();
+  trust_cta(R.segs, s, nseg, nchunk, R.partials, params, const_cast<float*>(R.seg_scale),
+            R.seg_out, R.ctl, parity, nullptr, 0);
+}
+
 __global__ void peer_fence_kernel(const gs_rank_ctx* __restrict__ ranks, const uint64_t* __restrict__ sig,
                                   int p, uint32_t epoch, uint32_t epoch_inc) {
   const PeerCta pc = peer_cta(ranks, 1);
@@ -349,6 +398,19 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
     return GS_ECUDA;
   }
   return gs_check_launch("gs_pass2_push");
+}
+
+int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   uint32_t epoch, int nseg, int nchunk, gs_step_params params, uint32_t parity,
+                   void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 32 && nranks >= 1 && nranks <= p && nseg >= 0 && nchunk >= 0 &&
+                 parity <= 1,
+             "gs_trust_fence: bad arguments");
+  GS_REQUIRE(ranks && sig, "gs_trust_fence: null pointer");
+  GS_REQUIRE(epoch != 0, "gs_trust_fence: epoch 0 is the reset value");
+  trust_fence_kernel<<<nranks * (nseg + 2), kThreads, 0, (cudaStream_t)stream>>>(
+      ranks, nranks, sig, p, epoch, nseg, nchunk, params, parity);
+  return gs_check_launch("gs_trust_fence");
 }
 
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,

@@ -241,43 +241,8 @@ lars_trust_kernel(const gs_segment* __restrict__ segs, int nseg, int nchunk,
                   int npeers) {
   gs::griddep_wait();                 // pass 1's partials are complete
   gs::griddep_launch_dependents();    // let pass 2 start issuing its loads now
-  const int s = blockIdx.x;
-  if (s == nseg) {
-    if (threadIdx.x == 0) {
-      // the next step's flag word and counter (the host read them after the
-      // previous step; nobody touches them before this step ends)
-      ctl->flags[parity ^ 1u] = 0u;
-      if (npeers > 0) {
-        // sharded update with separate collectives: the step is rejected if
-        // any rank saw a non-finite value
-        uint32_t f = 0;
-        for (int q = 0; q < npeers; ++q)
-          f |= *reinterpret_cast<const volatile uint32_t*>(
-              &reinterpret_cast<const gs_ctl*>(peer_ctl[q])->flags[parity]);
-        if (f) atomicOr(&ctl->flags[parity], f);
-      }
-    }
-    if (!(params.mode & GS_MODE_GRADNORM)) return;
-    double x = 0.0, y = 0.0, z = 0.0;
-#pragma unroll 8
-    for (int i = threadIdx.x; i < nchunk; i += kThreads) z += partials[3 * (int64_t)i + 2];
-    gs::block_sum3<kThreads>(x, y, z);
-    if (threadIdx.x == 0) ctl->grad_norm = __dsqrt_rn(z);
-    return;
-  }
-  const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
-  GS_DCHECK(cb >= 0 && cn >= 0 && cb + cn <= nchunk, "trust: segment's chunk range");
-  double x = 0.0, y = 0.0, z = 0.0;
-#pragma unroll 2
-  for (int i = threadIdx.x; i < cn; i += kThreads) {
-    const double* pp = partials + 3 * (int64_t)(cb + i);
-    x += pp[0];
-    y += pp[1];
-    z += pp[2];
-  }
-  gs::block_sum3<kThreads>(x, y, z);
-  if (threadIdx.x == 0)
-    trust_eval(segs[s].flags, x, y, z, params, seg_scale + s, seg_out + 4 * (int64_t)s);
+  trust_cta(segs, blockIdx.x, nseg, nchunk, partials, params, seg_scale, seg_out, ctl, parity,
+            peer_ctl, npeers);
 }
 
 // W2: also sum the updated masters' squares in pass 1's order and store the

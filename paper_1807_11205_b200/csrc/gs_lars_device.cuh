@@ -232,6 +232,58 @@ __device__ __forceinline__ void trust_eval(uint32_t sflags, double sw, double se
   o[3] = sg;
 }
 
+// One CTA of the trust kernel (gs_lars.cu lars_trust_kernel, gs_fused.cu
+// trust_fence_kernel): CTA s < nseg folds segment s's chunk partials
+// (256-strided in chunk order, then the fixed block tree -- the same order on
+// every path) and derives its trust scale; CTA nseg clears the next step's
+// flag word, ORs the peers' flags in (sharded update with separate
+// collectives) and folds every chunk's sum g^2 for the grad-norm metric
+// (experiment.py:408-411).
+__device__ __forceinline__ void trust_cta(const gs_segment* __restrict__ segs, int s, int nseg,
+                                          int nchunk, const double* __restrict__ partials,
+                                          const gs_step_params& params,
+                                          float* __restrict__ seg_scale,
+                                          double* __restrict__ seg_out, gs_ctl* __restrict__ ctl,
+                                          uint32_t parity, const uint64_t* __restrict__ peer_ctl,
+                                          int npeers) {
+  if (s == nseg) {
+    if (threadIdx.x == 0) {
+      // the next step's flag word (the host read it after the previous step;
+      // nobody touches it before this step ends)
+      ctl->flags[parity ^ 1u] = 0u;
+      if (npeers > 0) {
+        // sharded update with separate collectives: the step is rejected if
+        // any rank saw a non-finite value
+        uint32_t f = 0;
+        for (int q = 0; q < npeers; ++q)
+          f |= *reinterpret_cast<const volatile uint32_t*>(
+              &reinterpret_cast<const gs_ctl*>(peer_ctl[q])->flags[parity]);
+        if (f) atomicOr(&ctl->flags[parity], f);
+      }
+    }
+    if (!(params.mode & GS_MODE_GRADNORM)) return;
+    double x = 0.0, y = 0.0, z = 0.0;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < nchunk; i += kThreads) z += partials[3 * (int64_t)i + 2];
+    gs::block_sum3<kThreads>(x, y, z);
+    if (threadIdx.x == 0) ctl->grad_norm = __dsqrt_rn(z);
+    return;
+  }
+  const int cb = segs[s].chunk_begin, cn = segs[s].chunk_count;
+  GS_DCHECK(cb >= 0 && cn >= 0 && cb + cn <= nchunk, "trust: segment's chunk range");
+  double x = 0.0, y = 0.0, z = 0.0;
+#pragma unroll 2
+  for (int i = threadIdx.x; i < cn; i += kThreads) {
+    const double* pp = partials + 3 * (int64_t)(cb + i);
+    x += pp[0];
+    y += pp[1];
+    z += pp[2];
+  }
+  gs::block_sum3<kThreads>(x, y, z);
+  if (threadIdx.x == 0)
+    trust_eval(segs[s].flags, x, y, z, params, seg_scale + s, seg_out + 4 * (int64_t)s);
+}
+
 // ----------------------------------------------------------------- pass 2
 // v = m*v + s*eff (lars.py:178), w -= v (:179), w16 = f32_to_f16(w) (:180),
 // eff = g or g + wd*w (:169-172); every product and sum rounded separately.

@@ -35,6 +35,9 @@ int gs_pass2_push(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* p
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,
                   uint32_t epoch_inc, void* stream);
 int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
+int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   uint32_t epoch, int nseg, int nchunk, gs_step_params params, uint32_t parity,
+                   void* stream);
 
 #define GS_TRY(call)          \
   do {                        \
@@ -66,12 +69,8 @@ int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, 
     if (ranks[i].npack > 0) GS_TRY(gs_batched_copy(ranks[i].pack, ranks[i].npack, stream));
   GS_TRY(gs_rs_pass1(ctx, nranks, p, wires, sig, peer_partials, peer_ctl, 0, nbuckets, params,
                      hint, parity, 1, nblocks, stream));
-  GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 2, 0, stream));
-  for (int i = 0; i < nranks; ++i) {
-    const gs_step_rank& r = ranks[i];
-    GS_TRY(gs_lars_trust(r.segs, r.nseg, r.nchunk, r.partials, params, r.seg_scale, r.seg_out,
-                         r.ctl, parity, nullptr, 0, stream));
-  }
+  GS_TRY(gs_trust_fence(ctx, nranks, p, sig, 2, ranks[0].nseg, ranks[0].nchunk, params, parity,
+                        stream));
   GS_TRY(gs_pass2_push(ctx, nranks, p, peer_working, 0, nbuckets, max_own, params, hint, parity,
                        flag_mask, stream));
   // the closing fence also advances every rank's epoch base by the step's 4

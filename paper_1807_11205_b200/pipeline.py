@@ -403,7 +403,8 @@ class GradientPipeline:
                              epoch_base=dev.ptr(self.epoch_base), segs=dev.ptr(plan.base_segs),
                              chunks=dev.ptr(plan.d_chunks), own_list=dev.ptr(self._own_list),
                              own_off=dev.ptr(self._own_off), ctl=dev.ptr(plan.ctl),
-                             seg_scale=dev.ptr(plan.seg_scale), red=dev.ptr(self.red))
+                             seg_scale=dev.ptr(plan.seg_scale), red=dev.ptr(self.red),
+                             partials=dev.ptr(plan.partials), seg_out=dev.ptr(plan.seg_out))
         # this rank's one-entry context table for the native executor
         self._ctx_dev = dev.upload(self._ctx, d)
 
@@ -471,11 +472,10 @@ class GradientPipeline:
                            dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")), 0, nb,
                            plan.sp, plan.hint, plan.parity, 1, self._nblocks, sh)
             if timer:
-                timer("fence")
-            yield self._op("gs_peer_fence", p, sig, 2, 0, sh)
-            if timer:
-                timer("trust")
-            plan.trust(sh)
+                timer("fence_trust")
+            # the peer fence and the trust kernel in one launch
+            yield self._op("gs_trust_fence", p, sig, 2, plan.nseg, plan.nchunk, plan.sp,
+                           plan.parity, sh)
             if timer:
                 timer("pass2_push")
             yield self._op("gs_pass2_push", p, dev.ptr(a.peers("working")), 0, nb, None, plan.sp,
@@ -1114,8 +1114,8 @@ class GradientPipeline:
         if self.sharded:
             p, a = self.comm.topo.p, self.arena
             sig = dev.ptr(a.peers("sig"))
-            yield self._op("gs_peer_fence", p, sig, nb + 1, 0, sh)
-            plan.trust(sh)
+            yield self._op("gs_trust_fence", p, sig, nb + 1, plan.nseg, plan.nchunk, plan.sp,
+                           plan.parity, sh)
             yield self._op("gs_pass2_push", p, dev.ptr(a.peers("working")), 0, nb, None, plan.sp,
                            plan.hint, plan.parity, _MASK, sh, count=self._n_own)
             yield self._op("gs_peer_fence", p, sig, nb + 2, nb + 3, sh)

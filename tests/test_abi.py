@@ -51,6 +51,7 @@ def test_abi_version_and_errors_without_gpu():
     assert lib.gs_ordered_allreduce_f16(None, 1, 2, None, None, 0, 16, 0, 8, 0, None) == -1
     assert b"epoch 0" in lib.gs_last_error()
     assert lib.gs_peer_fence(None, 3, 2, None, 1, 0, None) == -1
+    assert lib.gs_trust_fence(None, 1, 2, None, 0, 1, 1, _native.StepParams(), 0, None) == -1
 
 
 def test_struct_layouts_match_header():
@@ -60,7 +61,7 @@ def test_struct_layouts_match_header():
                            (_native.COPY_DTYPE, "gs_copy", 24),
                            (_native.STEP_PARAMS_DTYPE, "gs_step_params", 56),
                            (_native.CTL_DTYPE, "gs_ctl", 48),
-                           (_native.RANK_CTX_DTYPE, "gs_rank_ctx", 96)):
+                           (_native.RANK_CTX_DTYPE, "gs_rank_ctx", 112)):
         assert dt.itemsize == size
         assert re.search(rf"}}\s*{name};\s*/\*\s*{size} bytes", text), name
     m = {k: int(v, 0) for k, v in re.findall(r"#define (GS_[A-Z0-9_]+) (\d+|0x[0-9a-f]+)u?", text)}

@@ -381,7 +381,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         # where the host runs ahead of the device): the events time the
         # device, not the host prologue; at N > 1 the barrier after the sleep
         # starts every rank's step together
-        torch.cuda._sleep(1_000_000)
+        torch.cuda._sleep(4_000_000)
         device_barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

@@ -283,6 +283,17 @@ int gs_oneshot_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const 
                              int64_t cap, uint32_t epoch, int nblocks, uint32_t parity,
                              void* stream);
 
+/* LL form of the same all-reduce (no fence, no barrier): every 4 bytes of
+ * payload travel as one 8-byte word {payload, epoch} into slot [parity][rank]
+ * (cap / 2 words) of every rank's inbox; each rank polls its own slots until
+ * every word carries this call's epoch, folds in the reference's tree order
+ * and writes its buffer.  Same bits; 2 x (p-1) x S bytes out per rank.
+ * Whole 8-element vectors only (n % 8 == 0, offset % 8 == 0, n <= cap);
+ * consecutive LL / one-shot calls on the same inboxes alternate parity. */
+int gs_ll_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                        const uint64_t* inbox, int64_t offset, int64_t n, int64_t cap,
+                        uint32_t epoch, int nblocks, uint32_t parity, void* stream);
+
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,
                           const uint64_t* bufs, const uint64_t* sig, int64_t offset, int64_t n,
                           uint32_t epoch, int nblocks, int push, void* stream);

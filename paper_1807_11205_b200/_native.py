@@ -118,6 +118,8 @@ SIGNATURES = {
     "gs_oneshot_allreduce_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                          c_int64, c_int64, c_int64, c_uint32, c_int, c_uint32,
                                          c_void_p]),
+    "gs_ll_allreduce_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int64, c_int64,
+                                    c_int64, c_uint32, c_int, c_uint32, c_void_p]),
     "gs_hier_allreduce_f16": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int64,
                                       c_int64, c_uint32, c_int, c_int, c_void_p]),
     "gs_ordered_reduce_scatter_f16": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p,

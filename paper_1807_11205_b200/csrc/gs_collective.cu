@@ -478,6 +478,107 @@ oneshot_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
   if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
 }
 
+// LL form (no barrier): every 4 bytes of payload (two binary16 values)
+// travel as one 8-byte word {payload, epoch} into slot [parity][rank] of
+// every rank's inbox (single 64-bit stores, two per 16-byte vector store);
+// each rank polls ITS inbox -- all of a thread's words from all p slots are
+// loaded at once and re-loaded until every flag carries this call's epoch --
+// then folds in the reference's tree order into its wire.  The flag in the
+// data is the synchronisation: no fence, no barrier.  Consecutive LL calls
+// alternate parity (a peer can write call c+2 only after this rank's call
+// c+1 words reached it, i.e. after this rank folded call c).
+constexpr int kLLUnits = 4;  // 4-byte units per thread (8 halves, one uint4)
+
+__device__ __forceinline__ void st_relaxed_sys_v2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_sys_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads)
+ll_allreduce_kernel(const gs_rank_ctx* __restrict__ ranks, int nb,
+                    const uint64_t* __restrict__ bufs, const uint64_t* __restrict__ inbox,
+                    int64_t offset, int64_t n, int64_t cap, uint32_t epoch, uint32_t parity) {
+  const PeerCta c = peer_cta(ranks, nb);
+  const int rank = c.R->rank;
+  if (c.R->epoch_base != nullptr) epoch += *c.R->epoch_base;
+  uint16_t* mine = reinterpret_cast<uint16_t*>(bufs[rank]) + offset;
+  // whole 8-half vectors (n % 8 == 0, 16-byte aligned: the host checks)
+  const int64_t nv = n / 8;
+  const uint64_t tag = (uint64_t)epoch << 32;
+  const size_t slot_words = (size_t)cap / 2;
+  uint64_t* dst[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+    dst[q] = reinterpret_cast<uint64_t*>(inbox[q]) + ((size_t)parity * P + rank) * slot_words;
+  const int64_t v = (int64_t)c.lb * kThreads + threadIdx.x;  // this thread's vector
+  const int64_t stride = (int64_t)nb * kThreads;
+  for (int64_t i = v; i < nv; i += stride) {
+    const uint4 x = __ldcv(reinterpret_cast<const uint4*>(mine) + i);
+    const uint64_t w0 = tag | x.x, w1 = tag | x.y, w2 = tag | x.z, w3 = tag | x.w;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      st_relaxed_sys_v2(dst[q] + 4 * i, w0, w1);
+      st_relaxed_sys_v2(dst[q] + 4 * i + 2, w2, w3);
+    }
+  }
+  const uint64_t* src[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+    src[q] = reinterpret_cast<const uint64_t*>(inbox[rank]) + ((size_t)parity * P + q) * slot_words;
+  uint32_t bad = 0;
+  for (int64_t i = v; i < nv; i += stride) {
+    uint64_t w[P][4];
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t spins = 0;
+    for (;;) {
+      int missing = -1;  // the first peer whose words are not in yet
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        ld_relaxed_sys_v2(src[q] + 4 * i, w[q][0], w[q][1]);
+        ld_relaxed_sys_v2(src[q] + 4 * i + 2, w[q][2], w[q][3]);
+      }
+#pragma unroll
+      for (int q = P - 1; q >= 0; --q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if ((uint32_t)(w[q][k] >> 32) != epoch) missing = q;
+      if (missing < 0) break;
+      if ((++spins & 63u) == 0) {
+        uint32_t* status = c.R->status;
+        if (status != nullptr && *reinterpret_cast<volatile uint32_t*>(status) != 0u) break;
+        const uint64_t limit = c.R->timeout_ns ? c.R->timeout_ns : kPeerTimeoutNs;
+        if (globaltimer_ns() - t0 > limit) {
+          if (status != nullptr)  // the first report wins (threads may miss different peers)
+            atomicCAS(status, 0u, 0x80000000u | (kSiteOrderedAllreduce << 20) |
+                                      ((uint32_t)missing << 8) | (uint32_t)rank);
+          else
+            __trap();
+          break;
+        }
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float a[P], b[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const float2 f = gs::widen2((uint32_t)w[q][k]);
+        a[q] = f.x;
+        b[q] = f.y;
+      }
+      o[k] = gs::narrow2(tree<P>(a), tree<P>(b));
+      bad |= ((o[k] & 0x7C00u) == 0x7C00u) | ((o[k] & 0x7C000000u) == 0x7C000000u);
+    }
+    reinterpret_cast<uint4*>(mine)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  bad = __reduce_or_sync(0xFFFFFFFFu, bad);
+  if (c.R->nonfinite != nullptr && bad && (threadIdx.x & 31) == 0) atomicOr(c.R->nonfinite, 1u);
+}
+
 __global__ void counter_add_kernel(uint32_t* counter, uint32_t inc) { *counter += inc; }
 
 }  // namespace
@@ -628,6 +729,37 @@ int gs_oneshot_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const 
   }
 #undef GS_OS
   return gs_check_launch("gs_oneshot_allreduce_f16");
+}
+
+int gs_ll_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* bufs,
+                        const uint64_t* inbox, int64_t offset, int64_t n, int64_t cap,
+                        uint32_t epoch, int nblocks, uint32_t parity, void* stream) {
+  GS_PEER_ARGS("gs_ll_allreduce_f16");
+  GS_REQUIRE(n >= 0 && offset >= 0 && n <= cap && n % 8 == 0 && offset % 8 == 0 &&
+                 parity <= 1 && cap % 8 == 0,
+             "gs_ll_allreduce_f16: need whole 8-element vectors at an 8-element offset, "
+             "n <= cap and parity 0/1");
+  if (p == 1 || n == 0) return GS_OK;
+  GS_REQUIRE(ranks && bufs && inbox, "gs_ll_allreduce_f16: null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+#define GS_LL(P)                                                                                 \
+  case P: {                                                                                      \
+    auto k = ll_allreduce_kernel<P>;                                                             \
+    const int nb = peer_grid((const void*)k, kThreads, 0, nblocks, nranks);                      \
+    k<<<nb * nranks, kThreads, 0, s>>>(ranks, nb, bufs, inbox, offset, n, cap, epoch, parity);   \
+    break;                                                                                       \
+  }
+  switch (p) {
+    GS_LL(2)
+    GS_LL(3)
+    GS_LL(4)
+    GS_LL(5)
+    GS_LL(6)
+    GS_LL(7)
+    GS_LL(8)
+  }
+#undef GS_LL
+  return gs_check_launch("gs_ll_allreduce_f16");
 }
 
 int gs_hier_allreduce_f16(const gs_rank_ctx* ranks, int nranks, int p, int k,

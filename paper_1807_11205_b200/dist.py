@@ -206,19 +206,28 @@ class OrderedWire:
         self._setup(bases, device, push, comm.timeout_s)
         dist.barrier()
 
-    #: buckets of at most this many binary16 elements take the one-shot
-    #: kernel (gs_oneshot_allreduce_f16: one barrier, (p-1) x S bytes out).
+    #: inbox slot capacity (binary16 elements) for the small-bucket kernels
+    SMALL_CAP_ELEMS = 1 << 17
+    #: buckets up to this many elements take the one-shot kernel
+    #: (gs_oneshot_allreduce_f16: one barrier, (p-1) x S bytes out).
     #: Measured at p = 4 (profiles/r02/y_n4, aa_n4): 13.1-14.3 µs up to 8 KB
     #: vs 19-20 (pull) / 15.3-16.1 (push) and NCCL's 14.6-15.0; from 16 KB
     #: on the (p-1) x S bytes make it tie or lose to the push form.
     ONESHOT_MAX_ELEMS = 4096
+    #: buckets up to this many elements take the LL kernel when whole
+    #: 8-element vectors (gs_ll_allreduce_f16: no fence, no barrier).
+    #: Measured at p = 4 (profiles/r02/ii_n4): 9.0-12.7 µs up to 256 KB,
+    #: 15.5 µs at 512 KB, vs NCCL ring 15.2-17.4 and the push form 16.4-24.1;
+    #: at 1 MB its doubled bytes lose (32.5 vs 19.2 NCCL, 24.7 push)
+    LL_MAX_ELEMS = 1 << 17
 
     @staticmethod
     def oneshot_cap(total: int, itemsize: int) -> int:
-        """Elements per inbox slot (0: no one-shot form, e.g. the fp32 wire)."""
+        """Elements per inbox slot (0: no small-bucket forms, e.g. the fp32
+        wire or SMALL_CAP_ELEMS = 0)."""
         if itemsize != 2:
             return 0
-        return (min(total, OrderedWire.ONESHOT_MAX_ELEMS) + 255) // 256 * 256
+        return (min(total, OrderedWire.SMALL_CAP_ELEMS) + 255) // 256 * 256
 
     @staticmethod
     def sig_bytes(nblocks: int, p: int) -> int:
@@ -229,7 +238,8 @@ class OrderedWire:
         """[wire A | wire B | signal area (3 barrier phases) | inbox (2 parities
         x p slots of oneshot_cap elements) | status]"""
         cap = OrderedWire.oneshot_cap(total, itemsize)
-        return 2 * total * itemsize + OrderedWire.sig_bytes(nblocks, p) + 2 * p * cap * 2 + 128
+        # 4 bytes per element and slot: the LL form's {payload, epoch} words
+        return 2 * total * itemsize + OrderedWire.sig_bytes(nblocks, p) + 2 * p * cap * 4 + 128
 
     def _setup(self, bases, device, push: bool, timeout_s: float) -> None:
         """Tables and this rank's context from every rank's base address
@@ -271,20 +281,37 @@ class OrderedWire:
     def grid_for(self, n: int) -> int:
         return max(1, min(self.nblocks, -(-int(n) // self.MIN_ELEMS_PER_CTA)))
 
+    def small_form(self, offset: int, n: int) -> str:
+        """The size rule: "ll", "oneshot" or "none" (the pull / push kernel)."""
+        if not self.cap or not 0 < n <= self.cap:
+            return "none"
+        if n <= OrderedWire.LL_MAX_ELEMS and n % 8 == 0 and offset % 8 == 0:
+            return "ll"
+        return "oneshot" if n <= OrderedWire.ONESHOT_MAX_ELEMS else "none"
+
     def allreduce_op(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0,
-                     oneshot: bool | None = None):
+                     small: str | None = None):
         """The bucket all-reduce as a peer op; `slot` (0-based within the
         step, < per_step) makes the epoch unique among the step's calls.
-        oneshot: None = the one-shot kernel for buckets up to
-        ONESHOT_MAX_ELEMS (bit-identical either way)."""
+        small: "oneshot" (one barrier), "ll" (no barrier; whole 8-element
+        vectors) or "none" (pull / push kernel); None = small_form's size
+        rule.  Bit-identical either way."""
         from . import _device as dev
         from ._peer import PeerOp
 
-        if oneshot is None:
-            oneshot = 0 < n <= self.cap
-        if oneshot and self.cap and 0 < n <= self.cap:
+        if small is None:
+            small = self.small_form(offset, n)
+        if small == "ll" and not (n % 8 == 0 and offset % 8 == 0):
+            small = "oneshot"
+        if small != "none" and self.cap and 0 < n <= self.cap:
             parity = self._oneshot_calls & 1
             self._oneshot_calls += 1
+            if small == "ll":
+                grid = max(1, min(self.nblocks, -(-n // (8 * 256))))
+                return PeerOp("gs_ll_allreduce_f16", self.ctx,
+                              (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.inbox_dev),
+                               offset, n, self.cap, slot + 1, grid, parity, stream_h),
+                              device=self.device)
             return PeerOp("gs_oneshot_allreduce_f16", self.ctx,
                           (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.inbox_dev),
                            dev.ptr(self.sig_dev), offset, n, self.cap, slot + 1, self.grid_for(n),
@@ -304,8 +331,8 @@ class OrderedWire:
         from . import _device as dev
         from ._peer import PeerOp
 
-        if 0 < n <= self.cap:
-            return self.allreduce_op(half, offset, n, stream_h, slot, oneshot=True)
+        if self.small_form(offset, n) != "none":
+            return self.allreduce_op(half, offset, n, stream_h, slot)
 
         return PeerOp("gs_hier_allreduce_f16", self.ctx,
                       (self.p, k, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
@@ -313,9 +340,9 @@ class OrderedWire:
                       device=self.device)
 
     def allreduce(self, half: int, offset: int, n: int, stream_h: int, slot: int = 0,
-                  oneshot: bool | None = None) -> None:
+                  small: str | None = None) -> None:
         from ._peer import launch
-        launch([self.allreduce_op(half, offset, n, stream_h, slot, oneshot)])
+        launch([self.allreduce_op(half, offset, n, stream_h, slot, small)])
 
     def advance(self, per_step: int, stream_h: int) -> None:
         from . import _device as dev

@@ -97,6 +97,7 @@ class LocalOrderedWire:
 
     from .dist import OrderedWire as _OW
     MIN_ELEMS_PER_CTA = _OW.MIN_ELEMS_PER_CTA
+    small_form = _OW.small_form
     nbytes_for = _OW.nbytes_for
     oneshot_cap = staticmethod(_OW.oneshot_cap)
     sig_bytes = staticmethod(_OW.sig_bytes)

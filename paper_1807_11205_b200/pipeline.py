@@ -909,11 +909,13 @@ class GradientPipeline:
         """Own bit-exact all-reduce of one bucket: flat, or over
         Topology(p, k)'s two levels (hierarchical buckets, hier_variant =
         'ordered_hier'); identical results."""
+        # the padded range (its zero slack stays zero under the fold): whole
+        # 8-element vectors, so small buckets qualify for the LL kernel
         if bk.algorithm == "ordered_hier" and self.f16:
-            return self.ordered.hier_op(half, bk.start, bk.length, self.comm.topo.k, sh, slot=slot)
+            return self.ordered.hier_op(half, bk.start, bk.padded, self.comm.topo.k, sh, slot=slot)
         # fp32: the reference's left fold does not factor over groups, so the
         # hierarchical buckets take the flat kernel (the same fold)
-        return self.ordered.allreduce_op(half, bk.start, bk.length, sh, slot=slot)
+        return self.ordered.allreduce_op(half, bk.start, bk.padded, sh, slot=slot)
 
     def _bucket_host_ranges(self):
         """Per bucket, the [lo, hi) element range of the registration-order

@@ -49,7 +49,7 @@ def random_f16(rng, n, special=True):
 
 # ---------------------------------------------------------------- collectives
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
-@pytest.mark.parametrize("form", ["pull", "push", "oneshot"])
+@pytest.mark.parametrize("form", ["pull", "push", "oneshot", "ll"])
 def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
     """gs_ordered_allreduce_f16 (pull and push forms) and
     the small-bucket gs_oneshot_allreduce_f16 == fold_f16_tree on every
@@ -59,18 +59,16 @@ def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
     world = LocalWorld(gs.Topology(p, 1), d, peer_ctas=8, timeout_s=20.0)
     total = 1 << 16
     push = form == "push"
-    if form == "oneshot":  # inboxes large enough for every bucket below
-        from paper_1807_11205_b200.dist import OrderedWire
-        monkeypatch.setattr(OrderedWire, "ONESHOT_MAX_ELEMS", total)
     wires = [c.make_ordered_wire(total, d, push=push) for c in world.comms]
     rng = np.random.default_rng(100 + p)
     sh_ = torch.cuda.current_stream().cuda_stream
-    for slot, (off, n) in enumerate([(0, 40000), (8, 1), (1003, 12345), (4096, 0)]):
+    for slot, (off, n) in enumerate([(0, 40000), (8, 1), (1003, 12345), (4096, 0),
+                                     (2048, 8 * 1001)]):
         data = [random_f16(rng, n) for _ in range(p)]
         for w, x in zip(wires, data):
             w.halves[0][off:off + n].copy_(torch.from_numpy(x))
-        launch([w.allreduce_op(0, off, n, sh_, slot=slot, oneshot=form == "oneshot")
-                for w in wires])
+        small = form if form in ("oneshot", "ll") else "none"
+        launch([w.allreduce_op(0, off, n, sh_, slot=slot, small=small) for w in wires])
         torch.cuda.synchronize()
         want = rp.fold_f16_tree([x for x in data]) if n else np.zeros(0, np.uint16)
         for r, w in enumerate(wires):
@@ -89,7 +87,7 @@ def test_hierarchical_allreduce_bit_exact(p, k, push, monkeypatch):
     from paper_1807_11205_b200.dist import OrderedWire
     # no one-shot inbox: every bucket below runs the two-level kernel (small
     # buckets take the one-shot kernel by default: test_hier_op_small_buckets)
-    monkeypatch.setattr(OrderedWire, "ONESHOT_MAX_ELEMS", 0)
+    monkeypatch.setattr(OrderedWire, "SMALL_CAP_ELEMS", 0)
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
     wires = [c.make_ordered_wire(1 << 16, d, push=push) for c in world.comms]
@@ -110,8 +108,8 @@ def test_hierarchical_allreduce_bit_exact(p, k, push, monkeypatch):
 
 @pytest.mark.parametrize("p,k", [(4, 2), (8, 4)])
 def test_hier_op_small_buckets(p, k):
-    """hier_op sends buckets up to ONESHOT_MAX_ELEMS to the one-shot kernel
-    (the reference's tree factors over the groups, so the bits are the
+    """hier_op sends small buckets to the LL (whole vectors) or one-shot
+    kernel (the reference's tree factors over the groups, so the bits are the
     hierarchy's); alternating parities over consecutive calls."""
     d = dev.require_cuda()
     world = LocalWorld(gs.Topology(p, k), d, peer_ctas=8, timeout_s=20.0)
@@ -123,7 +121,9 @@ def test_hier_op_small_buckets(p, k):
         for w, x in zip(wires, data):
             w.halves[0][off:off + n].copy_(torch.from_numpy(x))
         ops = [w.hier_op(0, off, n, k, sh_, slot=slot) for w in wires]
-        assert ops[0].fn == "gs_oneshot_allreduce_f16"
+        want_fn = "gs_ll_allreduce_f16" if n % 8 == 0 and off % 8 == 0 else \
+            "gs_oneshot_allreduce_f16"
+        assert ops[0].fn == want_fn
         launch(ops)
         torch.cuda.synchronize()
         want = rp.fold_f16_tree(data)

@@ -43,7 +43,7 @@ def main() -> None:
     ap.add_argument("--min-log2", type=int, default=10)
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--variants",
-                    default="ring,hierarchical,sharded,ordered,ordered_push,ordered_oneshot,"
+                    default="ring,hierarchical,sharded,ordered,ordered_push,ordered_oneshot,ordered_ll,"
                             "ordered_hier,ordered_hier_push")
     ap.add_argument("--out", default=None, help="also write the lines to this file (rank 0)")
     args = ap.parse_args()
@@ -78,6 +78,8 @@ def main() -> None:
         variants.append(("ordered_push", 1))
     if "ordered_oneshot" in want:
         variants.append(("ordered_oneshot", 1))
+    if "ordered_ll" in want:
+        variants.append(("ordered_ll", 1))
     for form in ("ordered_hier", "ordered_hier_push"):
         if form in want:
             for k in (4, 2):
@@ -91,8 +93,8 @@ def main() -> None:
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     base = (torch.rand(max_elems, generator=g) * 2e-3 - 1e-3).to(torch.float16).to(dev)
     buf = torch.empty_like(base)
-    # one-shot inboxes up to 8 MB buckets, so the sweep shows the crossover
-    OrderedWire.ONESHOT_MAX_ELEMS = 1 << 22
+    # small-bucket inboxes up to 2 MB buckets, so the sweep shows the crossover
+    OrderedWire.SMALL_CAP_ELEMS = 1 << 20
     ow = OrderedWire(comms[1], max_elems, dev) if any(v[0].startswith("ordered") for v in variants) \
         else None
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -109,7 +111,7 @@ def main() -> None:
             comm = comms[k]
             algo = "ordered" if name.startswith("ordered") else name.split("_")[0]
             nn = n - n % k if algo == "sharded" else n
-            if nn == 0 or (name == "ordered_oneshot" and nn > ow.cap):
+            if nn == 0 or (name in ("ordered_oneshot", "ordered_ll") and nn > ow.cap):
                 continue
             if algo == "ordered":
                 def refill():
@@ -123,7 +125,8 @@ def main() -> None:
                     ow.push = _push
                     sh = int(s0.cuda_stream)
                     op = ow.hier_op(half[0], 0, nn, _k, sh) if _k else \
-                        ow.allreduce_op(half[0], 0, nn, sh, oneshot=name == "ordered_oneshot")
+                        ow.allreduce_op(half[0], 0, nn, sh, small={"ordered_oneshot": "oneshot",
+                                                                   "ordered_ll": "ll"}.get(name, "none"))
                     launch([op])
                     ow.advance(1, sh)
                     half[0] ^= 1

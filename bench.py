@@ -62,6 +62,9 @@ def parse(argv=None):
     ap.add_argument("--loss-scale", type=float, default=1024.0,
                     help="initial loss scale (a non-power-of-two value takes the IEEE-division "
                          "kernels)")
+    ap.add_argument("--wire", default="f16", choices=["f16", "f32"],
+                    help="f32: the reference's own run_experiment path (fp32 gradients fused at "
+                         "4 B/element, mean all-reduce); replicated update only")
     ap.add_argument("--no-grad-norm", action="store_true",
                     help="A/B only: do not compute the grad-norm metric (experiment.py:408-411)")
     return ap.parse_args(argv)
@@ -147,7 +150,10 @@ def workload_config(args, world: int) -> dict:
     k = args.group_size if algo in ("hierarchical", "sharded") and world % args.group_size == 0 \
         else 1
     extra = {} if getattr(args, "loss_scale", 1024.0) == 1024.0 else {"loss_scale": args.loss_scale}
-    return {**extra, "workload": f"{args.model} fused MP-LARS step, fp16 wire, p={world}",
+    if getattr(args, "wire", "f16") != "f16":
+        extra["wire"] = args.wire
+    wire = "fp16" if getattr(args, "wire", "f16") == "f16" else "fp32"
+    return {**extra, "workload": f"{args.model} fused MP-LARS step, {wire} wire, p={world}",
             "model": args.model, "params": sum(sizes), "tensors": len(specs),
             "theta": args.theta, "buckets": nb, "algorithm": algo,
             "topology": f"Topology({world},{k})" if world > 1 else "1 GPU",
@@ -308,8 +314,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     pipe = gs.GradientPipeline(specs, cfg, threshold_bytes=args.theta, comm=comm, eta_bytes=eta,
                                hier_variant=args.algorithm if not flat else "hierarchical",
                                flat_variant="ordered" if args.algorithm == "ordered" else "ring",
-                               sharded_update=args.algorithm.startswith("zero") and world > 1,
+                               sharded_update=(args.algorithm.startswith("zero") and world > 1
+                                               and args.wire == "f16"),
                                fused_collective=args.algorithm == "zero",
+                               wire_dtype=args.wire,
                                init_master=sh.synth_master(specs, seed=0),
                                loss_scale=gs.LossScale(args.loss_scale, policy="fixed" if args.overflow
                                                        else "dynamic"), device=dev,
@@ -318,6 +326,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     if args.overflow and rank == 0:
         wire_np[len(wire_np) // 2] = 0x7C00  # +Inf: every step is skipped
     grads_host = torch.from_numpy(wire_np).pin_memory()
+    if args.wire == "f32":  # the same values as fp32 gradients
+        grads_host = grads_host.view(torch.float16).float().pin_memory()
     grads = grads_host.to(dev)
     if pipe.sharded and pipe.fused_collective:
         # the gradients live in their bucket slots of the raw wire (DDP's
@@ -435,12 +445,14 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     p2_name = "pass2_push" if "pass2_push" in phase_ms else "pass2"
     p2_elems = pipe.owned_elems if pipe.sharded else n_params
     p2_ms_local = statistics.median(phase_ms[p2_name])
-    t = torch.tensor([mean_ms, -20.0 * p2_elems / (p2_ms_local * 1e-3) / 1e9],
+    # pass 2 per element: r g (2 or 4) w 4 v 4, w v 4 w 4 w16 2
+    p2_bpe = 20 if args.wire == "f16" else 22
+    t = torch.tensor([mean_ms, -p2_bpe * p2_elems / (p2_ms_local * 1e-3) / 1e9],
                      dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     mean_ms, achieved = float(t[0]), -float(t[1])
-    pass2_bytes = 20 * p2_elems
+    pass2_bytes = p2_bpe * p2_elems
     pass2_ms = p2_ms_local
 
     # ---- all-reduce bus bandwidth on the whole fp16 gradient (S = 2N bytes)
@@ -468,7 +480,8 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(float(te[0]), 4), "unit": "ms",
-               "h2d_bytes_per_step": 2 * n_params, "d2h_bytes_per_step": 4 + 8}
+               "h2d_bytes_per_step": (2 if args.wire == "f16" else 4) * n_params,
+               "d2h_bytes_per_step": 4 + 8}
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -505,7 +518,10 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
     # and w (4); pass 2 reads g w v (10) and writes v w w16 (10); a pack adds
     # 4 (p = 1 lazy wire and the in-place sharded step: no pack at all)
     packs = world > 1 and not (pipe.sharded and pipe.fused_collective)
-    update_bytes = (26 + (4 if packs or pipe.snapshot_wire else 0)) * n_params
+    # (26 B/elem for fp16 gradients, 30 for the fp32 wire)
+    update_bytes = ((26 if args.wire == "f16" else 30) +
+                    ((4 if args.wire == "f16" else 8) if packs or pipe.snapshot_wire else 0)
+                    ) * n_params
     roofline = {"bound": "hbm",
                 "kernel": "gs_pass2_push" if p2_name == "pass2_push" else "gs_lars_pass2",
                 "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
@@ -522,7 +538,7 @@ def run_ours(args, rank: int, world: int, local: int) -> None:
         "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "wire_dtype": "f16", "data": "synthetic",
+        "dtype": "f32", "wire_dtype": args.wire, "data": "synthetic",
         "config": workload_config(args, world),
         "kernels": (
             "pass1 -> trust -> pass2 (lazy wire: the kernels read the gradients in place; the "

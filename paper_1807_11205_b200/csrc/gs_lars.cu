@@ -80,18 +80,27 @@ struct P1Batch {
   F8 wv[kP1Rounds];
 };
 
-// does the chunk take the register-batched vector path (else p1_chunk)
-template <bool F16>
-__device__ __forceinline__ bool p1_batched(const P1Meta& m) {
+// is the chunk on the 16-byte vector path (the summation order pass 2's
+// carried sum w^2 was formed in)
+__device__ __forceinline__ bool p1_vec_ok(const P1Meta& m) {
   const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
   return m.len <= kThreads * 8 * kP1Rounds &&
          (lars ? p1_vec_path<true>(m.g, m.w) : p1_vec_path<false>(m.g, m.w));
 }
 
-template <bool F16>
+// does the chunk take the register-batched path (else p1_chunk).  fp32
+// gradients (8 registers per vector) and the IEEE-division forms take
+// p1_chunk with 2-vector batches, which keeps them at 3 CTAs/SM instead of
+// 1-2 (same per-thread order, same bits)
+template <bool F16, bool POW2>
+__device__ __forceinline__ bool p1_batched(const P1Meta& m) {
+  return F16 && POW2 && p1_vec_ok(m);
+}
+
+template <bool F16, bool POW2>
 __device__ __forceinline__ void p1_issue(const P1Meta& m, P1Batch<F16>& bt) {
   using Gt = G<F16>;
-  if (!p1_batched<F16>(m)) return;
+  if (!p1_batched<F16, POW2>(m)) return;
   const int nv = m.len / 8, t = threadIdx.x;
   const bool lars = (m.sflags & GS_SEG_LARS_ENABLED) != 0;
   const typename Gt::T* g = static_cast<const typename Gt::T*>(m.g);
@@ -109,8 +118,8 @@ template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, 
 __device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& bt, const Ctx& cx,
                                            Acc& a) {
   using Gt = G<F16>;
-  if (!p1_batched<F16>(m)) {  // misaligned / oversized: the generic loop
-    p1_chunk<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(
+  if (!p1_batched<F16, POW2>(m)) {  // fp32 / IEEE division / misaligned: the generic loop
+    p1_chunk<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2, (F16 && POW2) ? kP1Rounds : 2>(
         static_cast<const typename Gt::T*>(m.g), m.w, m.len, cx, a);
     return;
   }
@@ -142,7 +151,7 @@ __device__ __forceinline__ void p1_consume(const P1Meta& m, const P1Batch<F16>& 
 // (the power-of-two form with per-element finite tests, mul > 1, needs a few
 // more registers than 64: 3 CTAs / SM so it does not spill)
 template <bool F16, bool POW2, bool RAWFLAG>
-constexpr int kP1MinBlocks = !F16 ? 1 : POW2 ? (RAWFLAG ? GS_P1_MINB : 3) : 2;
+constexpr int kP1MinBlocks = (F16 && POW2 && RAWFLAG) ? GS_P1_MINB : 3;
 
 // one chunk's partials: the fixed block tree of gs::block_sum3 over
 // double-buffered scratch (one barrier per chunk)
@@ -178,7 +187,7 @@ __device__ __forceinline__ uint32_t p1_run(const P1Meta& cur, const P1Batch<F16>
   const bool decay = (cx.u.mode & GS_MODE_DECAY) && !(cur.sflags & GS_SEG_DECAY_EXEMPT);
   // the previous pass 2's sum w^2 stands in for this chunk's when it was
   // formed in this very order (pass 2 stores NaN where it was not)
-  const bool cached = lars && !isnan(cur.wc) && p1_batched<F16>(cur);
+  const bool cached = lars && !isnan(cur.wc) && p1_vec_ok(cur);
   if (lars && decay) {
     if (cached)
       p1_consume<F16, POW2, RAWFLAG, GNORM, true, true, false>(cur, bt, cx, a);
@@ -215,7 +224,7 @@ lars_pass1_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restric
   const int i = blockIdx.x;
   const P1Meta m = p1_meta<F16>(segs, chunks, chunk0 + i, wsq);
   P1Batch<F16> bt;
-  p1_issue<F16>(m, bt);
+  p1_issue<F16, POW2>(m, bt);
   Acc a;
   bool cached;
   flag_acc |= p1_run<F16, POW2, RAWFLAG, GNORM>(m, bt, cx, cached, a);
@@ -310,7 +319,7 @@ __device__ __forceinline__ void p2_chunk(const typename G<F16>::T* __restrict__ 
 // forward, so the first chunks pass 2 needs are the ones still in L2
 // (ResNet-50: 84.0 -> 81.2 us, profiles/r02a)
 template <bool F16, bool POW2>
-__global__ void __launch_bounds__(kThreads, F16 && POW2 ? 4 : POW2 ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, F16 && POW2 ? 4 : (F16 || POW2) ? 3 : 2)
 lars_pass2_kernel(const gs_segment* __restrict__ segs, const gs_chunk* __restrict__ chunks,
                   int chunk0, const gs_step_params params, const float* __restrict__ seg_scale,
                   const gs_ctl* __restrict__ ctl, uint32_t parity, uint32_t flag_mask,

@@ -160,7 +160,10 @@ __device__ __forceinline__ bool p1_vec_path(const void* g, const float* w) {
   return gs::is_aligned16(g) && (!LARS || gs::is_aligned16(w));
 }
 
-template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2 = true>
+// R: vectors per thread per load batch (any R gives the same per-thread
+// order, hence the same bits)
+template <bool F16, bool POW2, bool RAWFLAG, bool GNORM, bool LARS, bool DECAY, bool W2 = true,
+          int R = kP1Rounds>
 __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ g,
                                          const float* __restrict__ w, int len, const Ctx& cx,
                                          Acc& a) {
@@ -173,19 +176,19 @@ __device__ __forceinline__ void p1_chunk(const typename G<F16>::T* __restrict__ 
   // batch (4 x 16 B of g, 4 x 32 B of w) before any arithmetic; each thread
   // still visits its vectors t, t+256, t+512, ... in increasing order, so
   // the batching never changes the summation order
-  constexpr int kBatch = kP1Rounds * kThreads;
+  constexpr int kBatch = R * kThreads;
   int done = 0;
   for (; done + kBatch <= nv; done += kBatch) {
-    typename Gt::V gv[kP1Rounds];
-    F8 wv[kP1Rounds];
+    typename Gt::V gv[R];
+    F8 wv[R];
 #pragma unroll
-    for (int k = 0; k < kP1Rounds; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
+    for (int k = 0; k < R; ++k) gv[k] = Gt::ld(g + 8 * (done + t + k * kThreads));
     if (kW) {
 #pragma unroll
-      for (int k = 0; k < kP1Rounds; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
+      for (int k = 0; k < R; ++k) wv[k] = ldw(w + 8 * (done + t + k * kThreads));
     }
 #pragma unroll
-    for (int k = 0; k < kP1Rounds; ++k)
+    for (int k = 0; k < R; ++k)
       p1_vec<F16, POW2, RAWFLAG, GNORM, LARS, DECAY, W2>(gv[k], kW ? wv[k] : F8{}, cx, a);
   }
   for (int i = done + t; i < nv; i += kThreads) {

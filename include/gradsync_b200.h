@@ -141,7 +141,8 @@ typedef struct gs_rank_ctx {
                                    raw wires the fold reads) */
   const double* partials;       /* gs_trust_fence: this rank's chunk partials */
   double* seg_out;              /* gs_trust_fence: per-segment norms / rates */
-} gs_rank_ctx; /* 112 bytes */
+  uint32_t* seg_ready;          /* gs_zero_update: per-segment "scale published" epochs */
+} gs_rank_ctx; /* 120 bytes */
 
 /* One rank's buffers for the native step executor (gs_step_*): a HOST
  * struct (the executor reads it on the host and launches from it). */
@@ -365,6 +366,16 @@ int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* 
                    uint32_t epoch, int nseg, int nchunk, gs_step_params params, uint32_t parity,
                    void* stream);
 
+/* gs_trust_fence and gs_pass2_push in ONE launch (the whole second half of
+ * the sharded step): fence CTAs, then trust CTAs (each publishes its
+ * segment's epoch in ctx.seg_ready[s] after the scale), then pass-2 CTAs
+ * (max_chunks per rank) that wait for their chunk's segment.  Every wait is
+ * on CTAs earlier in the grid, so it cannot deadlock.  Same bits. */
+int gs_zero_update(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   const uint64_t* peer_working, uint32_t epoch, int nseg, int nchunk, int b0,
+                   int b1, int max_chunks, gs_step_params params, uint32_t hint, uint32_t parity,
+                   uint32_t flag_mask, void* stream);
+
 /* ---- native step executor (gs_step.cu) ---------------------------------
  * One call launches a whole step — the same kernels, in the same order, as
  * the pipeline's per-kernel path, without per-kernel host work. */
@@ -376,9 +387,9 @@ int gs_step_replicated(const gs_step_rank* rank, int g_is_f16, gs_step_params pa
 
 /* The sharded (ZeRO-1) step in fused kernels for `nranks` ranks (1 on a box,
  * p when emulated; ranks = host array, ctx = device gs_rank_ctx table):
- * [pack per rank] -> gs_rs_pass1 -> gs_trust_fence (fence + trust) ->
- * gs_pass2_push -> gs_peer_fence (which adds 4 to every rank's epoch
- * base).  Epochs
+ * [pack per rank] -> gs_rs_pass1 -> gs_zero_update (fence + trust +
+ * pass 2 with the working-weight push) -> gs_peer_fence (which adds 4 to
+ * every rank's epoch base).  Epochs
  * 1, 2, 3 of the step; max_own >= every rank's owned chunk count. */
 int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, int p,
                  const uint64_t* wires, const uint64_t* sig, const uint64_t* peer_partials,

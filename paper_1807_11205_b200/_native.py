@@ -57,7 +57,7 @@ RANK_CTX_DTYPE = np.dtype([
     ("rank", "<i4"), ("reserved", "<i4"), ("timeout_ns", "<u8"), ("status", "<u8"),
     ("epoch_base", "<u8"), ("segs", "<u8"), ("chunks", "<u8"), ("own_list", "<u8"),
     ("own_off", "<u8"), ("ctl", "<u8"), ("seg_scale", "<u8"), ("nonfinite", "<u8"),
-    ("red", "<u8"), ("partials", "<u8"), ("seg_out", "<u8"),
+    ("red", "<u8"), ("partials", "<u8"), ("seg_out", "<u8"), ("seg_ready", "<u8"),
 ])
 STEP_RANK_DTYPE = np.dtype([
     ("pack", "<u8"), ("npack", "<i4"), ("nseg", "<i4"), ("segs", "<u8"), ("chunks", "<u8"),
@@ -68,7 +68,7 @@ STEP_RANK_DTYPE = np.dtype([
 assert STEP_RANK_DTYPE.itemsize == 96
 assert SEGMENT_DTYPE.itemsize == 64
 assert CTL_DTYPE.itemsize == 48
-assert RANK_CTX_DTYPE.itemsize == 112
+assert RANK_CTX_DTYPE.itemsize == 120
 assert CHUNK_DTYPE.itemsize == 16
 assert COPY_DTYPE.itemsize == 24
 assert STEP_PARAMS_DTYPE.itemsize == 56
@@ -132,6 +132,9 @@ SIGNATURES = {
                             c_void_p]),
     "gs_pass2_push": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int, StepParams,
                               c_uint32, c_uint32, c_uint32, c_void_p]),
+    "gs_zero_update": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_uint32, c_int, c_int,
+                               c_int, c_int, c_int, StepParams, c_uint32, c_uint32, c_uint32,
+                               c_void_p]),
     "gs_trust_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_int, c_int,
                                StepParams, c_uint32, c_void_p]),
     "gs_peer_fence": (c_int, [c_void_p, c_int, c_int, c_void_p, c_uint32, c_uint32, c_void_p]),

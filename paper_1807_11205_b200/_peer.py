@@ -43,7 +43,7 @@ def decode_status(status: int) -> str:
 def rank_ctx(rank: int, *, timeout_s: float = 120.0, status: int = 0, epoch_base: int = 0,
              segs: int = 0, chunks: int = 0, own_list: int = 0, own_off: int = 0, ctl: int = 0,
              seg_scale: int = 0, nonfinite: int = 0, red: int = 0, partials: int = 0,
-             seg_out: int = 0) -> np.ndarray:
+             seg_out: int = 0, seg_ready: int = 0) -> np.ndarray:
     """One gs_rank_ctx record (addresses as ints; 0 = NULL)."""
     r = np.zeros(1, dtype=_native.RANK_CTX_DTYPE)
     r["rank"] = rank
@@ -51,7 +51,7 @@ def rank_ctx(rank: int, *, timeout_s: float = 120.0, status: int = 0, epoch_base
     r["status"], r["epoch_base"], r["segs"], r["chunks"] = status, epoch_base, segs, chunks
     r["own_list"], r["own_off"], r["ctl"], r["seg_scale"] = own_list, own_off, ctl, seg_scale
     r["nonfinite"], r["red"] = nonfinite, red
-    r["partials"], r["seg_out"] = partials, seg_out
+    r["partials"], r["seg_out"], r["seg_ready"] = partials, seg_out, seg_ready
     return r
 
 

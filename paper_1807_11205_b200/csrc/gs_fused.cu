@@ -235,6 +235,34 @@ __device__ __forceinline__ void p2_push_chunk(const uint16_t* __restrict__ g, fl
   }
 }
 
+// wait (one thread) until *w == epoch: a gpu-scope acquire, bounded like
+// every peer wait (gives up when the rank's status records a failure or
+// after the rank's timeout)
+__device__ __forceinline__ void wait_epoch(const uint32_t* w, uint32_t epoch, const gs_rank_ctx& R) {
+  uint32_t v, spins = 0;
+  const uint64_t t0 = globaltimer_ns();
+  const uint64_t limit = R.timeout_ns ? R.timeout_ns : kPeerTimeoutNs;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+    if (v == epoch) break;
+    if ((++spins & 63u) == 0) {
+      if (R.status != nullptr && *reinterpret_cast<volatile uint32_t*>(R.status) != 0u) break;
+      if (globaltimer_ns() - t0 > limit) break;
+    }
+  }
+}
+
+template <bool POW2>
+__device__ __forceinline__ void pass2_push_cta(const PeerCta& pc, const uint64_t* __restrict__ peer_working,
+                                               int p, int b0, int b1, const gs_step_params& params,
+                                               uint32_t parity, uint32_t flag_mask,
+                                               uint32_t ready_epoch);
+__device__ __forceinline__ void trust_fence_cta(const gs_rank_ctx* __restrict__ ranks, int nranks,
+                                                const uint64_t* __restrict__ sig, int p,
+                                                uint32_t epoch, int nseg, int nchunk,
+                                                const gs_step_params& params, uint32_t parity,
+                                                int b, bool publish);
+
 // one CTA per owned chunk (grid = nranks x max owned count; a rank's surplus
 // CTAs exit), visited in reverse of rs_pass1's order: the chunks rs_pass1
 // folded last are still in L2
@@ -245,13 +273,51 @@ pass2_push_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t*
                   uint32_t flag_mask) {
   gs::griddep_wait();  // the trust kernel's scales (PDL launch)
   const PeerCta pc = peer_cta(ranks, nb);
+  pass2_push_cta<POW2>(pc, peer_working, p, b0, b1, params, parity, flag_mask, 0u);
+}
+
+// the fence CTAs, the trust CTAs and the pass-2 CTAs of the sharded step in
+// one grid (gs_zero_update); a pass-2 CTA waits for its segment's epoch in
+// seg_ready, which its trust CTA publishes after the scale
+template <bool POW2>
+__global__ void __launch_bounds__(kThreads, POW2 ? 4 : 2)
+zero_update_kernel(const gs_rank_ctx* __restrict__ ranks, int nranks, const uint64_t* __restrict__ sig,
+                   const uint64_t* __restrict__ peer_working, int p, uint32_t epoch, int nseg,
+                   int nchunk, int b0, int b1, int max_chunks, const gs_step_params params,
+                   uint32_t parity, uint32_t flag_mask) {
+  const int nfence = nranks, ntrust = nranks * (nseg + 1);
+  const int b = blockIdx.x;
+  if (b < nfence + ntrust) {
+    trust_fence_cta(ranks, nranks, sig, p, epoch, nseg, nchunk, params, parity, b, true);
+    return;
+  }
+  const int b2 = b - nfence - ntrust;
+  PeerCta pc;
+  pc.R = ranks + b2 / max_chunks;
+  pc.lb = b2 % max_chunks;
+  pc.nb = max_chunks;
+  const uint32_t ep = epoch + (pc.R->epoch_base != nullptr ? *pc.R->epoch_base : 0u);
+  pass2_push_cta<POW2>(pc, peer_working, p, b0, b1, params, parity, flag_mask, ep);
+}
+
+// the work of one pass2_push CTA; ready_epoch != 0: first wait until the
+// chunk's segment has published its scale (gs_zero_update)
+template <bool POW2>
+__device__ __forceinline__ void pass2_push_cta(const PeerCta& pc, const uint64_t* __restrict__ peer_working,
+                                               int p, int b0, int b1, const gs_step_params& params,
+                                               uint32_t parity, uint32_t flag_mask,
+                                               uint32_t ready_epoch) {
   const gs_rank_ctx& R = *pc.R;
-  if (R.ctl->flags[parity] & flag_mask) return;  // lars.py:161-163
   int i0, i1;
   own_range(R, b0, b1, i0, i1);
   if (pc.lb >= i1 - i0) return;
   const int c = R.own_list[i1 - 1 - pc.lb];
   const gs_chunk ch = R.chunks[c];
+  if (ready_epoch != 0u) {
+    if (threadIdx.x == 0) wait_epoch(&R.seg_ready[ch.seg], ready_epoch, R);
+    __syncthreads();
+  }
+  if (R.ctl->flags[parity] & flag_mask) return;  // lars.py:161-163
   const gs_segment* sp = R.segs + ch.seg;
   const uint32_t sflags = sp->flags;
   Ctx cx;
@@ -279,14 +345,14 @@ pass2_push_kernel(const gs_rank_ctx* __restrict__ ranks, int nb, const uint64_t*
 // trust CTA s of rank r, which waits for its rank's word.  The fence CTAs
 // come first in the grid, so they are dispatched before any waiting trust
 // CTA and the launch cannot deadlock even when it does not fit at once.
-__global__ void __launch_bounds__(kThreads)
-trust_fence_kernel(const gs_rank_ctx* __restrict__ ranks, int nranks, const uint64_t* __restrict__ sig,
-                   int p, uint32_t epoch, int nseg, int nchunk, const gs_step_params params,
-                   uint32_t parity) {
-  gs::griddep_launch_dependents();  // pass 2 (PDL) may start issuing its loads
-  if ((int)blockIdx.x < nranks) {
+__device__ __forceinline__ void trust_fence_cta(const gs_rank_ctx* __restrict__ ranks, int nranks,
+                                                const uint64_t* __restrict__ sig, int p,
+                                                uint32_t epoch, int nseg, int nchunk,
+                                                const gs_step_params& params, uint32_t parity,
+                                                int b, bool publish) {
+  if (b < nranks) {
     PeerCta pc;
-    pc.R = ranks + blockIdx.x;
+    pc.R = ranks + b;
     pc.lb = 0;
     pc.nb = 1;
     if (pc.R->epoch_base != nullptr) epoch += *pc.R->epoch_base;
@@ -297,29 +363,27 @@ trust_fence_kernel(const gs_rank_ctx* __restrict__ ranks, int nranks, const uint
                    : "memory");
     return;
   }
-  const int b = blockIdx.x - nranks;
+  b -= nranks;
   const gs_rank_ctx& R = ranks[b / (nseg + 1)];
   const int s = b % (nseg + 1);
   if (R.epoch_base != nullptr) epoch += *R.epoch_base;
-  if (threadIdx.x == 0) {
-    const uint32_t* w = &R.ctl->counter[0];
-    uint32_t v;
-    uint32_t spins = 0;
-    const uint64_t t0 = globaltimer_ns();
-    const uint64_t limit = R.timeout_ns ? R.timeout_ns : kPeerTimeoutNs;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
-      if (v == epoch) break;
-      if ((++spins & 63u) == 0) {
-        // the fence CTA gave up (its wait timed out and recorded a status)
-        if (R.status != nullptr && *reinterpret_cast<volatile uint32_t*>(R.status) != 0u) break;
-        if (globaltimer_ns() - t0 > limit) break;
-      }
-    }
-  }
+  if (threadIdx.x == 0) wait_epoch(&R.ctl->counter[0], epoch, R);
   __syncthreads();
   trust_cta(R.segs, s, nseg, nchunk, R.partials, params, const_cast<float*>(R.seg_scale),
             R.seg_out, R.ctl, parity, nullptr, 0);
+  if (publish && s < nseg && threadIdx.x == 0) {
+    // thread 0 wrote the scale: publish the segment (release, gpu scope)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&R.seg_ready[s]), "r"(epoch)
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+trust_fence_kernel(const gs_rank_ctx* __restrict__ ranks, int nranks, const uint64_t* __restrict__ sig,
+                   int p, uint32_t epoch, int nseg, int nchunk, const gs_step_params params,
+                   uint32_t parity) {
+  gs::griddep_launch_dependents();  // pass 2 (PDL) may start issuing its loads
+  trust_fence_cta(ranks, nranks, sig, p, epoch, nseg, nchunk, params, parity, blockIdx.x, false);
 }
 
 __global__ void peer_fence_kernel(const gs_rank_ctx* __restrict__ ranks, const uint64_t* __restrict__ sig,
@@ -411,6 +475,29 @@ int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* 
   trust_fence_kernel<<<nranks * (nseg + 2), kThreads, 0, (cudaStream_t)stream>>>(
       ranks, nranks, sig, p, epoch, nseg, nchunk, params, parity);
   return gs_check_launch("gs_trust_fence");
+}
+
+int gs_zero_update(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   const uint64_t* peer_working, uint32_t epoch, int nseg, int nchunk, int b0,
+                   int b1, int max_chunks, gs_step_params params, uint32_t hint, uint32_t parity,
+                   uint32_t flag_mask, void* stream) {
+  GS_REQUIRE(p >= 1 && p <= 32 && nranks >= 1 && nranks <= p && nseg >= 0 && nchunk >= 0 &&
+                 parity <= 1 && b0 >= 0 && b1 >= b0 && max_chunks >= 0,
+             "gs_zero_update: bad arguments");
+  GS_REQUIRE(ranks && sig && peer_working, "gs_zero_update: null pointer");
+  GS_REQUIRE(epoch != 0, "gs_zero_update: epoch 0 is the reset value");
+  const int mc = max_chunks > 0 ? max_chunks : 1;
+  const dim3 grid(nranks * (nseg + 2) + nranks * mc);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (hint & GS_HINT_POW2)
+    zero_update_kernel<true><<<grid, kThreads, 0, s>>>(ranks, nranks, sig, peer_working, p, epoch,
+                                                        nseg, nchunk, b0, b1, mc, params, parity,
+                                                        flag_mask);
+  else
+    zero_update_kernel<false><<<grid, kThreads, 0, s>>>(ranks, nranks, sig, peer_working, p,
+                                                         epoch, nseg, nchunk, b0, b1, mc, params,
+                                                         parity, flag_mask);
+  return gs_check_launch("gs_zero_update");
 }
 
 int gs_peer_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig, uint32_t epoch,

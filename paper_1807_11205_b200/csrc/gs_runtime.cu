@@ -12,7 +12,7 @@ static_assert(sizeof(gs_chunk) == 16, "gs_chunk layout");
 static_assert(sizeof(gs_copy) == 24, "gs_copy layout");
 static_assert(sizeof(gs_step_params) == 56, "gs_step_params layout");
 static_assert(sizeof(gs_ctl) == 48, "gs_ctl layout");
-static_assert(sizeof(gs_rank_ctx) == 112, "gs_rank_ctx layout");
+static_assert(sizeof(gs_rank_ctx) == 120, "gs_rank_ctx layout");
 static_assert(sizeof(gs_step_rank) == 96, "gs_step_rank layout");
 
 static thread_local char g_err[512] = "";

@@ -38,6 +38,10 @@ int gs_counter_add(uint32_t* counter, uint32_t inc, void* stream);
 int gs_trust_fence(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
                    uint32_t epoch, int nseg, int nchunk, gs_step_params params, uint32_t parity,
                    void* stream);
+int gs_zero_update(const gs_rank_ctx* ranks, int nranks, int p, const uint64_t* sig,
+                   const uint64_t* peer_working, uint32_t epoch, int nseg, int nchunk, int b0,
+                   int b1, int max_chunks, gs_step_params params, uint32_t hint, uint32_t parity,
+                   uint32_t flag_mask, void* stream);
 
 #define GS_TRY(call)          \
   do {                        \
@@ -69,10 +73,9 @@ int gs_step_zero(const gs_step_rank* ranks, int nranks, const gs_rank_ctx* ctx, 
     if (ranks[i].npack > 0) GS_TRY(gs_batched_copy(ranks[i].pack, ranks[i].npack, stream));
   GS_TRY(gs_rs_pass1(ctx, nranks, p, wires, sig, peer_partials, peer_ctl, 0, nbuckets, params,
                      hint, parity, 1, nblocks, stream));
-  GS_TRY(gs_trust_fence(ctx, nranks, p, sig, 2, ranks[0].nseg, ranks[0].nchunk, params, parity,
-                        stream));
-  GS_TRY(gs_pass2_push(ctx, nranks, p, peer_working, 0, nbuckets, max_own, params, hint, parity,
-                       flag_mask, stream));
+  // fence + trust + pass 2 with the working-weight push: one launch
+  GS_TRY(gs_zero_update(ctx, nranks, p, sig, peer_working, 2, ranks[0].nseg, ranks[0].nchunk, 0,
+                        nbuckets, max_own, params, hint, parity, flag_mask, stream));
   // the closing fence also advances every rank's epoch base by the step's 4
   GS_TRY(gs_peer_fence(ctx, nranks, p, sig, 3, 4, stream));
   return GS_OK;

@@ -399,12 +399,15 @@ class GradientPipeline:
         #: elements this rank updates (pass 2) per step
         self.owned_elems = int(clen[own_list].sum()) if own_list else 0
         plan, a = self.plan, self.arena
+        # per-segment "scale published" epochs of gs_zero_update
+        self._seg_ready = torch.zeros(max(1, plan.nseg), dtype=torch.int32, device=d)
         self._ctx = rank_ctx(r, timeout_s=self.comm.timeout_s, status=dev.ptr(plan.ctl) + 16,
                              epoch_base=dev.ptr(self.epoch_base), segs=dev.ptr(plan.base_segs),
                              chunks=dev.ptr(plan.d_chunks), own_list=dev.ptr(self._own_list),
                              own_off=dev.ptr(self._own_off), ctl=dev.ptr(plan.ctl),
                              seg_scale=dev.ptr(plan.seg_scale), red=dev.ptr(self.red),
-                             partials=dev.ptr(plan.partials), seg_out=dev.ptr(plan.seg_out))
+                             partials=dev.ptr(plan.partials), seg_out=dev.ptr(plan.seg_out),
+                             seg_ready=dev.ptr(self._seg_ready))
         # this rank's one-entry context table for the native executor
         self._ctx_dev = dev.upload(self._ctx, d)
 
@@ -472,14 +475,12 @@ class GradientPipeline:
                            dev.ptr(a.peers("partials")), dev.ptr(a.peers("ctl")), 0, nb,
                            plan.sp, plan.hint, plan.parity, 1, self._nblocks, sh)
             if timer:
-                timer("fence_trust")
-            # the peer fence and the trust kernel in one launch
-            yield self._op("gs_trust_fence", p, sig, 2, plan.nseg, plan.nchunk, plan.sp,
-                           plan.parity, sh)
-            if timer:
-                timer("pass2_push")
-            yield self._op("gs_pass2_push", p, dev.ptr(a.peers("working")), 0, nb, None, plan.sp,
-                           plan.hint, plan.parity, _MASK, sh, count=self._n_own)
+                timer("update")
+            # the peer fence, the trust kernel and pass 2 with the working-
+            # weight push in one launch
+            yield self._op("gs_zero_update", p, sig, dev.ptr(a.peers("working")), 2, plan.nseg,
+                           plan.nchunk, 0, nb, None, plan.sp, plan.hint, plan.parity, _MASK, sh,
+                           count=self._n_own)
             if timer:
                 timer("fence_end")
             # the closing fence also advances the epoch base for the next step

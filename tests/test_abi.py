@@ -61,7 +61,7 @@ def test_struct_layouts_match_header():
                            (_native.COPY_DTYPE, "gs_copy", 24),
                            (_native.STEP_PARAMS_DTYPE, "gs_step_params", 56),
                            (_native.CTL_DTYPE, "gs_ctl", 48),
-                           (_native.RANK_CTX_DTYPE, "gs_rank_ctx", 112)):
+                           (_native.RANK_CTX_DTYPE, "gs_rank_ctx", 120)):
         assert dt.itemsize == size
         assert re.search(rf"}}\s*{name};\s*/\*\s*{size} bytes", text), name
     m = {k: int(v, 0) for k, v in re.findall(r"#define (GS_[A-Z0-9_]+) (\d+|0x[0-9a-f]+)u?", text)}

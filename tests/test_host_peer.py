@@ -13,13 +13,13 @@ from paper_1807_11205_b200._peer import PeerOp, decode_status, rank_ctx
 def test_rank_ctx_record_layout():
     r = rank_ctx(3, timeout_s=2.5, status=0x1000, epoch_base=0x2000, segs=0x3000, chunks=0x4000,
                  own_list=0x5000, own_off=0x6000, ctl=0x7000, seg_scale=0x8000, nonfinite=0x9000,
-                 red=0xA000, partials=0xB000, seg_out=0xC000)
-    assert r.dtype == _native.RANK_CTX_DTYPE and r.nbytes == 112
+                 red=0xA000, partials=0xB000, seg_out=0xC000, seg_ready=0xD000)
+    assert r.dtype == _native.RANK_CTX_DTYPE and r.nbytes == 120
     raw = np.frombuffer(r.tobytes(), dtype="<u8")
     assert int(r["rank"][0]) == 3 and int(r["timeout_ns"][0]) == 2_500_000_000
     # every pointer at its C offset (gradsync_b200.h gs_rank_ctx)
     assert list(raw[2:]) == [0x1000, 0x2000, 0x3000, 0x4000, 0x5000, 0x6000, 0x7000, 0x8000,
-                             0x9000, 0xA000, 0xB000, 0xC000]
+                             0x9000, 0xA000, 0xB000, 0xC000, 0xD000]
 
 
 def test_status_word_diagnosis():

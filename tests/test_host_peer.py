@@ -63,3 +63,25 @@ def test_batched_launch_requires_identical_arguments(monkeypatch):
            PeerOp("gs_peer_fence", rank_ctx(1), (2, 0, 2, 0, 0))]
     with pytest.raises(RuntimeError, match="ranks diverged"):
         _peer.launch(ops)
+
+
+def test_small_bucket_rule():
+    """OrderedWire's size rule (host only): whole-vector buckets up to
+    LL_MAX_ELEMS take the LL kernel, other buckets up to ONESHOT_MAX_ELEMS the
+    one-shot kernel, the rest the pull / push kernel; nothing without an
+    inbox (fp32 wire)."""
+    from types import SimpleNamespace
+
+    from paper_1807_11205_b200.dist import OrderedWire
+
+    rule = OrderedWire.small_form
+    w = SimpleNamespace(cap=OrderedWire.oneshot_cap(1 << 20, 2))
+    assert w.cap == OrderedWire.SMALL_CAP_ELEMS
+    assert rule(w, 0, 8) == "ll" and rule(w, 256, OrderedWire.LL_MAX_ELEMS) == "ll"
+    assert rule(w, 0, 7) == "oneshot" and rule(w, 3, 16) == "oneshot"
+    assert rule(w, 0, OrderedWire.ONESHOT_MAX_ELEMS + 8) == "ll"
+    assert rule(w, 0, OrderedWire.ONESHOT_MAX_ELEMS + 3) == "none"
+    assert rule(w, 0, OrderedWire.LL_MAX_ELEMS + 8) == "none"
+    assert rule(w, 0, 0) == "none"
+    assert OrderedWire.oneshot_cap(1 << 20, 4) == 0
+    assert rule(SimpleNamespace(cap=0), 0, 8) == "none"

@@ -7,7 +7,7 @@ each emulated rank owns a full arena (wire halves, masters, velocities,
 partials, control block, signal area) in this device's memory, every rank's
 peer tables point at the other ranks' arenas, and each peer-synchronised
 launch (the ordered all-reduce, reduce-scatter / all-gather, gs_rs_pass1,
-gs_pass2_push, gs_peer_fence) is issued ONCE for all p ranks over a
+gs_zero_update, gs_peer_fence) is issued ONCE for all p ranks over a
 gs_rank_ctx table (CTA b serves rank b / nb), so every rank's CTAs are
 co-resident and the cross-rank waits resolve inside one kernel — on one
 stream, deterministically, and under ncu's kernel serialisation too.

@@ -166,7 +166,7 @@ class GradientPipeline:
       sharded_update: ZeRO-1 step: each rank folds and updates only its
         chunks of every bucket (masters / velocities sharded, working copy
         replicated); fused_collective selects the fused kernels
-        (gs_rs_pass1 / gs_pass2_push) over separate collectives.
+        (gs_rs_pass1 / gs_zero_update) over separate collectives.
       init_master: flat fp32 initial weights in registration order.
       grad_norm: compute the experiment's grad-norm metric.
       local_workers: with comm=None, simulate p workers on this GPU the way
@@ -454,7 +454,7 @@ class GradientPipeline:
         """The ZeRO-1 step.  Fused: [pack] -> gs_rs_pass1 over the rank's
         owned chunks of every bucket (fold from the peers' raw wires into the
         reduced wire + pass 1, partials and flags pushed to every peer) ->
-        fence -> trust -> gs_pass2_push (pass 2 + working-weight push) ->
+        gs_zero_update (fence, trust, pass 2 + working-weight push) ->
         fence.  Separate collectives: pack -> per bucket reduce-scatter +
         pass 1 -> all-gather of the partials -> trust -> pass 2 -> all-gather
         of the working weights."""
@@ -1117,10 +1117,10 @@ class GradientPipeline:
         if self.sharded:
             p, a = self.comm.topo.p, self.arena
             sig = dev.ptr(a.peers("sig"))
-            yield self._op("gs_trust_fence", p, sig, nb + 1, plan.nseg, plan.nchunk, plan.sp,
-                           plan.parity, sh)
-            yield self._op("gs_pass2_push", p, dev.ptr(a.peers("working")), 0, nb, None, plan.sp,
-                           plan.hint, plan.parity, _MASK, sh, count=self._n_own)
+            # fence + trust + pass 2 with the working-weight push, one launch
+            yield self._op("gs_zero_update", p, sig, dev.ptr(a.peers("working")), nb + 1,
+                           plan.nseg, plan.nchunk, 0, nb, None, plan.sp, plan.hint, plan.parity,
+                           _MASK, sh, count=self._n_own)
             yield self._op("gs_peer_fence", p, sig, nb + 2, nb + 3, sh)
             self._last_wire = self.red
         else:

@@ -247,7 +247,7 @@ def run_emulated(p, model="shufflenet_v2_x0_5", theta=256 << 10, steps=3, inject
 
 @pytest.mark.parametrize("p,executor", [(2, True), (4, True), (8, True), (2, False), (8, False)])
 def test_sharded_fused_step_bit_exact(p, executor):
-    """gs_rs_pass1 + trust + gs_pass2_push + gs_peer_fence (ZeRO-1 step),
+    """gs_rs_pass1 + gs_zero_update + gs_peer_fence (ZeRO-1 step),
     shufflenet shapes, theta = 256 KiB, 3 steps, +Inf on the last rank at
     step 2 (skipped everywhere, loss scale halved) — through the native
     executor (gs_step_zero, all ranks in one call) and through the

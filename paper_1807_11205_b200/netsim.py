@@ -309,3 +309,13 @@ def calibrated_eta(p: int, k: int, link: LinkModel, sizes_bytes=None, itemsize: 
     if x is None:
         return float("inf"), rows
     return (0 if x == rows[0]["bytes"] else x), rows
+
+
+def eta_from_sweep(path, p: int, k: int, itemsize: int = 2):
+    """The hybrid threshold η for Topology(p, k) seeded from a measured
+    all-reduce sweep file (`tools/allreduce_sweep.py` JSONL): calibrate the
+    link model on the file's flat-ring (and literal-hierarchy) rows, then
+    `calibrated_eta`.  Returns bytes (int), or float("inf")."""
+    link = calibrate_from_sweep(load_sweep(path), p, k, itemsize=itemsize)
+    eta, _ = calibrated_eta(p, k, link, itemsize=itemsize)
+    return eta

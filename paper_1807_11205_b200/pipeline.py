@@ -34,6 +34,8 @@ lockstep on one device and launches each op once for all of them.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -93,6 +95,19 @@ class StepResult:
     grad_norm: float           # experiment.py:408-411 (0.0 when not applied)
     flags: int
     algorithms: list = field(default_factory=list)
+
+
+def resolve_eta(eta_bytes, topo=None, itemsize: int = 2):
+    """The pipeline's hybrid threshold: an int (bytes), float("inf") (every
+    bucket hierarchical, the reference's config 1) or the path of a measured
+    sweep file (`tools/allreduce_sweep.py` JSONL), from which netsim seeds η
+    for `topo` (netsim.eta_from_sweep)."""
+    if isinstance(eta_bytes, (str, os.PathLike)):
+        if topo is None:
+            raise ValueError("eta_bytes from a sweep file needs a Communicator (p > 1)")
+        from .netsim import eta_from_sweep
+        eta_bytes = eta_from_sweep(eta_bytes, topo.p, topo.k, itemsize)
+    return eta_bytes if eta_bytes == float("inf") else int(eta_bytes)
 
 
 def _roundup(n: int, a: int) -> int:
@@ -156,7 +171,9 @@ class GradientPipeline:
         i.e. reversed registration).
       comm: dist.Communicator (or emulation.LocalComm) for p > 1; None = a
         single worker, no collective.
-      eta_bytes: hybrid threshold (collectives.py:238-244) on fp16 bucket bytes.
+      eta_bytes: hybrid threshold (collectives.py:238-244) on fp16 bucket bytes;
+        float("inf") = every bucket hierarchical; a path = seed it from a
+        measured sweep file through the netsim model (resolve_eta).
       hier_variant: variant for hierarchical buckets: "hierarchical" = the
         literal master path over NCCL, "sharded" = RS/AR/AG over NCCL,
         "ordered_hier" = own bit-exact two-level kernel (power-of-two k).
@@ -205,9 +222,8 @@ class GradientPipeline:
         self.p = comm.topo.p if comm is not None else int(local_workers)
         self.local = comm is None and self.p > 1
         self.emulated = bool(getattr(comm, "emulated", False))
-        # eta = inf (every bucket hierarchical, the reference's config 1 and
-        # netsim.calibrated_eta when ring never wins) is kept as a float
-        self.eta_bytes = eta_bytes if eta_bytes == float("inf") else int(eta_bytes)
+        self.eta_bytes = resolve_eta(eta_bytes, comm.topo if comm is not None else None,
+                                     2 if wire_dtype == "f16" else 4)
         self.hier_variant = hier_variant
         self.grad_norm_enabled = grad_norm
         self.device = device or dev.require_cuda()

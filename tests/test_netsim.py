@@ -213,3 +213,17 @@ def test_calibration_flat_only_sweep_and_eta_edges():
     eta, sweep = calibrated_eta(64, 8, LinkModel(alpha=1e-5, beta_inv=1e9),
                                 [4 * 10**i for i in range(8)], itemsize=4)
     assert 0 < eta < float("inf") and eta == find_crossover(sweep)
+
+
+def test_eta_from_sweep_file_seeds_the_pipeline_threshold():
+    """GradientPipeline(eta_bytes=<sweep file>) resolves through netsim: the
+    4-GPU B200 sweep gives eta = 0 (flat ring for every bucket)."""
+    from paper_1807_11205_b200 import collectives, netsim
+    from paper_1807_11205_b200.pipeline import resolve_eta
+
+    path = ROOT / "profiles" / "final_n4" / "sweep_fin_n4.jsonl"
+    assert netsim.eta_from_sweep(path, 4, 2) == 0
+    assert resolve_eta(str(path), collectives.Topology(4, 2)) == 0
+    assert resolve_eta(float("inf")) == float("inf") and resolve_eta(4096.0) == 4096
+    with pytest.raises(ValueError, match="needs a Communicator"):
+        resolve_eta(str(path), None)

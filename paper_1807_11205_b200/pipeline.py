@@ -332,6 +332,9 @@ class GradientPipeline:
         self._inc = None
         real_comm = comm is not None and not self.emulated
         self._pack_stream = torch.cuda.Stream(device=d) if real_comm else None
+        # replicated update at p > 1: pass 1 of bucket b runs on its own
+        # stream so it overlaps the all-reduce of bucket b + 1
+        self._p1_stream = torch.cuda.Stream(device=d) if real_comm else None
         # the incremental API's side stream (bucket work under backward);
         # emulated ranks keep one stream so their peer launches batch
         self._side_stream = torch.cuda.Stream(device=d) if not self.emulated else None
@@ -893,6 +896,10 @@ class GradientPipeline:
                         ev = torch.cuda.Event()
                         ev.record(ps)
                         works.append(ev)
+            p1s = self._p1_stream if self._p1_stream is not None and not timer else s0
+            if p1s is not s0:
+                p1s.wait_stream(s0)
+            sh1 = int(p1s.cuda_stream)
             for b, bk in enumerate(self.buckets):
                 w = works[b]
                 if isinstance(w, torch.cuda.Event):
@@ -905,7 +912,11 @@ class GradientPipeline:
                     yield self._ordered_op(half, bk, sh, b)
                 if timer:
                     timer(f"pass1_{b}")
-                plan.pass1(sh, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
+                if p1s is not s0:
+                    p1s.wait_stream(s0)
+                plan.pass1(sh1, g_is_f16=self.f16, chunk0=bk.chunk0, nchunk=bk.nchunk)
+            if p1s is not s0:
+                s0.wait_stream(p1s)
             if ps is not s0:
                 s0.wait_stream(ps)
             if self.ordered is not None:

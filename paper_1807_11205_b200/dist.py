@@ -207,7 +207,7 @@ class OrderedWire:
         dist.barrier()
 
     #: inbox slot capacity (binary16 elements) for the small-bucket kernels
-    SMALL_CAP_ELEMS = 1 << 17
+    SMALL_CAP_ELEMS = 1 << 18
     #: buckets up to this many elements take the one-shot kernel
     #: (gs_oneshot_allreduce_f16: one barrier, (p-1) x S bytes out).
     #: Measured at p = 4 (profiles/r02/y_n4, aa_n4): 13.1-14.3 µs up to 8 KB
@@ -216,10 +216,12 @@ class OrderedWire:
     ONESHOT_MAX_ELEMS = 4096
     #: buckets up to this many elements take the LL kernel when whole
     #: 8-element vectors (gs_ll_allreduce_f16: no fence, no barrier).
-    #: Measured at p = 4 (profiles/r02/ii_n4): 9.0-12.7 µs up to 256 KB,
-    #: 15.5 µs at 512 KB, vs NCCL ring 15.2-17.4 and the push form 16.4-24.1;
-    #: at 1 MB its doubled bytes lose (32.5 vs 19.2 NCCL, 24.7 push)
-    LL_MAX_ELEMS = 1 << 17
+    #: Measured at p = 4 (profiles/r02/ii_n4, fp16 bytes): 9.0-12.7 µs up to
+    #: 128 KB, 15.5 µs at 256 KB and 20.9 µs at 512 KB vs NCCL ring 15.2-17.4
+    #: and the push form 16.4-25.2; at 1 MB its doubled bytes lose (32.5 vs
+    #: 24.7 push).  512 KB rather than 256 KB: a θ = 256 KiB bucket closes just
+    #: above θ and would otherwise miss the LL form
+    LL_MAX_ELEMS = 1 << 18
 
     @staticmethod
     def oneshot_cap(total: int, itemsize: int) -> int:

@@ -280,6 +280,17 @@ class OrderedWire:
     #: slots still pair up)
     MIN_ELEMS_PER_CTA = 16384
 
+    #: buckets up to this many bytes take the push form at p >= 4 even on a
+    #: pull wire: p = 4 sweeps (r2ii, r2tt, r2ac) put it 2-4 µs ahead from
+    #: 128 KB to 2 MB, even from 4 MB on; at p = 2 neither form leads there
+    #: (r2t).  fp16 wire only (measured there).  Same fold order,
+    #: bit-identical; 0 disables
+    PUSH_MAX_BYTES = 2 << 20
+
+    def push_for(self, n: int) -> bool:
+        return self.push or (self.p >= 4 and self.itemsize == 2
+                             and n * 2 <= OrderedWire.PUSH_MAX_BYTES)
+
     def grid_for(self, n: int) -> int:
         return max(1, min(self.nblocks, -(-int(n) // self.MIN_ELEMS_PER_CTA)))
 
@@ -321,7 +332,7 @@ class OrderedWire:
         return PeerOp("gs_ordered_allreduce_f16" if self.itemsize == 2 else
                       "gs_ordered_allreduce_f32", self.ctx,
                       (self.p, dev.ptr(self.bufs_dev[half]), dev.ptr(self.sig_dev), offset, n,
-                       slot + 1, self.grid_for(n), 1 if self.push else 0, stream_h),
+                       slot + 1, self.grid_for(n), 1 if self.push_for(n) else 0, stream_h),
                       device=self.device)
 
     def hier_op(self, half: int, offset: int, n: int, k: int, stream_h: int, slot: int = 0):

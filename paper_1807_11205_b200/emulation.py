@@ -103,6 +103,7 @@ class LocalOrderedWire:
     sig_bytes = staticmethod(_OW.sig_bytes)
     _setup = _OW._setup
     grid_for = _OW.grid_for
+    push_for = _OW.push_for
     allreduce_op = _OW.allreduce_op
     hier_op = _OW.hier_op
     allreduce = _OW.allreduce

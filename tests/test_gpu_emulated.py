@@ -19,6 +19,7 @@ import paper_1807_11205_b200 as gs
 from paper_1807_11205_b200 import _device as dev
 from paper_1807_11205_b200 import _native, shapes as sh
 from paper_1807_11205_b200._peer import PeerOp, PeerTimeoutError, launch, rank_ctx
+from paper_1807_11205_b200.dist import OrderedWire
 from paper_1807_11205_b200.emulation import LocalWorld
 
 pytestmark = pytest.mark.gpu
@@ -59,6 +60,9 @@ def test_ordered_allreduce_bit_exact(p, form, monkeypatch):
     world = LocalWorld(gs.Topology(p, 1), d, peer_ctas=8, timeout_s=20.0)
     total = 1 << 16
     push = form == "push"
+    if form == "pull":
+        # keep the pull kernel on every bucket (no size rule)
+        monkeypatch.setattr(OrderedWire, "PUSH_MAX_BYTES", 0)
     wires = [c.make_ordered_wire(total, d, push=push) for c in world.comms]
     rng = np.random.default_rng(100 + p)
     sh_ = torch.cuda.current_stream().cuda_stream

@@ -85,3 +85,19 @@ def test_small_bucket_rule():
     assert rule(w, 0, 0) == "none"
     assert OrderedWire.oneshot_cap(1 << 20, 4) == 0
     assert rule(SimpleNamespace(cap=0), 0, 8) == "none"
+
+
+def test_push_form_rule():
+    """Pull wires at p >= 4 take the push kernel for fp16 buckets up to
+    PUSH_MAX_BYTES (host only)."""
+    from types import SimpleNamespace
+
+    from paper_1807_11205_b200.dist import OrderedWire
+
+    rule = OrderedWire.push_for
+    lim = OrderedWire.PUSH_MAX_BYTES // 2
+    assert rule(SimpleNamespace(push=False, p=4, itemsize=2), lim)
+    assert not rule(SimpleNamespace(push=False, p=4, itemsize=2), lim + 1)
+    assert not rule(SimpleNamespace(push=False, p=2, itemsize=2), 8)
+    assert not rule(SimpleNamespace(push=False, p=8, itemsize=4), 8)
+    assert rule(SimpleNamespace(push=True, p=2, itemsize=4), 1 << 30)

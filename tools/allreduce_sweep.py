@@ -95,6 +95,7 @@ def main() -> None:
     buf = torch.empty_like(base)
     # small-bucket inboxes up to 2 MB buckets, so the sweep shows the crossover
     OrderedWire.SMALL_CAP_ELEMS = 1 << 20
+    OrderedWire.PUSH_MAX_BYTES = 0  # "ordered" is the pure pull form here
     ow = OrderedWire(comms[1], max_elems, dev) if any(v[0].startswith("ordered") for v in variants) \
         else None
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
